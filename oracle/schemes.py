@@ -1,0 +1,111 @@
+"""Lie / Strang splitting compositions and the time-stepping loop (oracle; test infra only).
+
+Composition names follow the paper's figure legends ("we identify the methods ... by
+in which order the subproblems are solved"): F1F2, F12, F12F3, F1F2F3, F1F3F2, F12F4,
+F1F2F4, F1F4F2, F12F3F4, plus the four-term F1F2F3F4 (beyond the paper, reading G19).
+
+Lie:  apply the listed flows in order, each over h (reading G5).
+Strang: flows f1..fm applied as
+        f1(h/2) ... f_{m-1}(h/2) f_m(h) f_{m-1}(h/2) ... f1(h/2);  m = 1 -> f1(h).
+T4 uses the midpoint rule under Strang and explicit Euler under Lie (reading G4).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import flows, lowrank, quadrature
+
+COMPOSITIONS = {
+    "F1F2": ["T1", "T2"], "F12": ["T12"], "F12F3": ["T12", "T3"],
+    "F1F2F3": ["T1", "T2", "T3"], "F1F3F2": ["T1", "T3", "T2"],
+    "F12F4": ["T12", "T4"], "F1F2F4": ["T1", "T2", "T4"], "F1F4F2": ["T1", "T4", "T2"],
+    "F12F3F4": ["T12", "T3", "T4"], "F1F2F3F4": ["T1", "T2", "T3", "T4"],
+}
+
+
+def step_sequence(scheme, composition, h):
+    """[(flow, tau), ...] in application order for one step."""
+    fl = COMPOSITIONS[composition]
+    if scheme == "lie":
+        return [(f, h) for f in fl]
+    if scheme != "strang":
+        raise ValueError(scheme)
+    if len(fl) == 1:
+        return [(fl[0], h)]
+    half = [(f, h / 2) for f in fl[:-1]]
+    return half + [(fl[-1], h)] + half[::-1]
+
+
+@dataclass
+class OracleOptions:
+    tol: float = 1e-16
+    rank_cap: int | None = None
+    quad_nodes: int = 14
+    quad_subpanels: int = 1
+
+
+class OracleSolver:
+    """Runs a splitting scheme on a workloads.Problem in LDL^T form."""
+
+    def __init__(self, prob, h, opts=OracleOptions(), method="auto"):
+        self.p = prob
+        self.h = h
+        self.o = opts
+        self.op = flows.Operator(prob.A, method, prob.heat_nx, prob.heat_dim)
+        n = prob.n
+        if prob.C is not None and prob.C.shape[0] > 0:
+            self.LQ, self.DQ = prob.C.T.copy(), np.eye(prob.C.shape[0])   # Q = C^T C (G11)
+        else:
+            self.LQ, self.DQ = np.zeros((n, 0)), np.zeros((0, 0))
+        self.delta = quadrature.panel_width(prob.A, h, opts.quad_subpanels)
+        self._LI = {}
+        # P0 is compressed when loaded (reading G10)
+        L0 = prob.L0 if prob.L0 is not None else np.zeros((n, 0))
+        D0 = prob.D0 if prob.D0 is not None else np.zeros((0, 0))
+        self.L, self.D = lowrank.column_compression(L0, D0, opts.tol, opts.rank_cap)
+        self.t = 0.0
+
+    def integral(self, tau):
+        key = round(tau / self.delta)
+        if key not in self._LI:
+            self._LI[key] = flows.build_integral(self.op, tau, self.delta, self.o.quad_nodes,
+                                                 self.LQ, self.DQ, self.o.tol, self.o.rank_cap)
+        return self._LI[key]
+
+    def apply_flow(self, f, tau, order=2):
+        o, p = self.o, self.p
+        if f == "T1":
+            self.L, self.D = flows.T1(self.op, tau, self.L, self.D)
+        elif f == "T2":
+            self.L, self.D = flows.T2(tau, self.L, self.D, self.LQ, self.DQ, o.tol, o.rank_cap)
+        elif f == "T3":
+            self.L, self.D = flows.T3(tau, self.L, self.D, p.B, p.R)
+        elif f == "T4":
+            self.L, self.D = flows.T4(tau, self.L, self.D, p.S, order, o.tol, o.rank_cap)
+        elif f == "T12":
+            LI, DI = self.integral(tau)
+            self.L, self.D = flows.T12(self.op, tau, self.L, self.D, LI, DI, o.tol, o.rank_cap)
+        else:
+            raise ValueError(f)
+
+    def step(self, scheme, composition, nsteps=1):
+        seq = step_sequence(scheme, composition, self.h)
+        order = 2 if scheme == "strang" else 1
+        for _ in range(nsteps):
+            for f, tau in seq:
+                self.apply_flow(f, tau, order)
+            self.t += self.h
+        return self.L, self.D
+
+    def factor(self):
+        """Canonical (L, D): compressed, L orthonormal, D diagonal sorted by |.| desc."""
+        return lowrank.column_compression(self.L, self.D, self.o.tol, None)
+
+
+def integrate(prob, scheme, composition, nsteps, T=None, opts=OracleOptions(), method="auto"):
+    T = prob.T if T is None else T
+    s = OracleSolver(prob, T / nsteps, opts, method)
+    s.step(scheme, composition, nsteps)
+    return s

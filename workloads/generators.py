@@ -1,0 +1,185 @@
+"""Problem generators (problem data only; no method arithmetic).
+
+Readings of the paper used here (all listed in DESIGN.md §Readings):
+  * G13  FD scaling: n_x interior points per direction, dx = 1/(n_x+1),
+         A = (n_x+1)^2 (T (x) I + I (x) T), T = tridiag(1,-2,1)   ("central second-order
+         finite differences with n_x grid points").
+  * G12  "randomly chosen" factors = uniform [0,1] entries (MATLAB `rand`), D = I,
+         numpy PCG64 with seed 1000*config + role (1=C, 2=L0, 3=B, 4=S).
+  * G17  convection-diffusion for config 3: A = Lap - 10 xi1 d/dxi1 - 100 xi2 d/dxi2, central FD.
+  * G18  Example 2: Dirichlet on x=0 and y=0, control edge x=1 (x=u), stochastic
+         Robin edge y=1 (n.grad x = 0.5(0.5 + dW) x) by a one-sided ghost-node elimination:
+         A gets +0.25/dx on the y=1 row, S = diag(0.5/dx) on the y=1 row, B = (n_x+1)^2 on the
+         x=1 column; C = (1/n)(1,...,1) (Q = C^T C, reading G11), P0 = 0.
+All matrices are float64, C-contiguous numpy arrays; A is returned DENSE because the
+north star's boundary takes a dense A (BASELINE.json north_star: "dle_init/dre_init with A").
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+
+@dataclass
+class Problem:
+    """One differential matrix equation  P' = A^T P + P A + Q [+ S P S^T] [- P B R^-1 B^T P].
+
+    Q = C^T C (C is p x n), P(0) = L0 D0 L0^T.  B, R, S optional (None).
+    `heat_nx` / `heat_dim` are structure hints (the operator is the Dirichlet FD Laplacian)
+    that let test code use the closed-form sine eigenbasis; they carry no arithmetic.
+    """
+    A: np.ndarray
+    C: Optional[np.ndarray]
+    L0: Optional[np.ndarray]
+    D0: Optional[np.ndarray]
+    B: Optional[np.ndarray] = None
+    R: Optional[np.ndarray] = None
+    S: Optional[np.ndarray] = None
+    T: float = 0.5
+    name: str = ""
+    heat_nx: Optional[int] = None
+    heat_dim: Optional[int] = None
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n(self) -> int:
+        return self.A.shape[0]
+
+    @property
+    def is_dre(self) -> bool:
+        return self.B is not None
+
+
+def _tridiag(n: int) -> np.ndarray:
+    T = np.zeros((n, n))
+    i = np.arange(n)
+    T[i, i] = -2.0
+    T[i[:-1], i[:-1] + 1] = 1.0
+    T[i[1:], i[1:] - 1] = 1.0
+    return T
+
+
+def heat1d_matrix(n: int) -> np.ndarray:
+    """1D Dirichlet Laplacian on (0,1), n interior points, dx = 1/(n+1)."""
+    return (n + 1) ** 2 * _tridiag(n)
+
+
+def heat2d_matrix(nx: int) -> np.ndarray:
+    """2D Dirichlet Laplacian on the unit square, nx^2 unknowns."""
+    T = _tridiag(nx)
+    I = np.eye(nx)
+    return (nx + 1) ** 2 * (np.kron(T, I) + np.kron(I, T))
+
+
+def convdiff2d_matrix(nx: int, c1: float = 10.0, c2: float = 100.0) -> np.ndarray:
+    """A = Lap - c1*xi1*d/dxi1 - c2*xi2*d/dxi2, central differences (reading G17).
+
+    Unknown ordering: index = i*nx + j with xi1 = (i+1)dx, xi2 = (j+1)dx.
+    """
+    n = nx * nx
+    dx = 1.0 / (nx + 1)
+    A = heat2d_matrix(nx)
+    for i in range(nx):
+        for j in range(nx):
+            k = i * nx + j
+            x1, x2 = (i + 1) * dx, (j + 1) * dx
+            if i + 1 < nx:
+                A[k, k + nx] -= c1 * x1 / (2 * dx)
+            if i - 1 >= 0:
+                A[k, k - nx] += c1 * x1 / (2 * dx)
+            if j + 1 < nx:
+                A[k, k + 1] -= c2 * x2 / (2 * dx)
+            if j - 1 >= 0:
+                A[k, k - 1] += c2 * x2 / (2 * dx)
+    assert A.shape == (n, n)
+    return A
+
+
+def stochastic_heat_matrices(nx: int):
+    """Example 2 structure (reading G18). Returns (A, B, S, C)."""
+    n = nx * nx
+    dx = 1.0 / (nx + 1)
+    A = heat2d_matrix(nx)
+    S = np.zeros((n, n))
+    B = np.zeros((n, 1))
+    for i in range(nx):          # i: x-index, j: y-index, index = i*nx + j
+        for j in range(nx):
+            k = i * nx + j
+            if j == nx - 1:      # Robin edge y = 1
+                A[k, k] += 0.25 / dx
+                S[k, k] = 0.5 / dx
+            if i == nx - 1:      # control edge x = 1: boundary value u enters the stencil
+                B[k, 0] = (nx + 1) ** 2
+    C = np.full((1, n), 1.0 / n)
+    return A, B, S, C
+
+
+def _rng(config: int, role: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(1000 * config + role))
+
+
+def uniform_factor(config: int, role: int, rows: int, cols: int) -> np.ndarray:
+    return _rng(config, role).random((rows, cols))
+
+
+# BASELINE.json configs (index 1..5), with the survey's §8(d) recipe.
+CONFIGS = {
+    1: dict(desc="DLE 1D heat n=100, C rank-1, Lie F1F2, T=0.1, 100 steps", kind="heat1d", n=100,
+            p=1, r0=5, m=0, T=0.1, nsteps=100, scheme="lie", composition="F1F2"),
+    2: dict(desc="DLE 2D heat n=1024, Strang F1F2 and F12 with 5-node Gauss", kind="heat2d", nx=32,
+            p=1, r0=5, m=0, T=0.5, nsteps=100, scheme="strang", composition="F12",
+            quad_nodes=5, quad_subpanels=4),
+    3: dict(desc="DRE 2D convection-diffusion n=2500, Strang F12F3", kind="convdiff2d", nx=50,
+            p=2, r0=5, m=1, T=0.5, nsteps=100, scheme="strang", composition="F12F3"),
+    4: dict(desc="generalized DRE (S P S^T) n=4900, Lie/Strang F12F3F4 and F1F2F3F4",
+            kind="stochastic", nx=70, p=1, r0=0, m=1, T=0.5, nsteps=100, scheme="strang",
+            composition="F12F3F4"),
+    5: dict(desc="DRE 2D heat n=10000 FP64, rank cap 64, Strang F12F3", kind="heat2d", nx=100,
+            p=2, r0=5, m=1, T=0.5, nsteps=100, scheme="strang", composition="F12F3",
+            rank_cap=64),
+}
+
+
+def make_config(config: int, nx: Optional[int] = None, n: Optional[int] = None,
+                rinv: float = 1.0, dle: bool = False) -> Problem:
+    """Build the problem of BASELINE.json config `config` (optionally at a smaller size).
+
+    `nx`/`n` override the size (same recipe, e.g. the n=25 verification problems of P:L370).
+    `rinv` sets R = (1/rinv) I (P:L384 uses R^-1 in {1, 1e-3}). `dle=True` drops B.
+    """
+    c = dict(CONFIGS[config])
+    kind = c["kind"]
+    heat_nx = heat_dim = None
+    S = None
+    if kind == "heat1d":
+        nn = n or c["n"]
+        A = heat1d_matrix(nn)
+        heat_nx, heat_dim = nn, 1
+    elif kind == "heat2d":
+        nxx = nx or c["nx"]
+        A = heat2d_matrix(nxx)
+        heat_nx, heat_dim = nxx, 2
+    elif kind == "convdiff2d":
+        nxx = nx or c["nx"]
+        A = convdiff2d_matrix(nxx)
+    elif kind == "stochastic":
+        nxx = nx or c["nx"]
+        A, Bs, S, Cs = stochastic_heat_matrices(nxx)
+    else:
+        raise ValueError(kind)
+    N = A.shape[0]
+    if kind == "stochastic":
+        C = Cs
+        B = None if dle else Bs
+    else:
+        C = uniform_factor(config, 1, c["p"], N)
+        B = None if (dle or c["m"] == 0) else uniform_factor(config, 3, N, c["m"])
+    r0 = c["r0"]
+    L0 = uniform_factor(config, 2, N, r0) if r0 > 0 else np.zeros((N, 0))
+    D0 = np.eye(r0)
+    R = None if B is None else np.eye(B.shape[1]) / rinv
+    return Problem(A=np.ascontiguousarray(A), C=C, L0=L0, D0=D0, B=B, R=R, S=S, T=c["T"],
+                   name=f"config{config}", heat_nx=heat_nx, heat_dim=heat_dim,
+                   meta=dict(c, config=config))
