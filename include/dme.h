@@ -1,0 +1,165 @@
+/*
+ * dme.h — C ABI of the B200 hot path for low-rank splitting schemes on (generalized) differential
+ * Lyapunov and Riccati equations (Mena, Pfurtscheller, Stillfjord, arXiv 1805.08990).
+ *
+ *   P' = A^T P + P A + Q [+ S P S^T] [- P B R^{-1} B^T P],   P(0) = P0,   Q = C^T C     (PAPER §1, §2)
+ *
+ * The solution is kept in low-rank form P = L D L^T. Each step applies Lie / Strang
+ * compositions of the sub-flows
+ *   T1  linear      L <- exp(tau A^T) L                                  eq:F_sol_LDL
+ *   T2  constant    [L, L_Q], blkdiag(D, tau D_Q)
+ *   T12 affine      [exp(tau A^T) L, L_I(tau)], blkdiag(D, D_I)          eq:full P:L129, Alg. 2
+ *   T3  Riccati     D <- (I + tau D L^T B R^-1 B^T L)^-1 D               eq:nonlinear P:L152-156, Alg. 3
+ *   T4  bilinear    [L, sqrt(tau) S L, tau/sqrt(2) S^2 L], blkdiag(D,D,D) P:L170-180, Alg. 4
+ * with column compression after every rank-growing flow. exp(tau A^T) is a dense FP64
+ * matrix computed once at init by scaling-and-squaring Padé-13 (BASELINE.json north_star); L_I is
+ * the composite Gauss-Legendre quadrature factor of the integral term (reading G6 in DESIGN.md).
+ *
+ * Conventions
+ *  - All matrices are FP64, HOST pointers, ROW-MAJOR (C order): element (i, j) of an r x c matrix
+ *    X is X[i*c + j]. Inputs are copied at init; the caller keeps ownership and may free them.
+ *  - Device memory: the library carves everything out of ONE caller-owned device buffer
+ *    (options.workspace, options.workspace_bytes >= dme_workspace_size(...)); it never calls
+ *    cudaMalloc on the hot path. Work is enqueued on options.stream (cudaStream_t, NULL = legacy).
+ *  - Errors: every call returns a dme_status; no call aborts or throws across the ABI.
+ *    dme_last_error() returns a thread-local description of the last failure.
+ *    Validation failures leave the context unchanged; CUDA/NCCL failures poison it
+ *    (every later call returns DME_ERR_POISONED).
+ *  - A context is not thread-safe; separate contexts are independent.
+ *  - Multi-GPU (world_size > 1): one process per GPU; rows of exp(tau A^T) are sharded over the
+ *    ranks and the updated factor is all-gathered (NCCL) after every T1/T12 action. dme_split_step
+ *    is collective. The small systems are replicated, so dme_get_factor works on every rank.
+ */
+#ifndef DME_H
+#define DME_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dme_ctx dme_ctx; /* opaque, owned by the library */
+
+typedef enum {
+  DME_OK = 0,
+  DME_ERR_INVALID = 1,  /* NULL pointer, n <= 0, non-finite input, R not SPD, D0 not PSD, h <= 0 */
+  DME_ERR_DIM = 2,      /* inconsistent sizes (e.g. m > 8, rank bound above the small-system limit) */
+  DME_ERR_CONFIG = 3,   /* composition needs data the problem lacks (F3 without B, F4 without S),
+                           unknown scheme / composition / flow, tau not in {h/2, h} */
+  DME_ERR_SINGULAR = 4, /* a small linear system is singular */
+  DME_ERR_NUMERIC = 5,  /* non-finite result, expm overflow, Padé denominator pivot too small */
+  DME_ERR_CAPACITY = 6, /* caller buffer too small (get_factor) or workspace too small */
+  DME_ERR_CUDA = 7,
+  DME_ERR_NCCL = 8,
+  DME_ERR_NOMEM = 9,
+  DME_ERR_POISONED = 10
+} dme_status;
+
+typedef enum { DME_LIE = 0, DME_STRANG = 1 } dme_scheme;
+
+/* Figure-legend names of the paper: order in which the sub-problems are solved. */
+typedef enum {
+  DME_F1F2 = 0,     /* DLE splitting, Alg. 1                                 */
+  DME_F12 = 1,      /* DLE quadrature, Alg. 2                                */
+  DME_F12F3 = 2,    /* DRE two-term: T12(h/2) T3(h) T12(h/2)            */
+  DME_F1F2F3 = 3,   /* DRE three-term: T1 T2 T3 T2 T1            */
+  DME_F1F3F2 = 4,   /* DRE three-term reversed: T1 T3 T2 T3 T1            */
+  DME_F12F4 = 5,    /* generalized DLE, T3 replaced by T4            */
+  DME_F1F2F4 = 6,
+  DME_F1F4F2 = 7,
+  DME_F12F3F4 = 8,  /* generalized DRE: T12(h/2) T3(h/2) T4(h) T3(h/2) T12(h/2)   */
+  DME_F1F2F3F4 = 9  /* four-term splitting (beyond the paper; reading G19)         */
+} dme_composition;
+
+typedef struct {
+  int64_t n;          /* state dimension                                                    */
+  const double* A;    /* n x n                                                              */
+  int64_t p;          /* rows of C (p >= 0); Q = C^T C                                      */
+  const double* C;    /* p x n (NULL iff p == 0)                                            */
+  int64_t m;          /* columns of B; 0 for a DLE                                          */
+  const double* B;    /* n x m                                                              */
+  const double* R;    /* m x m, symmetric positive definite                                 */
+  const double* S;    /* n x n or NULL (generalized equations)                              */
+  int64_t r0;         /* columns of L0 (0 => P0 = 0)                                        */
+  const double* L0;   /* n x r0                                                             */
+  const double* D0;   /* r0 x r0 symmetric positive semidefinite (NULL => identity)         */
+} dme_problem;
+
+typedef struct {
+  double h;               /* step size; E_{h/2}, E_h and L_I(h/2), L_I(h) are built at init    */
+  double trunc_tol;       /* relative truncation tolerance of the compression (default 1e-16)  */
+  int32_t rank_cap;       /* maximum rank kept by a compression (0 = no cap)                   */
+  int32_t quad_nodes;     /* Gauss-Legendre nodes per panel (default 14)               */
+  int32_t quad_subpanels; /* P0 >= 1, power of two: panels per Padé scaling step (default 1)   */
+  int32_t device;         /* CUDA device ordinal                                               */
+  void* stream;           /* cudaStream_t (NULL = legacy default stream)                       */
+  int32_t world_size;     /* ranks (1 = single GPU)                                            */
+  int32_t world_rank;
+  const void* nccl_uid;   /* 128-byte ncclUniqueId from dme_get_unique_id on rank 0           */
+  void* workspace;        /* device buffer, >= dme_workspace_size bytes, 256-byte aligned     */
+  size_t workspace_bytes;
+} dme_options;
+
+typedef struct {
+  double t;                 /* integrated time (steps * h)                                     */
+  int64_t steps;            /* completed steps                                                 */
+  int64_t rank;             /* current rank of the factor                                      */
+  int64_t max_rank;         /* largest rank seen after a compression                           */
+  int64_t q_half, q_full;   /* ranks of L_I(h/2), L_I(h)                                       */
+  int32_t squarings;        /* s: Padé-13 scaling exponent of (h/2) A^T                        */
+  int32_t quad_panels;      /* panels of the composite rule on [0, h/2]                        */
+  double panel_width;       /* delta = (h/2) / panels                                          */
+  double pade_min_pivot;    /* smallest |u_ii| of the Padé denominator factorisation           */
+  double last_drop;         /* largest discarded pivot / max diag of the last compression      */
+  int64_t e_passes;         /* number of E*L actions (T1/T12/T4 passes)                        */
+  int64_t compressions;
+  double init_seconds;      /* host wall time of the init call                                 */
+} dme_stats;
+
+void dme_default_options(dme_options* opt);
+const char* dme_status_string(dme_status s);
+const char* dme_last_error(void);
+
+/* Bytes of device workspace needed for this problem/options. */
+dme_status dme_workspace_size(const dme_problem* prob, const dme_options* opt, size_t* bytes);
+/* 128-byte NCCL unique id (rank 0 calls it and broadcasts the bytes). */
+dme_status dme_get_unique_id(void* uid128);
+
+/* Build the context: upload, Padé-13 expm of (h/2)A^T and its square, quadrature factors,
+ * compression of P0. dle_init requires m == 0; dre_init requires m >= 1. Collective. */
+dme_status dme_dle_init(const dme_problem* prob, const dme_options* opt, dme_ctx** ctx);
+dme_status dme_dre_init(const dme_problem* prob, const dme_options* opt, dme_ctx** ctx);
+
+/* Advance nsteps steps of the composition (collective when world_size > 1). */
+dme_status dme_split_step(dme_ctx* ctx, dme_scheme scheme, dme_composition comp, int64_t nsteps);
+
+/* Copy the factor to the host: *r <- rank; if L != NULL, L (n x r) and, if D != NULL, D (r x r)
+ * with P = L D L^T. Returns DME_ERR_CAPACITY (and sets *r) when r > capacity_cols. */
+dme_status dme_get_factor(dme_ctx* ctx, int64_t* r, double* L, double* D, int64_t capacity_cols);
+dme_status dme_get_stats(dme_ctx* ctx, dme_stats* st);
+dme_status dme_destroy(dme_ctx* ctx);
+
+/* ---- test hooks (same semantics as the step, one flow at a time) ----------------------------- */
+typedef enum {
+  DME_FLOW_T1 = 0, DME_FLOW_T2 = 1, DME_FLOW_T3 = 2, DME_FLOW_T4_MIDPOINT = 3,
+  DME_FLOW_T4_EULER = 4, DME_FLOW_T12 = 5, DME_FLOW_COMPRESS = 6
+} dme_flow;
+/* Apply one flow over tau (T1/T12: tau must be h/2 or h). */
+dme_status dme_debug_apply(dme_ctx* ctx, int32_t flow, double tau);
+/* Replace the state by P = L L^T (L: n x r host, row-major; no compression). */
+dme_status dme_debug_set_factor(dme_ctx* ctx, int64_t r, const double* L);
+/* Copy E_{h/2} (which = 0) or E_h (which = 1) to the host (n x n). */
+dme_status dme_debug_get_exp(dme_ctx* ctx, int32_t which, double* E);
+/* Copy L_I(h/2) (which = 0) or L_I(h) (which = 1), P_I = L_I L_I^T, n x q, to the host. */
+dme_status dme_debug_get_integral(dme_ctx* ctx, int32_t which, int64_t* q, double* L,
+                                  int64_t capacity_cols);
+/* C (M x N) = A (M x K) * B (K x N) through the library's DMMA GEMM (host buffers). */
+dme_status dme_debug_matmul(int64_t M, int64_t N, int64_t K, const double* A, const double* B,
+                            double* C);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DME_H */

@@ -1,0 +1,210 @@
+// Element-wise / reduction / tall-times-small kernels of the DME path.
+#include "aux.h"
+#include "common.cuh"
+
+namespace dme {
+
+namespace {
+
+// out = alpha * A^T  (n x n, row-major with leading dims lda / ldo), 32x32 smem tiles
+__global__ void transpose_scale_kernel(const double* __restrict__ A, int64_t n, int64_t lda,
+                                       double alpha, double* __restrict__ out, int64_t ldo) {
+  __shared__ double tile[32][33];
+  const int64_t bx = (int64_t)blockIdx.x * 32, by = (int64_t)blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int64_t r = by + j, c = bx + threadIdx.x;
+    if (r < n && c < n) tile[j][threadIdx.x] = A[r * lda + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int64_t r = bx + j, c = by + threadIdx.x;
+    if (r < n && c < n) out[r * ldo + c] = alpha * tile[threadIdx.x][j];
+  }
+}
+
+// partial[b] = max over the rows handled by block b of sum_j |A_ij|
+__global__ void rowabs_max_kernel(const double* __restrict__ A, int64_t n, int64_t lda,
+                                  double* __restrict__ partial) {
+  __shared__ double red[32];
+  double best = 0.0;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) s += fabs(A[i * lda + j]);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      best = fmax(best, t);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = best;
+}
+
+__global__ void max_reduce_kernel(const double* __restrict__ partial, int cnt, double* out) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) v = fmax(v, partial[i]);
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+    *out = t;
+  }
+}
+
+__global__ void lincomb_kernel(double* __restrict__ out, int64_t n, int64_t ld, LinTerm t0,
+                               LinTerm t1, LinTerm t2, LinTerm t3, double diag) {
+  const int64_t total = n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    const int64_t o = i * ld + j;
+    double v = (i == j) ? diag : 0.0;
+    if (t0.X) v += t0.c * t0.X[o];
+    if (t1.X) v += t1.c * t1.X[o];
+    if (t2.X) v += t2.c * t2.X[o];
+    if (t3.X) v += t3.c * t3.X[o];
+    out[o] = v;
+  }
+}
+
+__global__ void copy_cols_kernel(double* __restrict__ dst, int64_t ldd, const double* __restrict__ src,
+                                 int64_t lds, int64_t rows, int64_t cols, double alpha) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    dst[i + j * ldd] = alpha * src[i + j * lds];
+  }
+}
+
+// dst (rows x cols, col-major ldd) = alpha * src^T  where src is cols x rows row-major (lds)
+__global__ void rowmajor_to_colmajor_kernel(double* __restrict__ dst, int64_t ldd,
+                                            const double* __restrict__ src, int64_t lds,
+                                            int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    dst[i + j * ldd] = src[i * lds + j];
+  }
+}
+
+// C (M x N, col-major ldc) = A (M x K, col-major lda) * B (K x N, col-major ldb); K, N small.
+// One CTA owns a 128-row block and all N columns (N <= 64 per launch slice), so C may alias A
+// when N <= the columns read (row-local: the whole K loop completes before the epilogue).
+constexpr int TS_BM = 128, TS_BN = 64, TS_BK = 16;
+__global__ void __launch_bounds__(256) tall_small_kernel(const double* A, int64_t lda,
+                                                         const double* __restrict__ B, int64_t ldb,
+                                                         double* C, int64_t ldc, int64_t M,
+                                                         int64_t N, int64_t K) {
+  __shared__ double sA[TS_BK][TS_BM + 4];
+  __shared__ double sB[TS_BN][TS_BK + 4];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % 4, wn = warp / 4;  // warp tile 32 x 32
+  const int64_t m0 = (int64_t)blockIdx.x * TS_BM;
+  const int64_t n0 = (int64_t)blockIdx.y * TS_BN;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int64_t k0 = 0; k0 < K; k0 += TS_BK) {
+    for (int e = tid; e < TS_BK * TS_BM; e += 256) {
+      const int kk = e / TS_BM, mm = e % TS_BM;
+      const int64_t gm = m0 + mm, gk = k0 + kk;
+      sA[kk][mm] = (gm < M && gk < K) ? A[gm + gk * lda] : 0.0;
+    }
+    for (int e = tid; e < TS_BN * TS_BK; e += 256) {
+      const int nn = e / TS_BK, kk = e % TS_BK;
+      const int64_t gn = n0 + nn, gk = k0 + kk;
+      sB[nn][kk] = (gn < N && gk < K) ? B[gk + gn * ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < TS_BK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) af[a] = sA[ks + t][wm * 32 + a * 8 + g];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = sB[wn * 32 + b * 8 + g][ks + t];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t row = m0 + wm * 32 + a * 8 + g;
+        const int64_t col = n0 + wn * 32 + b * 8 + t * 2 + e;
+        if (row < M && col < N) C[row + col * ldc] = acc[a][b][e];
+      }
+}
+
+inline int grid_for(int64_t total, int threads = 256) {
+  int64_t b = (total + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+
+void transpose_scale(const double* A, int64_t n, int64_t lda, double alpha, double* out,
+                     int64_t ldo, cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
+  transpose_scale_kernel<<<grid, dim3(32, 8), 0, st>>>(A, n, lda, alpha, out, ldo);
+  DME_KCHECK();
+}
+
+void rowabs_max(const double* A, int64_t n, int64_t lda, double* scratch, double* out,
+                cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>(n, 1024);
+  rowabs_max_kernel<<<blocks, 256, 0, st>>>(A, n, lda, scratch);
+  DME_KCHECK();
+  max_reduce_kernel<<<1, 1024, 0, st>>>(scratch, blocks, out);
+  DME_KCHECK();
+}
+
+void lincomb(double* out, int64_t n, int64_t ld, LinTerm t0, LinTerm t1, LinTerm t2, LinTerm t3,
+             double diag, cudaStream_t st) {
+  lincomb_kernel<<<grid_for(n * n), 256, 0, st>>>(out, n, ld, t0, t1, t2, t3, diag);
+  DME_KCHECK();
+}
+
+void copy_cols(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+               int64_t cols, double alpha, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  copy_cols_kernel<<<grid_for(rows * cols), 256, 0, st>>>(dst, ldd, src, lds, rows, cols, alpha);
+  DME_KCHECK();
+}
+
+void rowmajor_to_colmajor(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                          int64_t cols, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  rowmajor_to_colmajor_kernel<<<grid_for(rows * cols), 256, 0, st>>>(dst, ldd, src, lds, rows, cols);
+  DME_KCHECK();
+}
+
+void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                int64_t M, int64_t N, int64_t K, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  if (K <= 0) throw std::runtime_error("tall_small: K must be positive");
+  if (C == A && N > TS_BN) throw std::runtime_error("tall_small: in place needs N <= 64");
+  dim3 grid((unsigned)ceil_div(M, TS_BM), (unsigned)ceil_div(N, TS_BN));
+  tall_small_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K);
+  DME_KCHECK();
+}
+
+}  // namespace dme

@@ -1,0 +1,31 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace dme {
+
+struct LinTerm {
+  double c = 0.0;
+  const double* X = nullptr;
+};
+
+// out = alpha * A^T (n x n row-major)
+void transpose_scale(const double* A, int64_t n, int64_t lda, double alpha, double* out,
+                     int64_t ldo, cudaStream_t st);
+// *out = max_i sum_j |A_ij|  (= ||A^T||_1); scratch >= 1024 doubles
+void rowabs_max(const double* A, int64_t n, int64_t lda, double* scratch, double* out,
+                cudaStream_t st);
+// out = sum_i c_i X_i + diag * I   (n x n, shared leading dim)
+void lincomb(double* out, int64_t n, int64_t ld, LinTerm t0, LinTerm t1, LinTerm t2, LinTerm t3,
+             double diag, cudaStream_t st);
+// dst[:, j] = alpha * src[:, j], column-major
+void copy_cols(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+               int64_t cols, double alpha, cudaStream_t st);
+// dst (rows x cols column-major) <- src (rows x cols row-major)
+void rowmajor_to_colmajor(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                          int64_t cols, cudaStream_t st);
+// C = A * B, A: M x K column-major, B: K x N column-major (small K, N), C: column-major
+void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                int64_t M, int64_t N, int64_t K, cudaStream_t st);
+
+}  // namespace dme

@@ -1,0 +1,956 @@
+// C-ABI implementation: context, init (upload, Padé-13 expm, quadrature ladder), composition driver.
+// See include/dme.h for the contract and DESIGN.md for the design and the paper readings.
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "aux.h"
+#include "common.cuh"
+#include "dme.h"
+#include "gemm_nt.h"
+#include "lu.h"
+#include "small.h"
+
+using namespace dme;
+
+void axpy_cols(double* Y, int64_t ldy, const double* X, int64_t ldx, int64_t rows, int64_t cols,
+               double alpha, cudaStream_t st);
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct DmeError : std::runtime_error {
+  dme_status code;
+  DmeError(dme_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define DME_REQUIRE(cond, code, msg) \
+  do {                               \
+    if (!(cond)) throw DmeError(code, msg); \
+  } while (0)
+#define DME_NCCL(x)                                                                       \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess)                                                                \
+      throw DmeError(DME_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+
+// Padé-13 coefficients b_0..b_13 (Higham 2005, Table 2.2 / eq. 2.3)
+const double PADE_B[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
+                           1187353796428800.0,  129060195264000.0,   10559470521600.0,
+                           670442572800.0,      33522128640.0,       1323241920.0,
+                           40840800.0,          960960.0,            16380.0,
+                           182.0,               1.0};
+const double THETA13 = 5.371920351148152;
+
+constexpr int64_t KMAX = SMALL_K_MAX;  // column capacity of every factor buffer
+
+// Gauss-Legendre nodes/weights on [0,1] by Newton on P_q (Golub-Welsch-free; own implementation)
+void gauss_legendre01(int q, std::vector<double>& c, std::vector<double>& w) {
+  c.assign(q, 0.0);
+  w.assign(q, 0.0);
+  for (int i = 0; i < q; ++i) {
+    double x = std::cos(M_PI * (i + 0.75) / (q + 0.5));
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int k = 2; k <= q; ++k) {
+        const double pk = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = pk;
+      }
+      const double dp = q * (x * p1 - p0) / (x * x - 1.0);
+      const double dx = p1 / dp;
+      x -= dx;
+      if (std::fabs(dx) < 1e-17) break;
+    }
+    double p0 = 1.0, p1 = x;
+    for (int k = 2; k <= q; ++k) {
+      const double pk = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+      p0 = p1;
+      p1 = pk;
+    }
+    const double dp = q * (x * p1 - p0) / (x * x - 1.0);
+    c[q - 1 - i] = 0.5 * (x + 1.0);
+    w[q - 1 - i] = 1.0 / ((1.0 - x * x) * dp * dp);  // = (2/((1-x^2)P'^2)) / 2
+  }
+}
+
+struct Planner {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+}  // namespace
+
+struct dme_ctx {
+  int64_t n = 0, ldn = 0, p = 0, m = 0, r0 = 0;
+  bool has_S = false, dre = false;
+  int world = 1, rank = 0;
+  int64_t nloc = 0, row0 = 0, rows_loc = 0;
+  dme_options opt{};
+  cudaStream_t st = nullptr;
+  double h = 0;
+  // persistent device buffers
+  double *E_half = nullptr, *E_full = nullptr, *S = nullptr, *Bcol = nullptr, *LQ = nullptr;
+  double *Zc12h = nullptr, *Zc12f = nullptr, *Zc2 = nullptr, *Z = nullptr, *Ztmp = nullptr;
+  double *G = nullptr, *H = nullptr, *Tm = nullptr, *Vg = nullptr, *LRinv = nullptr, *sstats = nullptr;
+  double *norm_dev = nullptr, *red_scratch = nullptr, *stage = nullptr;
+  int* r_dev = nullptr;
+  GemmScratch gs;
+  // init-only device buffers
+  double *Aup = nullptr, *X0 = nullptr, *BT = nullptr, *X2 = nullptr, *X4 = nullptr, *X6 = nullptr;
+  double *T1 = nullptr, *U = nullptr, *V = nullptr, *lu_scr = nullptr, *Wa = nullptr, *Wb = nullptr;
+  double *Yn = nullptr, *L0d = nullptr, *D0d = nullptr;
+  // host state
+  int64_t r = 0, qh = 0, qf = 0;
+  int32_t rank_cap = 0, qn = 14, subpanels = 1;
+  std::vector<double> lrinv_host;
+  dme_stats stats{};
+  bool poisoned = false;
+  ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+void plan_buffers(dme_ctx* c, Planner& P) {
+  const int64_t n = c->n, ld = c->ldn;
+  const size_t nn = (size_t)n * ld, fk = (size_t)ld * KMAX;
+  c->E_half = P.take<double>(nn);
+  c->E_full = P.take<double>(nn);
+  if (c->has_S) c->S = P.take<double>(nn);
+  c->Bcol = P.take<double>((size_t)ld * std::max<int64_t>(c->m, 1));
+  c->LQ = P.take<double>((size_t)ld * std::max<int64_t>(c->p, 1));
+  c->Zc12h = P.take<double>(fk);
+  c->Zc12f = P.take<double>(fk);
+  c->Zc2 = P.take<double>(fk);
+  c->Z = P.take<double>(fk);
+  c->Ztmp = P.take<double>(fk);
+  c->G = P.take<double>((size_t)KMAX * KMAX);
+  c->H = P.take<double>((size_t)KMAX * SMALL_M_MAX);
+  c->Tm = P.take<double>((size_t)KMAX * KMAX);
+  c->Vg = P.take<double>((size_t)KMAX * KMAX);
+  c->LRinv = P.take<double>(SMALL_M_MAX * SMALL_M_MAX);
+  c->sstats = P.take<double>(16);
+  c->norm_dev = P.take<double>(16);
+  c->red_scratch = P.take<double>(1024);
+  c->r_dev = P.take<int>(16);
+  c->gs.max_grid = 256;
+  c->gs.max_tiles = 1 << 16;
+  c->gs.partial = P.take<double>(GemmScratch::partial_doubles(c->gs.max_grid));
+  c->gs.counters = P.take<int>((size_t)c->gs.max_tiles);
+  if (c->world > 1) c->stage = P.take<double>((size_t)c->world * c->nloc * KMAX);
+  // init-only
+  c->Aup = P.take<double>(nn);
+  c->X0 = P.take<double>(nn);
+  c->BT = P.take<double>(nn);
+  c->X2 = P.take<double>(nn);
+  c->X4 = P.take<double>(nn);
+  c->X6 = P.take<double>(nn);
+  c->T1 = P.take<double>(nn);
+  c->U = P.take<double>(nn);
+  c->V = P.take<double>(nn);
+  c->lu_scr = P.take<double>(lu_scratch_doubles(n));
+  c->Wa = P.take<double>((size_t)ld * std::max<int64_t>(c->p, 1));
+  c->Wb = P.take<double>((size_t)ld * std::max<int64_t>(c->p, 1));
+  c->Yn = P.take<double>((size_t)ld * std::max<int64_t>(c->p * c->qn, 1));
+  c->L0d = P.take<double>((size_t)ld * std::max<int64_t>(c->r0, 1));
+  c->D0d = P.take<double>((size_t)std::max<int64_t>(c->r0 * c->r0, 1));
+}
+
+void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
+  c->n = pr->n;
+  c->ldn = (pr->n + 15) / 16 * 16;
+  c->p = pr->p;
+  c->m = pr->m;
+  c->r0 = pr->r0;
+  c->has_S = pr->S != nullptr;
+  c->opt = *o;
+  c->world = o->world_size > 0 ? o->world_size : 1;
+  c->rank = o->world_rank;
+  c->nloc = (c->n + c->world - 1) / c->world;
+  c->nloc = (c->nloc + 15) / 16 * 16;
+  c->row0 = std::min<int64_t>(c->n, (int64_t)c->rank * c->nloc);
+  c->rows_loc = std::min<int64_t>(c->nloc, c->n - c->row0);
+  c->qn = o->quad_nodes > 0 ? o->quad_nodes : 14;
+  c->subpanels = o->quad_subpanels > 0 ? o->quad_subpanels : 1;
+  int64_t cap = o->rank_cap > 0 ? o->rank_cap : c->n;
+  c->rank_cap = (int32_t)std::min<int64_t>(cap, KMAX);
+  c->h = o->h;
+}
+
+bool all_finite(const double* x, size_t cnt) {
+  for (size_t i = 0; i < cnt; ++i)
+    if (!std::isfinite(x[i])) return false;
+  return true;
+}
+
+void validate(const dme_problem* pr, const dme_options* o, bool dre) {
+  DME_REQUIRE(pr && o, DME_ERR_INVALID, "NULL problem or options");
+  DME_REQUIRE(pr->n > 0 && pr->A, DME_ERR_INVALID, "n must be positive and A non-NULL");
+  DME_REQUIRE(std::isfinite(o->h) && o->h > 0, DME_ERR_INVALID, "h must be positive and finite");
+  DME_REQUIRE(pr->p >= 0 && (pr->p == 0 || pr->C), DME_ERR_INVALID, "C must be non-NULL when p > 0");
+  DME_REQUIRE(pr->r0 >= 0 && (pr->r0 == 0 || pr->L0), DME_ERR_INVALID, "L0 must be non-NULL when r0 > 0");
+  DME_REQUIRE(o->trunc_tol >= 0, DME_ERR_INVALID, "trunc_tol must be >= 0");
+  if (dre) {
+    DME_REQUIRE(pr->m >= 1 && pr->B && pr->R, DME_ERR_INVALID, "dre_init needs m >= 1, B and R");
+  } else {
+    DME_REQUIRE(pr->m == 0, DME_ERR_INVALID, "dle_init requires m == 0");
+  }
+  DME_REQUIRE(pr->m <= SMALL_M_MAX, DME_ERR_DIM, "m exceeds 8");
+  const int qn = o->quad_nodes > 0 ? o->quad_nodes : 14;
+  DME_REQUIRE(qn <= 64, DME_ERR_DIM, "quad_nodes must be <= 64");
+  DME_REQUIRE(pr->p * qn <= KMAX && pr->r0 <= KMAX && pr->p <= KMAX, DME_ERR_DIM,
+              "p * quad_nodes and r0 must be <= 224");
+  const int sp = o->quad_subpanels > 0 ? o->quad_subpanels : 1;
+  DME_REQUIRE((sp & (sp - 1)) == 0, DME_ERR_INVALID, "quad_subpanels must be a power of two");
+  DME_REQUIRE(o->world_size <= 1 || o->nccl_uid, DME_ERR_INVALID, "nccl_uid required for world_size > 1");
+  // input finiteness (host scan; inputs are host arrays)
+  const size_t nn = (size_t)pr->n * pr->n;
+  DME_REQUIRE(all_finite(pr->A, nn), DME_ERR_INVALID, "A has non-finite entries");
+  if (pr->p) DME_REQUIRE(all_finite(pr->C, (size_t)pr->p * pr->n), DME_ERR_INVALID, "C non-finite");
+  if (pr->S) DME_REQUIRE(all_finite(pr->S, nn), DME_ERR_INVALID, "S non-finite");
+  if (pr->r0) DME_REQUIRE(all_finite(pr->L0, (size_t)pr->n * pr->r0), DME_ERR_INVALID, "L0 non-finite");
+  if (pr->m) {
+    DME_REQUIRE(all_finite(pr->B, (size_t)pr->n * pr->m) && all_finite(pr->R, (size_t)pr->m * pr->m),
+                DME_ERR_INVALID, "B or R non-finite");
+  }
+}
+
+// Host preprocessing of the m x m input weight: R = L_R L_R^T (validates SPD), returns L_R^{-1}.
+std::vector<double> chol_inverse_lower(const double* R, int m) {
+  std::vector<double> L(m * m, 0.0), Li(m * m, 0.0);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j)
+      DME_REQUIRE(std::fabs(R[i * m + j] - R[j * m + i]) <= 1e-12 * (std::fabs(R[i * m + j]) + 1e-300),
+                  DME_ERR_INVALID, "R is not symmetric");
+  for (int j = 0; j < m; ++j) {
+    double d = R[j * m + j];
+    for (int k = 0; k < j; ++k) d -= L[j * m + k] * L[j * m + k];
+    DME_REQUIRE(d > 0, DME_ERR_INVALID, "R is not positive definite");
+    L[j * m + j] = std::sqrt(d);
+    for (int i = j + 1; i < m; ++i) {
+      double s = R[i * m + j];
+      for (int k = 0; k < j; ++k) s -= L[i * m + k] * L[j * m + k];
+      L[i * m + j] = s / L[j * m + j];
+    }
+  }
+  for (int c = 0; c < m; ++c) {
+    for (int i = 0; i < m; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= L[i * m + k] * Li[k * m + c];
+      Li[i * m + c] = s / L[i * m + i];
+    }
+  }
+  return Li;
+}
+
+void check_psd_host(const double* D, int64_t r) {
+  // symmetric and positive semidefinite up to round-off (LDL^T with diagonal pivoting)
+  std::vector<double> a(D, D + r * r);
+  double mx = 0;
+  for (int64_t i = 0; i < r * r; ++i) mx = std::max(mx, std::fabs(a[i]));
+  for (int64_t i = 0; i < r; ++i)
+    for (int64_t j = 0; j < r; ++j)
+      DME_REQUIRE(std::fabs(a[i * r + j] - a[j * r + i]) <= 1e-12 * mx, DME_ERR_INVALID,
+                  "D0 is not symmetric");
+  std::vector<char> used(r, 0);
+  for (int64_t step = 0; step < r; ++step) {
+    int64_t pv = -1;
+    double best = -1e300;
+    for (int64_t i = 0; i < r; ++i)
+      if (!used[i] && a[i * r + i] > best) { best = a[i * r + i]; pv = i; }
+    if (pv < 0 || best <= 1e-13 * mx) {
+      for (int64_t i = 0; i < r; ++i)
+        if (!used[i]) DME_REQUIRE(a[i * r + i] >= -1e-10 * mx, DME_ERR_INVALID, "D0 is not PSD");
+      return;
+    }
+    used[pv] = 1;
+    for (int64_t i = 0; i < r; ++i)
+      for (int64_t j = 0; j < r; ++j)
+        if (!used[i] && !used[j]) a[i * r + j] -= a[i * r + pv] * a[pv * r + j] / best;
+  }
+}
+
+void sync(dme_ctx* c) { DME_CUDA(cudaStreamSynchronize(c->st)); }
+
+// ------------------------------------------------------------------ building blocks
+// out (col-major, ldo) = alpha * E * X  (E: n x n row-major, X: n x k col-major), sharded over ranks
+void epass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t ldo,
+           double alpha) {
+  if (k <= 0) return;
+  c->stats.e_passes++;
+  if (c->world == 1) {
+    GemmNTArgs g;
+    g.A = E; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
+    g.M = c->n; g.N = k; g.K = c->n; g.alpha = alpha;
+    g.out = out; g.out_rs = 1; g.out_cs = ldo;
+    gemm_nt(g, c->gs, c->st);
+    return;
+  }
+  // row shard: local rows into this rank's staging block (nloc x k, col-major), allgather, unpack
+  double* mine = c->stage + (size_t)c->rank * c->nloc * k;
+  if (c->rows_loc > 0) {
+    GemmNTArgs g;
+    g.A = E + c->row0 * c->ldn; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
+    g.M = c->rows_loc; g.N = k; g.K = c->n; g.alpha = alpha;
+    g.out = mine; g.out_rs = 1; g.out_cs = c->nloc;
+    gemm_nt(g, c->gs, c->st);
+  }
+  DME_NCCL(ncclAllGather(mine, c->stage, (size_t)c->nloc * k, ncclDouble, c->comm, c->st));
+  for (int gr = 0; gr < c->world; ++gr) {
+    const int64_t r0 = std::min<int64_t>(c->n, (int64_t)gr * c->nloc);
+    const int64_t rows = std::min<int64_t>(c->nloc, c->n - r0);
+    if (rows > 0)
+      copy_cols(out + r0, ldo, c->stage + (size_t)gr * c->nloc * k, c->nloc, rows, k, 1.0, c->st);
+  }
+}
+
+// Compress the factor Zc (n x k, col-major ldn) into out (n x r); optionally fuse T3(tau3).
+int64_t compress(dme_ctx* c, const double* Zc, int64_t k, double* out, bool t3, double tau3,
+                 bool do_compress = true) {
+  if (k <= 0) return 0;
+  DME_REQUIRE(k <= KMAX, DME_ERR_DIM, "factor width exceeds the small-system limit (224)");
+  c->stats.compressions += do_compress ? 1 : 0;
+  if (do_compress) {
+    GemmNTArgs g;
+    g.A = Zc; g.lda = c->ldn; g.B = Zc; g.ldb = c->ldn;
+    g.M = k; g.N = k; g.K = c->n;
+    g.out = c->G; g.out_rs = 1; g.out_cs = KMAX;
+    gemm_nt(g, c->gs, c->st);
+  }
+  if (t3) {
+    GemmNTArgs g;
+    g.A = Zc; g.lda = c->ldn; g.B = c->Bcol; g.ldb = c->ldn;
+    g.M = k; g.N = c->m; g.K = c->n;
+    g.out = c->H; g.out_rs = 1; g.out_cs = KMAX;
+    gemm_nt(g, c->gs, c->st);
+  }
+  SmallArgs a;
+  a.k = (int)k;
+  a.compress = do_compress ? 1 : 0;
+  a.G = c->G; a.ldg = KMAX;
+  a.tol = c->opt.trunc_tol;
+  a.cap = c->rank_cap;
+  a.t3 = t3 ? 1 : 0;
+  a.m = (int)c->m;
+  a.H = c->H; a.ldh = KMAX;
+  a.LRinv = c->LRinv;
+  a.tau = tau3;
+  a.Tm = c->Tm; a.ldt = KMAX;
+  a.V = c->Vg; a.ldv = KMAX;
+  a.r_out = c->r_dev;
+  a.stats = c->sstats;
+  compress_t3(a, c->st);
+  int r_host = 0;
+  double st_host[3];
+  DME_CUDA(cudaMemcpyAsync(&r_host, c->r_dev, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  DME_CUDA(cudaMemcpyAsync(st_host, c->sstats, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (do_compress) c->stats.last_drop = st_host[2];
+  if (r_host > 0) tall_small(Zc, c->ldn, c->Tm, KMAX, out, c->ldn, c->n, r_host, k, c->st);
+  return r_host;
+}
+
+// ------------------------------------------------------------------ flows on the state Z
+void swapZ(dme_ctx* c) { std::swap(c->Z, c->Ztmp); }
+
+void flow_T1(dme_ctx* c, double tau) {
+  const double* E = (tau == c->h) ? c->E_full : c->E_half;
+  epass(c, E, c->Z, c->r, c->Ztmp, c->ldn, 1.0);
+  swapZ(c);
+}
+
+void finish_compress(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3) {
+  c->r = compress(c, Zc, k, c->Ztmp, t3, tau3);
+  swapZ(c);
+  c->stats.max_rank = std::max<int64_t>(c->stats.max_rank, c->r);
+}
+
+void flow_T2(dme_ctx* c, double tau, bool t3, double tau3) {
+  copy_cols(c->Zc2, c->ldn, c->Z, c->ldn, c->n, c->r, 1.0, c->st);
+  copy_cols(c->Zc2 + c->r * c->ldn, c->ldn, c->LQ, c->ldn, c->n, c->p, std::sqrt(tau), c->st);
+  finish_compress(c, c->Zc2, c->r + c->p, t3, tau3);
+}
+
+void flow_T12(dme_ctx* c, double tau, bool t3, double tau3) {
+  const bool full = (tau == c->h);
+  double* Zc = full ? c->Zc12f : c->Zc12h;
+  const int64_t q = full ? c->qf : c->qh;
+  epass(c, full ? c->E_full : c->E_half, c->Z, c->r, Zc + q * c->ldn, c->ldn, 1.0);
+  finish_compress(c, Zc, q + c->r, t3, tau3);
+}
+
+void flow_T3(dme_ctx* c, double tau) {
+  if (c->r == 0) return;
+  const int64_t r = compress(c, c->Z, c->r, c->Ztmp, true, tau, /*do_compress=*/false);
+  (void)r;
+  swapZ(c);
+}
+
+void flow_T4(dme_ctx* c, double tau, int order, bool t3, double tau3) {
+  if (c->r == 0) return;
+  const int64_t r = c->r, ld = c->ldn;
+  copy_cols(c->Zc2, ld, c->Z, ld, c->n, r, 1.0, c->st);
+  epass(c, c->S, c->Z, r, c->Zc2 + r * ld, ld, std::sqrt(tau));                  // sqrt(tau) S L
+  int64_t k = 2 * r;
+  if (order == 2) {                                                                 // tau/sqrt2 S^2 L
+    epass(c, c->S, c->Zc2 + r * ld, r, c->Zc2 + 2 * r * ld, ld, std::sqrt(tau) / std::sqrt(2.0));
+    k = 3 * r;
+  }
+  finish_compress(c, c->Zc2, k, t3, tau3);
+}
+
+struct Op {
+  int flow;
+  double tau;
+};
+
+std::vector<Op> step_sequence(dme_scheme scheme, dme_composition comp, double h) {
+  std::vector<int> fl;
+  switch (comp) {
+    case DME_F1F2: fl = {0, 1}; break;
+    case DME_F12: fl = {5}; break;
+    case DME_F12F3: fl = {5, 2}; break;
+    case DME_F1F2F3: fl = {0, 1, 2}; break;
+    case DME_F1F3F2: fl = {0, 2, 1}; break;
+    case DME_F12F4: fl = {5, 3}; break;
+    case DME_F1F2F4: fl = {0, 1, 3}; break;
+    case DME_F1F4F2: fl = {0, 3, 1}; break;
+    case DME_F12F3F4: fl = {5, 2, 3}; break;
+    case DME_F1F2F3F4: fl = {0, 1, 2, 3}; break;
+    default: throw DmeError(DME_ERR_CONFIG, "unknown composition");
+  }
+  std::vector<Op> seq;
+  if (scheme == DME_LIE) {
+    for (int f : fl) seq.push_back({f == 3 ? 4 : f, h});  // T4 by explicit Euler under Lie
+  } else if (scheme == DME_STRANG) {
+    if (fl.size() == 1) {
+      seq.push_back({fl[0], h});
+    } else {
+      for (size_t i = 0; i + 1 < fl.size(); ++i) seq.push_back({fl[i], h / 2});
+      seq.push_back({fl.back(), h});
+      for (size_t i = fl.size() - 1; i-- > 0;) seq.push_back({fl[i], h / 2});
+    }
+  } else {
+    throw DmeError(DME_ERR_CONFIG, "unknown scheme");
+  }
+  return seq;
+}
+
+void check_capable(dme_ctx* c, const std::vector<Op>& seq) {
+  for (const Op& o : seq) {
+    if (o.flow == DME_FLOW_T3) DME_REQUIRE(c->dre, DME_ERR_CONFIG, "composition uses F3 but the problem has no B");
+    if (o.flow == DME_FLOW_T4_MIDPOINT || o.flow == DME_FLOW_T4_EULER)
+      DME_REQUIRE(c->has_S, DME_ERR_CONFIG, "composition uses F4 but the problem has no S");
+    if (o.flow == DME_FLOW_T2) DME_REQUIRE(c->p >= 0, DME_ERR_CONFIG, "bad p");
+  }
+}
+
+// Execute a sequence; a compressing flow immediately followed by T3 runs T3 fused.
+void run_sequence(dme_ctx* c, const std::vector<Op>& seq) {
+  for (size_t i = 0; i < seq.size(); ++i) {
+    const Op& o = seq[i];
+    const bool next_t3 = i + 1 < seq.size() && seq[i + 1].flow == DME_FLOW_T3;
+    const double tau3 = next_t3 ? seq[i + 1].tau : 0.0;
+    switch (o.flow) {
+      case DME_FLOW_T1: flow_T1(c, o.tau); break;
+      case DME_FLOW_T2: flow_T2(c, o.tau, next_t3, tau3); if (next_t3) ++i; break;
+      case DME_FLOW_T3: flow_T3(c, o.tau); break;
+      case DME_FLOW_T4_MIDPOINT: flow_T4(c, o.tau, 2, next_t3, tau3); if (next_t3) ++i; break;
+      case DME_FLOW_T4_EULER: flow_T4(c, o.tau, 1, next_t3, tau3); if (next_t3) ++i; break;
+      case DME_FLOW_T12: flow_T12(c, o.tau, next_t3, tau3); if (next_t3) ++i; break;
+      default: throw DmeError(DME_ERR_CONFIG, "unknown flow");
+    }
+  }
+}
+
+// ------------------------------------------------------------------ init: expm + quadrature
+void matmul_sq(dme_ctx* c, const double* X, const double* Y, double* out) {
+  // out = X * Y  (n x n row-major): B operand rows = columns of Y = rows of Y^T
+  transpose_rect(Y, c->n, c->n, c->ldn, c->BT, c->ldn, c->st);
+  GemmNTArgs g;
+  g.A = X; g.lda = c->ldn; g.B = c->BT; g.ldb = c->ldn;
+  g.M = c->n; g.N = c->n; g.K = c->n;
+  g.out = out; g.out_rs = c->ldn; g.out_cs = 1;
+  gemm_nt(g, c->gs, c->st);
+}
+
+// L_I(2w) = compress([L_I(w), E_w L_I(w)])  (exact doubling of the composite rule, reading G6)
+void ladder_double(dme_ctx* c, double* LI, int64_t& q, const double* Ew) {
+  if (q == 0) return;
+  DME_REQUIRE(2 * q <= KMAX, DME_ERR_DIM, "quadrature factor rank exceeds 112");
+  epass(c, Ew, LI, q, LI + q * c->ldn, c->ldn, 1.0);
+  const int64_t qn = compress(c, LI, 2 * q, c->Ztmp, false, 0.0);
+  copy_cols(LI, c->ldn, c->Ztmp, c->ldn, c->n, qn, 1.0, c->st);
+  q = qn;
+}
+
+void init_all(dme_ctx* c, const dme_problem* pr) {
+  const int64_t n = c->n, ld = c->ldn;
+  cudaStream_t st = c->st;
+  DME_CUDA(cudaMemsetAsync(c->gs.counters, 0, sizeof(int) * c->gs.max_tiles, st));
+  // ---------------------------------------------------------------- upload (H2D boundary)
+  DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, cudaMemcpyHostToDevice, st));
+  if (c->has_S)
+    DME_CUDA(cudaMemcpy2DAsync(c->S, ld * 8, pr->S, n * 8, n * 8, n, cudaMemcpyHostToDevice, st));
+  if (c->p > 0)  // C (p x n row-major): row i of C = column i of L_Q = C^T
+    DME_CUDA(cudaMemcpy2DAsync(c->LQ, ld * 8, pr->C, n * 8, n * 8, c->p, cudaMemcpyHostToDevice, st));
+  if (c->m > 0) {
+    DME_CUDA(cudaMemcpyAsync(c->Wa, pr->B, n * c->m * 8, cudaMemcpyHostToDevice, st));
+    rowmajor_to_colmajor(c->Bcol, ld, c->Wa, c->m, n, c->m, st);
+    DME_CUDA(cudaMemcpyAsync(c->LRinv, c->lrinv_host.data(), c->m * c->m * 8, cudaMemcpyHostToDevice, st));
+  }
+  if (c->r0 > 0) {
+    DME_CUDA(cudaMemcpyAsync(c->Yn, pr->L0, n * c->r0 * 8, cudaMemcpyHostToDevice, st));
+    rowmajor_to_colmajor(c->L0d, ld, c->Yn, c->r0, n, c->r0, st);
+    std::vector<double> D0(c->r0 * c->r0, 0.0);
+    for (int64_t i = 0; i < c->r0; ++i)
+      for (int64_t j = 0; j < c->r0; ++j)
+        D0[i * c->r0 + j] = pr->D0 ? pr->D0[i * c->r0 + j] : (i == j ? 1.0 : 0.0);
+    DME_CUDA(cudaMemcpyAsync(c->D0d, D0.data(), D0.size() * 8, cudaMemcpyHostToDevice, st));
+    sync(c);
+  }
+  // ---------------------------------------------------------------- scaling: s from ||(h/2) A^T||_1
+  rowabs_max(c->Aup, n, ld, c->red_scratch, c->norm_dev, st);
+  double nrm = 0;
+  DME_CUDA(cudaMemcpyAsync(&nrm, c->norm_dev, 8, cudaMemcpyDeviceToHost, st));
+  sync(c);
+  DME_REQUIRE(std::isfinite(nrm), DME_ERR_NUMERIC, "non-finite norm of A");
+  const double tau0 = c->h / 2;
+  const double tn = tau0 * nrm;
+  int s = 0;
+  if (tn > THETA13) s = std::max(0, (int)std::ceil(std::log2(tn / THETA13)));
+  int sp_log = 0;
+  while ((1 << sp_log) < c->subpanels) ++sp_log;
+  const int s_total = s + sp_log;
+  const double delta = tau0 / std::ldexp(1.0, s_total);
+  c->stats.squarings = s;
+  c->stats.quad_panels = 1 << s_total;
+  c->stats.panel_width = delta;
+  // X0 = delta * A^T
+  transpose_scale(c->Aup, n, ld, delta, c->X0, ld, st);
+
+  // ---------------------------------------------------------------- first-panel node actions
+  // Y_i = exp(c_i delta A^T) L_Q = sum_j c_i^j W_j,  W_j = (delta A^T) W_{j-1} / j   (Taylor)
+  const int q = c->qn;
+  std::vector<double> cn, wn;
+  gauss_legendre01(q, cn, wn);
+  int64_t qI = 0;
+  if (c->p > 0) {
+    const double nx0 = delta * nrm;  // ||delta A^T||_1 bound for the truncation
+    int J = 1;
+    double term = 1.0;
+    while (J < 200) {
+      term *= nx0 / J;
+      if (term < 1e-18 && J > nx0) break;
+      ++J;
+    }
+    for (int i = 0; i < q; ++i)
+      copy_cols(c->Yn + (size_t)i * c->p * ld, ld, c->LQ, ld, n, c->p, 1.0, st);
+    copy_cols(c->Wa, ld, c->LQ, ld, n, c->p, 1.0, st);
+    double* Wcur = c->Wa;
+    double* Wnext = c->Wb;
+    std::vector<double> cpow(q, 1.0);
+    for (int j = 1; j <= J; ++j) {
+      GemmNTArgs g;
+      g.A = c->X0; g.lda = ld; g.B = Wcur; g.ldb = ld;
+      g.M = n; g.N = c->p; g.K = n; g.alpha = 1.0 / j;
+      g.out = Wnext; g.out_rs = 1; g.out_cs = ld;
+      gemm_nt(g, c->gs, st);
+      std::swap(Wcur, Wnext);
+      for (int i = 0; i < q; ++i) {
+        cpow[i] *= cn[i];
+        double* Yi = c->Yn + (size_t)i * c->p * ld;
+        axpy_cols(Yi, ld, Wcur, ld, n, c->p, cpow[i], st);  // Y_i += c_i^j W_j
+      }
+    }
+    // L_I(delta) = [sqrt(w_i delta) Y_i]  (D_I = blkdiag(w_i D_Q), D_Q = I; square-root form)
+    for (int i = 0; i < q; ++i)
+      copy_cols(c->Zc12h + (size_t)i * c->p * ld, ld, c->Yn + (size_t)i * c->p * ld, ld, n, c->p,
+                std::sqrt(wn[i] * delta), st);
+    qI = compress(c, c->Zc12h, (int64_t)q * c->p, c->Ztmp, false, 0.0);
+    copy_cols(c->Zc12h, ld, c->Ztmp, ld, n, qI, 1.0, st);
+  }
+
+  // ---------------------------------------------------------------- Padé-13 on X0 (Higham 2005)
+  const double* b = PADE_B;
+  matmul_sq(c, c->X0, c->X0, c->X2);
+  matmul_sq(c, c->X2, c->X2, c->X4);
+  matmul_sq(c, c->X4, c->X2, c->X6);
+  lincomb(c->T1, n, ld, {b[13], c->X6}, {b[11], c->X4}, {b[9], c->X2}, {}, 0.0, st);
+  matmul_sq(c, c->X6, c->T1, c->U);  // Y1 = X6 W1
+  lincomb(c->T1, n, ld, {1.0, c->U}, {b[7], c->X6}, {b[5], c->X4}, {b[3], c->X2}, b[1], st);
+  matmul_sq(c, c->X0, c->T1, c->U);  // U = X0 W2
+  lincomb(c->T1, n, ld, {b[12], c->X6}, {b[10], c->X4}, {b[8], c->X2}, {}, 0.0, st);
+  matmul_sq(c, c->X6, c->T1, c->V);  // Y2 = X6 Z1
+  lincomb(c->V, n, ld, {1.0, c->V}, {b[6], c->X6}, {b[4], c->X4}, {b[2], c->X2}, b[0], st);
+  lincomb(c->X4, n, ld, {1.0, c->V}, {-1.0, c->U}, {}, {}, 0.0, st);  // Q = V - U
+  lincomb(c->X6, n, ld, {1.0, c->V}, {1.0, c->U}, {}, {}, 0.0, st);   // P = V + U
+  lu_nopiv_solve_right(c->X4, c->X6, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 1);
+  double minpiv = 0;
+  DME_CUDA(cudaMemcpyAsync(&minpiv, c->norm_dev + 1, 8, cudaMemcpyDeviceToHost, st));
+  sync(c);
+  c->stats.pade_min_pivot = minpiv;
+  DME_REQUIRE(std::isfinite(minpiv) && minpiv > 1e-8 * b[0], DME_ERR_NUMERIC,
+              "Padé denominator factorisation hit a tiny pivot");
+
+  // ---------------------------------------------------------------- squaring ladder + quadrature
+  double* Ecur = c->X6;
+  double* spare[2] = {c->X2, c->U};
+  int si = 0;
+  int64_t q_cur = qI;
+  for (int j = 0; j < s_total; ++j) {
+    ladder_double(c, c->Zc12h, q_cur, Ecur);  // L_I(2w) from E_w, w = delta 2^j
+    double* En = spare[si];
+    matmul_sq(c, Ecur, Ecur, En);
+    spare[si] = (Ecur == c->X6) ? c->V : Ecur;
+    si ^= 1;
+    Ecur = En;
+  }
+  DME_CUDA(cudaMemcpyAsync(c->E_half, Ecur, (size_t)n * ld * 8, cudaMemcpyDeviceToDevice, st));
+  c->qh = q_cur;
+  // L_I(h) = compress([L_I(h/2), E_{h/2} L_I(h/2)]),  E_h = E_{h/2}^2
+  copy_cols(c->Zc12f, ld, c->Zc12h, ld, n, c->qh, 1.0, st);
+  int64_t qf = c->qh;
+  ladder_double(c, c->Zc12f, qf, c->E_half);
+  c->qf = qf;
+  matmul_sq(c, c->E_half, c->E_half, c->E_full);
+  c->stats.q_half = c->qh;
+  c->stats.q_full = c->qf;
+
+  // ---------------------------------------------------------------- P0: Z0 = L0 D0^{1/2}, compressed
+  c->r = 0;
+  if (c->r0 > 0) {
+    // square-root factor of D0 through the same kernel: D0 = W Theta W^T, Tm = W Theta^{1/2}
+    DME_CUDA(cudaMemcpy2DAsync(c->G, KMAX * 8, c->D0d, c->r0 * 8, c->r0 * 8, c->r0,
+                               cudaMemcpyDeviceToDevice, st));
+    SmallArgs a;
+    a.k = (int)c->r0; a.compress = 1; a.G = c->G; a.ldg = KMAX; a.tol = 1e-15; a.cap = (int)c->r0;
+    a.Tm = c->Tm; a.ldt = KMAX; a.r_out = c->r_dev; a.stats = c->sstats;
+    a.V = c->Vg; a.ldv = KMAX; a.sqrt_scale = 1;
+    compress_t3(a, st);
+    int rd = 0;
+    DME_CUDA(cudaMemcpyAsync(&rd, c->r_dev, 4, cudaMemcpyDeviceToHost, st));
+    sync(c);
+    if (rd > 0) {
+      tall_small(c->L0d, ld, c->Tm, KMAX, c->Zc2, ld, n, rd, c->r0, st);
+      c->r = compress(c, c->Zc2, rd, c->Z, false, 0.0);
+    }
+  }
+  c->stats.rank = c->r;
+  c->stats.max_rank = c->r;
+  sync(c);
+}
+
+dme_status fail(const std::exception& e, dme_status code, dme_ctx* c = nullptr) {
+  g_last_error = e.what();
+  if (c && (code == DME_ERR_CUDA || code == DME_ERR_NCCL)) c->poisoned = true;
+  return code;
+}
+
+template <class F>
+dme_status guarded(dme_ctx* c, F&& f) {
+  if (c && c->poisoned) {
+    g_last_error = "context poisoned by an earlier CUDA/NCCL failure";
+    return DME_ERR_POISONED;
+  }
+  try {
+    f();
+    return DME_OK;
+  } catch (const DmeError& e) {
+    return fail(e, e.code, c);
+  } catch (const CudaError& e) {
+    return fail(e, DME_ERR_CUDA, c);
+  } catch (const std::bad_alloc& e) {
+    return fail(e, DME_ERR_NOMEM, c);
+  } catch (const std::exception& e) {
+    return fail(e, DME_ERR_CUDA, c);
+  }
+}
+
+dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** out, bool dre) {
+  if (!out) {
+    g_last_error = "NULL ctx out-pointer";
+    return DME_ERR_INVALID;
+  }
+  *out = nullptr;
+  dme_ctx* c = nullptr;
+  dme_status s = guarded(nullptr, [&] {
+    validate(pr, o, dre);
+    auto t0 = std::chrono::steady_clock::now();
+    std::unique_ptr<dme_ctx> cp(new dme_ctx());
+    c = cp.get();
+    fill_dims(c, pr, o);
+    c->dre = dre;
+    if (dre) c->lrinv_host = chol_inverse_lower(pr->R, (int)pr->m);
+    if (pr->r0 > 0 && pr->D0) check_psd_host(pr->D0, pr->r0);
+    DME_CUDA(cudaSetDevice(o->device));
+    c->st = reinterpret_cast<cudaStream_t>(o->stream);
+    Planner sizing;
+    plan_buffers(c, sizing);
+    DME_REQUIRE(o->workspace && o->workspace_bytes >= sizing.off + 256, DME_ERR_CAPACITY,
+                "workspace too small: need " + std::to_string(sizing.off + 256) + " bytes");
+    Planner P;
+    P.base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(o->workspace) + 255) & ~uintptr_t(255));
+    plan_buffers(c, P);
+    if (c->world > 1) {
+      ncclUniqueId uid;
+      std::memcpy(&uid, o->nccl_uid, sizeof(uid));
+      DME_NCCL(ncclCommInitRank(&c->comm, c->world, uid, c->rank));
+    }
+    init_all(c, pr);
+    c->stats.init_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = cp.release();
+  });
+  if (s != DME_OK && c && *out == nullptr) {
+    // the unique_ptr already freed it
+  }
+  return s;
+}
+
+}  // namespace
+
+// axpy on a column block: Y[:, j] += alpha X[:, j]
+namespace {
+__global__ void axpy_cols_kernel(double* Y, int64_t ldy, const double* X, int64_t ldx, int64_t rows,
+                                 int64_t cols, double alpha) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    Y[i + j * ldy] += alpha * X[i + j * ldx];
+  }
+}
+}  // namespace
+void axpy_cols(double* Y, int64_t ldy, const double* X, int64_t ldx, int64_t rows, int64_t cols,
+               double alpha, cudaStream_t st) {
+  const int64_t total = rows * cols;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  axpy_cols_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(Y, ldy, X, ldx, rows, cols, alpha);
+  DME_KCHECK();
+}
+
+// ====================================================================== C ABI
+extern "C" {
+
+void dme_default_options(dme_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->h = 0.005;
+  o->trunc_tol = 1e-16;
+  o->rank_cap = 0;
+  o->quad_nodes = 14;
+  o->quad_subpanels = 1;
+  o->world_size = 1;
+}
+
+const char* dme_status_string(dme_status s) {
+  switch (s) {
+    case DME_OK: return "ok";
+    case DME_ERR_INVALID: return "invalid argument";
+    case DME_ERR_DIM: return "dimension error";
+    case DME_ERR_CONFIG: return "configuration error";
+    case DME_ERR_SINGULAR: return "singular system";
+    case DME_ERR_NUMERIC: return "numerical failure";
+    case DME_ERR_CAPACITY: return "capacity exceeded";
+    case DME_ERR_CUDA: return "CUDA error";
+    case DME_ERR_NCCL: return "NCCL error";
+    case DME_ERR_NOMEM: return "out of memory";
+    case DME_ERR_POISONED: return "context poisoned";
+  }
+  return "unknown status";
+}
+
+const char* dme_last_error(void) { return g_last_error.c_str(); }
+
+dme_status dme_workspace_size(const dme_problem* pr, const dme_options* o, size_t* bytes) {
+  return guarded(nullptr, [&] {
+    DME_REQUIRE(pr && o && bytes, DME_ERR_INVALID, "NULL argument");
+    DME_REQUIRE(pr->n > 0, DME_ERR_INVALID, "n must be positive");
+    dme_ctx c;
+    fill_dims(&c, pr, o);
+    Planner P;
+    plan_buffers(&c, P);
+    *bytes = P.off + 512;
+  });
+}
+
+dme_status dme_get_unique_id(void* uid128) {
+  return guarded(nullptr, [&] {
+    DME_REQUIRE(uid128, DME_ERR_INVALID, "NULL uid");
+    ncclUniqueId id;
+    DME_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(uid128, &id, sizeof(id));
+  });
+}
+
+dme_status dme_dle_init(const dme_problem* pr, const dme_options* o, dme_ctx** ctx) {
+  return init_common(pr, o, ctx, false);
+}
+dme_status dme_dre_init(const dme_problem* pr, const dme_options* o, dme_ctx** ctx) {
+  return init_common(pr, o, ctx, true);
+}
+
+dme_status dme_split_step(dme_ctx* c, dme_scheme scheme, dme_composition comp, int64_t nsteps) {
+  if (!c) { g_last_error = "NULL ctx"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    DME_REQUIRE(nsteps >= 0, DME_ERR_INVALID, "nsteps must be >= 0");
+    auto seq = step_sequence(scheme, comp, c->h);
+    check_capable(c, seq);
+    for (int64_t s = 0; s < nsteps; ++s) {
+      run_sequence(c, seq);
+      c->stats.steps++;
+    }
+    c->stats.t = c->stats.steps * c->h;
+    c->stats.rank = c->r;
+    DME_CUDA(cudaGetLastError());
+  });
+}
+
+dme_status dme_get_factor(dme_ctx* c, int64_t* r, double* L, double* D, int64_t cap) {
+  if (!c) { g_last_error = "NULL ctx"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    DME_REQUIRE(r, DME_ERR_INVALID, "NULL r");
+    *r = c->r;
+    if (!L && !D) return;
+    DME_REQUIRE(c->r <= cap, DME_ERR_CAPACITY, "factor has more columns than capacity_cols");
+    if (L && c->r > 0) {
+      std::vector<double> tmp((size_t)c->n * c->r);
+      DME_CUDA(cudaMemcpy2DAsync(tmp.data(), c->n * 8, c->Z, c->ldn * 8, c->n * 8, c->r,
+                                 cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      for (int64_t j = 0; j < c->r; ++j)
+        for (int64_t i = 0; i < c->n; ++i) L[i * c->r + j] = tmp[(size_t)j * c->n + i];
+    }
+    if (D)  // square-root form: P = Z Z^T, i.e. D = I
+      for (int64_t i = 0; i < c->r; ++i)
+        for (int64_t j = 0; j < c->r; ++j) D[i * c->r + j] = i == j ? 1.0 : 0.0;
+  });
+}
+
+dme_status dme_get_stats(dme_ctx* c, dme_stats* st) {
+  if (!c || !st) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
+  c->stats.rank = c->r;
+  *st = c->stats;
+  return DME_OK;
+}
+
+dme_status dme_destroy(dme_ctx* c) {
+  if (!c) return DME_OK;
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return DME_OK;
+}
+
+dme_status dme_debug_apply(dme_ctx* c, int32_t flow, double tau) {
+  if (!c) { g_last_error = "NULL ctx"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    if (flow == DME_FLOW_T1 || flow == DME_FLOW_T12)
+      DME_REQUIRE(tau == c->h || tau == c->h / 2, DME_ERR_CONFIG, "tau must be h or h/2");
+    switch (flow) {
+      case DME_FLOW_T1: flow_T1(c, tau); break;
+      case DME_FLOW_T2: flow_T2(c, tau, false, 0); break;
+      case DME_FLOW_T3: DME_REQUIRE(c->dre, DME_ERR_CONFIG, "no B"); flow_T3(c, tau); break;
+      case DME_FLOW_T4_MIDPOINT: DME_REQUIRE(c->has_S, DME_ERR_CONFIG, "no S"); flow_T4(c, tau, 2, false, 0); break;
+      case DME_FLOW_T4_EULER: DME_REQUIRE(c->has_S, DME_ERR_CONFIG, "no S"); flow_T4(c, tau, 1, false, 0); break;
+      case DME_FLOW_T12: flow_T12(c, tau, false, 0); break;
+      case DME_FLOW_COMPRESS:
+        if (c->r > 0) {
+          copy_cols(c->Zc2, c->ldn, c->Z, c->ldn, c->n, c->r, 1.0, c->st);
+          finish_compress(c, c->Zc2, c->r, false, 0);
+        }
+        break;
+      default: throw DmeError(DME_ERR_CONFIG, "unknown flow");
+    }
+    sync(c);
+  });
+}
+
+dme_status dme_debug_set_factor(dme_ctx* c, int64_t r, const double* L) {
+  if (!c) { g_last_error = "NULL ctx"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    DME_REQUIRE(r >= 0 && r <= KMAX && (r == 0 || L), DME_ERR_INVALID, "bad factor");
+    if (r > 0) {
+      DME_CUDA(cudaMemcpyAsync(c->Ztmp, L, c->n * r * 8, cudaMemcpyHostToDevice, c->st));
+      rowmajor_to_colmajor(c->Z, c->ldn, c->Ztmp, r, c->n, r, c->st);
+    }
+    c->r = r;
+    sync(c);
+  });
+}
+
+dme_status dme_debug_get_exp(dme_ctx* c, int32_t which, double* E) {
+  if (!c || !E) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    const double* src = which ? c->E_full : c->E_half;
+    DME_CUDA(cudaMemcpy2DAsync(E, c->n * 8, src, c->ldn * 8, c->n * 8, c->n,
+                               cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  });
+}
+
+dme_status dme_debug_get_integral(dme_ctx* c, int32_t which, int64_t* q, double* L, int64_t cap) {
+  if (!c || !q) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    const int64_t qq = which ? c->qf : c->qh;
+    *q = qq;
+    if (!L) return;
+    DME_REQUIRE(qq <= cap, DME_ERR_CAPACITY, "capacity too small");
+    std::vector<double> tmp((size_t)c->n * std::max<int64_t>(qq, 1));
+    if (qq > 0)
+      DME_CUDA(cudaMemcpy2DAsync(tmp.data(), c->n * 8, which ? c->Zc12f : c->Zc12h, c->ldn * 8,
+                                 c->n * 8, qq, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    for (int64_t j = 0; j < qq; ++j)
+      for (int64_t i = 0; i < c->n; ++i) L[i * qq + j] = tmp[(size_t)j * c->n + i];
+  });
+}
+
+dme_status dme_debug_matmul(int64_t M, int64_t N, int64_t K, const double* A, const double* B,
+                            double* C) {
+  return guarded(nullptr, [&] {
+    DME_REQUIRE(M > 0 && N > 0 && K > 0 && A && B && C, DME_ERR_INVALID, "bad matmul args");
+    const int64_t ldk = (K + 1) / 2 * 2;
+    double *dA, *dBT, *dC, *part;
+    int* cnt;
+    GemmScratch gs;
+    gs.max_grid = 256;
+    gs.max_tiles = 1 << 16;
+    DME_CUDA(cudaMalloc(&dA, M * ldk * 8));
+    DME_CUDA(cudaMalloc(&dBT, N * ldk * 8));
+    DME_CUDA(cudaMalloc(&dC, M * N * 8));
+    DME_CUDA(cudaMalloc(&part, GemmScratch::partial_doubles(gs.max_grid) * 8));
+    DME_CUDA(cudaMalloc(&cnt, gs.max_tiles * sizeof(int)));
+    DME_CUDA(cudaMemset(cnt, 0, gs.max_tiles * sizeof(int)));
+    gs.partial = part;
+    gs.counters = cnt;
+    DME_CUDA(cudaMemcpy2D(dA, ldk * 8, A, K * 8, K * 8, M, cudaMemcpyHostToDevice));
+    std::vector<double> bt((size_t)N * K);
+    for (int64_t i = 0; i < K; ++i)
+      for (int64_t j = 0; j < N; ++j) bt[j * K + i] = B[i * N + j];
+    DME_CUDA(cudaMemcpy2D(dBT, ldk * 8, bt.data(), K * 8, K * 8, N, cudaMemcpyHostToDevice));
+    GemmNTArgs g;
+    g.A = dA; g.lda = ldk; g.B = dBT; g.ldb = ldk;
+    g.M = M; g.N = N; g.K = K;
+    g.out = dC; g.out_rs = N; g.out_cs = 1;
+    gemm_nt(g, gs, 0);
+    DME_CUDA(cudaDeviceSynchronize());
+    DME_CUDA(cudaMemcpy(C, dC, M * N * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dA); cudaFree(dBT); cudaFree(dC); cudaFree(part); cudaFree(cnt);
+  });
+}
+
+}  // extern "C"

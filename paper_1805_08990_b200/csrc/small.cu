@@ -1,0 +1,322 @@
+// One-CTA kernels on the small (k x k) systems of the column compression and the Riccati flow.
+//
+// Square-root form used by the whole GPU path (DESIGN.md §"Factor form"): the state is Z with
+// P = Z Z^T, i.e. Z = L D^{1/2} of the paper's P = L D L^T. Column compression (P:L245-246:
+// "a reduced SVD factorization, followed by a diagonalization of the small resulting system") of
+// a concatenated factor Zc (n x k) is, in this form, ONE symmetric eigendecomposition of the Gram
+// matrix G = Zc^T Zc = W Theta W^T: Theta are the nonzero eigenvalues of P = Zc Zc^T (the squared
+// singular values of Zc, i.e. the eigenvalues of the paper's Sigma V^T D V Sigma), and
+//   Z_new = Zc W_kept,   P_new = Z_new Z_new^T,   kept = theta_i > tol * theta_max (reading G7),
+// at most `cap` of them, sorted by theta descending (reading G8). W is orthogonal, so the only
+// error besides the truncation is eps*||P|| (an orthogonal W is backward
+// stable at the level of P; a pivoted-Cholesky/RRQR of G is not — it loses eps*cond(Z1)).
+// Riccati flow T3 (eq:nonlinear P:L152, low-rank P:L156) in square-root form: with W = Z^T B,
+//   (I + tau P B R^-1 B^T)^-1 P = Z K^-1 Z^T,  K = I + F F^T,  F = sqrt(tau) W L_R^{-T}  (R = L_R L_R^T),
+//   Z <- Z K^{-1/2},  K^{-1/2} = I + F g(F^T F) F^T,  g(x) = ((1+x)^{-1/2} - 1)/x = -1/(s (1+s)), s = sqrt(1+x).
+// Both are fused into one kernel producing Tm (k x r): the caller then forms Z_new = Zc Tm.
+#include "common.cuh"
+#include "small.h"
+
+#include <cmath>
+
+namespace dme {
+
+namespace {
+
+constexpr int NT = 1024;
+
+__device__ __forceinline__ int pidx(int i, int j) {  // packed symmetric slot of the pair {i, j}
+  return i >= j ? (i * (i + 1)) / 2 + j : (j * (j + 1)) / 2 + i;
+}
+
+// g(A) for a tiny symmetric PSD A (m x m, row-major, destroyed), serial cyclic Jacobi; one thread.
+__device__ void tiny_sym_fun_g(double* A, double* out, int m) {
+  double V[SMALL_M_MAX * SMALL_M_MAX];
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) V[i * m + j] = i == j ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) off += A[p * m + q] * A[p * m + q];
+    if (off == 0.0) break;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = A[p * m + q];
+        if (apq == 0.0) continue;
+        const double th = (A[q * m + q] - A[p * m + p]) / (2.0 * apq);
+        const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(1.0 + th * th));
+        const double c = 1.0 / sqrt(1.0 + tt * tt), s = tt * c;
+        for (int k = 0; k < m; ++k) {
+          const double akp = A[k * m + p], akq = A[k * m + q];
+          A[k * m + p] = c * akp - s * akq;
+          A[k * m + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < m; ++k) {
+          const double apk = A[p * m + k], aqk = A[q * m + k];
+          A[p * m + k] = c * apk - s * aqk;
+          A[q * m + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < m; ++k) {
+          const double vkp = V[k * m + p], vkq = V[k * m + q];
+          V[k * m + p] = c * vkp - s * vkq;
+          V[k * m + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) {
+        const double x = A[l * m + l] > 0.0 ? A[l * m + l] : 0.0;
+        const double s = sqrt(1.0 + x);
+        acc += V[i * m + l] * (-1.0 / (s * (1.0 + s))) * V[j * m + l];
+      }
+      out[i * m + j] = acc;
+    }
+}
+
+// Parallel cyclic two-sided Jacobi (round-robin ordering) on the packed symmetric matrix S
+// (k x k, in shared memory); eigenvectors accumulated in V (k x k column-major, ldv, global).
+__device__ void jacobi_eig(double* S, int k, double* V, int64_t ldv, int* pos, double* cs,
+                           int* s_rot) {
+  const int tid = threadIdx.x;
+  const int ke = k + (k & 1);  // even count; index k (if any) is a dummy
+  const int np = ke / 2;
+  for (int e = tid; e < k * k; e += NT) V[(e % k) + (size_t)(e / k) * ldv] = (e % k == e / k) ? 1.0 : 0.0;
+  for (int i = tid; i < ke; i += NT) pos[i] = i;
+  __syncthreads();
+  double dmax = 0.0;
+  for (int i = 0; i < k; ++i) dmax = fmax(dmax, fabs(S[pidx(i, i)]));
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (tid == 0) *s_rot = 0;
+    __syncthreads();
+    for (int round = 0; round < ke - 1; ++round) {
+      // rotation parameters for pair I = (pos[I], pos[ke-1-I])
+      for (int I = tid; I < np; I += NT) {
+        int p = pos[I], q = pos[ke - 1 - I];
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0, t = 0.0;
+        if (q < k) {
+          const double apq = S[pidx(p, q)], app = S[pidx(p, p)], aqq = S[pidx(q, q)];
+          if (fabs(apq) > 1e-17 * sqrt(fabs(app * aqq)) && fabs(apq) > 1e-19 * dmax) {
+            const double th = (aqq - app) / (2.0 * apq);
+            t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(1.0 + th * th));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            atomicAdd(s_rot, 1);
+          }
+        }
+        cs[3 * I] = c;
+        cs[3 * I + 1] = s;
+        cs[3 * I + 2] = t;
+      }
+      __syncthreads();
+      // A <- J^T A J on the 2x2 blocks (I <= J), each block owned by one thread
+      const int nblk = np * (np + 1) / 2;
+      for (int e = tid; e < nblk; e += NT) {
+        int J = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+        while ((J + 1) * (J + 2) / 2 <= e) ++J;
+        while (J * (J + 1) / 2 > e) --J;
+        const int I = e - J * (J + 1) / 2;  // I <= J
+        int pI = pos[I], qI = pos[ke - 1 - I], pJ = pos[J], qJ = pos[ke - 1 - J];
+        if (pI > qI) { const int t = pI; pI = qI; qI = t; }
+        if (pJ > qJ) { const int t = pJ; pJ = qJ; qJ = t; }
+        const double cI = cs[3 * I], sI = cs[3 * I + 1], tI = cs[3 * I + 2];
+        const double cJ = cs[3 * J], sJ = cs[3 * J + 1];
+        if (I == J) {
+          if (qI < k && sI != 0.0) {
+            const double apq = S[pidx(pI, qI)];
+            S[pidx(pI, pI)] -= tI * apq;
+            S[pidx(qI, qI)] += tI * apq;
+            S[pidx(pI, qI)] = 0.0;
+          }
+          continue;
+        }
+        const bool vI = qI < k, vJ = qJ < k;
+        if (!vI && !vJ) continue;
+        // gather (dummy rows/cols read as 0 and are never written)
+        double x00 = S[pidx(pI, pJ)];
+        double x01 = vJ ? S[pidx(pI, qJ)] : 0.0;
+        double x10 = vI ? S[pidx(qI, pJ)] : 0.0;
+        double x11 = (vI && vJ) ? S[pidx(qI, qJ)] : 0.0;
+        // rows (pair I)
+        double r00 = cI * x00 - sI * x10, r01 = cI * x01 - sI * x11;
+        double r10 = sI * x00 + cI * x10, r11 = sI * x01 + cI * x11;
+        // columns (pair J)
+        const double y00 = cJ * r00 - sJ * r01, y01 = sJ * r00 + cJ * r01;
+        const double y10 = cJ * r10 - sJ * r11, y11 = sJ * r10 + cJ * r11;
+        S[pidx(pI, pJ)] = y00;
+        if (vJ) S[pidx(pI, qJ)] = y01;
+        if (vI) S[pidx(qI, pJ)] = y10;
+        if (vI && vJ) S[pidx(qI, qJ)] = y11;
+      }
+      // V <- V J
+      for (int e = tid; e < k * np; e += NT) {
+        const int i = e % k, J = e / k;
+        int pJ = pos[J], qJ = pos[ke - 1 - J];
+        if (pJ > qJ) { const int t = pJ; pJ = qJ; qJ = t; }
+        const double sJ = cs[3 * J + 1];
+        if (qJ >= k || sJ == 0.0) continue;
+        const double cJ = cs[3 * J];
+        double* vp = V + i + (size_t)pJ * ldv;
+        double* vq = V + i + (size_t)qJ * ldv;
+        const double a = *vp, b = *vq;
+        *vp = cJ * a - sJ * b;
+        *vq = sJ * a + cJ * b;
+      }
+      __syncthreads();
+      // round-robin: keep pos[0], rotate pos[1..ke-1]
+      if (tid == 0) {
+        const int last = pos[ke - 1];
+        for (int i = ke - 1; i > 1; --i) pos[i] = pos[i - 1];
+        pos[1] = last;
+      }
+      __syncthreads();
+    }
+    if (*s_rot == 0) break;
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT, 1) compress_t3_kernel(SmallArgs a) {
+  extern __shared__ double S[];  // packed symmetric k(k+1)/2
+  __shared__ int pos[SMALL_K_MAX + 1];
+  __shared__ double cs[3 * (SMALL_K_MAX / 2 + 1)];
+  __shared__ double theta[SMALL_K_MAX];
+  __shared__ int rnk[SMALL_K_MAX];
+  __shared__ int s_rot, s_r;
+  __shared__ double Gam[SMALL_M_MAX * SMALL_M_MAX];
+  __shared__ double Phi[SMALL_M_MAX * SMALL_M_MAX];
+
+  const int tid = threadIdx.x;
+  const int k = a.k;
+  const int m = a.m;
+  int r;
+
+  if (a.compress) {
+    for (int e = tid; e < k * k; e += NT) {
+      const int i = e % k, j = e / k;
+      if (i >= j) S[pidx(i, j)] = 0.5 * (a.G[i + (size_t)j * a.ldg] + a.G[j + (size_t)i * a.ldg]);
+    }
+    __syncthreads();
+    jacobi_eig(S, k, a.V, a.ldv, pos, cs, &s_rot);
+    for (int i = tid; i < k; i += NT) theta[i] = S[pidx(i, i)];
+    __syncthreads();
+    // descending order, ties by index
+    for (int i = tid; i < k; i += NT) {
+      int c = 0;
+      const double ti = theta[i];
+      for (int j = 0; j < k; ++j) c += (theta[j] > ti) || (theta[j] == ti && j < i);
+      rnk[i] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double tmax = -1e300;
+      for (int i = 0; i < k; ++i) tmax = fmax(tmax, theta[i]);
+      int cnt = 0;
+      for (int i = 0; i < k; ++i) cnt += (tmax > 0.0 && theta[i] > a.tol * tmax);
+      s_r = cnt < a.cap ? cnt : a.cap;
+      double drop = 0.0;
+      for (int i = 0; i < k; ++i)
+        if (rnk[i] >= s_r) drop = fmax(drop, fabs(theta[i]));
+      if (a.stats) {
+        a.stats[0] = (double)s_r;
+        a.stats[1] = tmax;
+        a.stats[2] = tmax > 0 ? drop / tmax : 0.0;
+      }
+    }
+    __syncthreads();
+    r = s_r;
+    for (int e = tid; e < k * k; e += NT) {
+      const int i = e % k, j = e / k;  // V column j -> Tm column rnk[j]
+      if (rnk[j] < r)
+        a.Tm[i + (size_t)rnk[j] * a.ldt] =
+            a.V[i + (size_t)j * a.ldv] * (a.sqrt_scale ? sqrt(fmax(theta[j], 0.0)) : 1.0);
+    }
+    __syncthreads();
+  } else {
+    r = k;
+    for (int e = tid; e < k * k; e += NT) {
+      const int i = e % k, c = e / k;
+      a.Tm[i + (size_t)c * a.ldt] = i == c ? 1.0 : 0.0;
+    }
+    if (tid == 0 && a.stats) { a.stats[0] = k; a.stats[1] = 0; a.stats[2] = 0; }
+    __syncthreads();
+  }
+
+  if (a.t3 && r > 0) {
+    double* Fs = S;                                  // the packed area is free now:
+    double* Wd = S + SMALL_K_MAX * SMALL_M_MAX;      // F (r x m), W / U (k x m)
+    // W = Tm^T H  (r x m),  H = Zc^T B  (k x m)
+    for (int e = tid; e < r * m; e += NT) {
+      const int c = e % r, mu = e / r;
+      double acc = 0.0;
+      for (int i = 0; i < k; ++i) acc += a.Tm[i + (size_t)c * a.ldt] * a.H[i + (size_t)mu * a.ldh];
+      Wd[c * m + mu] = acc;
+    }
+    __syncthreads();
+    // F = sqrt(tau) W Linv^T   (Linv = L_R^{-1}, m x m row-major)
+    for (int e = tid; e < r * m; e += NT) {
+      const int c = e / m, mu = e % m;
+      double acc = 0.0;
+      for (int nu2 = 0; nu2 < m; ++nu2) acc += Wd[c * m + nu2] * a.LRinv[mu * m + nu2];
+      Fs[c * m + mu] = sqrt(a.tau) * acc;
+    }
+    __syncthreads();
+    if (tid < m * m) {  // Phi = F^T F
+      const int mu = tid / m, nu2 = tid % m;
+      double acc = 0.0;
+      for (int c = 0; c < r; ++c) acc += Fs[c * m + mu] * Fs[c * m + nu2];
+      Phi[mu * m + nu2] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {  // Gamma = g(Phi)
+      if (m == 1) {
+        const double s = sqrt(1.0 + fmax(Phi[0], 0.0));
+        Gam[0] = -1.0 / (s * (1.0 + s));
+      } else {
+        tiny_sym_fun_g(Phi, Gam, m);
+      }
+    }
+    __syncthreads();
+    // U = Tm F (k x m), then Tm <- Tm + U Gamma F^T
+    for (int e = tid; e < k * m; e += NT) {
+      const int i = e / m, mu = e % m;
+      double acc = 0.0;
+      for (int c = 0; c < r; ++c) acc += a.Tm[i + (size_t)c * a.ldt] * Fs[c * m + mu];
+      Wd[i * m + mu] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < k * r; e += NT) {
+      const int i = e % k, c = e / k;
+      double acc = 0.0;
+      for (int mu = 0; mu < m; ++mu) {
+        double ug = 0.0;
+        for (int nu2 = 0; nu2 < m; ++nu2) ug += Wd[i * m + nu2] * Gam[nu2 * m + mu];
+        acc += ug * Fs[c * m + mu];
+      }
+      a.Tm[i + (size_t)c * a.ldt] += acc;
+    }
+  }
+  if (tid == 0) *a.r_out = r;
+}
+
+}  // namespace
+
+void compress_t3(const SmallArgs& a, cudaStream_t st) {
+  if (a.k > SMALL_K_MAX) throw std::runtime_error("compress_t3: k exceeds SMALL_K_MAX");
+  if (a.t3 && a.m > SMALL_M_MAX) throw std::runtime_error("compress_t3: m exceeds SMALL_M_MAX");
+  size_t smem = a.compress ? sizeof(double) * (size_t)a.k * (a.k + 1) / 2 : 0;
+  if (smem < sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX) smem = sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX;
+  static bool attr = false;
+  if (!attr) {
+    DME_CUDA(cudaFuncSetAttribute(compress_t3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SMALL_SMEM_MAX));
+    attr = true;
+  }
+  compress_t3_kernel<<<1, NT, smem, st>>>(a);
+  DME_KCHECK();
+}
+
+}  // namespace dme

@@ -1,0 +1,77 @@
+"""CPU-side checks of the boundary: the C-ABI library loads and exports every symbol declared
+in include/dme.h (no compute calls: there is no GPU here), and the host-side logic that needs
+no device (status strings, default options, argument validation paths) behaves."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "dme.h")).read()
+    return sorted(set(re.findall(r"\b(dme_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    import paper_1805_08990_b200 as dme
+    lib = ctypes.CDLL(dme.LIB_PATH)
+    declared = _declared_symbols()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(dme.EXPORTED) == declared
+
+
+def test_status_strings_and_defaults():
+    import paper_1805_08990_b200 as dme
+    lib = dme._lib
+    for code, text in dme.STATUS.items():
+        assert lib.dme_status_string(code).decode() == text
+    o = dme._Options()
+    lib.dme_default_options(ctypes.byref(o))
+    assert o.trunc_tol == 1e-16 and o.quad_nodes == 14 and o.quad_subpanels == 1 and o.world_size == 1
+
+
+def test_workspace_size_host_only():
+    import numpy as np
+    import paper_1805_08990_b200 as dme
+    n = 100
+    A = np.zeros((n, n))
+    pr = dme._Problem(n=n, A=A.ctypes.data_as(dme._dp), p=0, C=None, m=0, B=None, R=None, S=None,
+                      r0=0, L0=None, D0=None)
+    o = dme._Options()
+    dme._lib.dme_default_options(ctypes.byref(o))
+    nb = ctypes.c_size_t(0)
+    assert dme._lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(nb)) == 0
+    assert nb.value > 12 * n * n * 8
+    pr.n = 0
+    assert dme._lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(nb)) == 1
+    assert b"positive" in dme._lib.dme_last_error()
+
+
+def test_init_rejects_bad_input_without_device():
+    # validation happens before any CUDA call: a NaN in A or a bad h is rejected on the host
+    import numpy as np
+    import paper_1805_08990_b200 as dme
+    n = 8
+    A = np.eye(n)
+    A[0, 0] = np.nan
+    pr = dme._Problem(n=n, A=A.ctypes.data_as(dme._dp), p=0, C=None, m=0, B=None, R=None, S=None,
+                      r0=0, L0=None, D0=None)
+    o = dme._Options()
+    dme._lib.dme_default_options(ctypes.byref(o))
+    ctx = ctypes.c_void_p()
+    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+    A[0, 0] = 1.0
+    o.h = -1.0
+    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+    o.h = 0.01
+    R = np.array([[-1.0]])
+    B = np.ones((n, 1))
+    pr.m, pr.B, pr.R = 1, B.ctypes.data_as(dme._dp), R.ctypes.data_as(dme._dp)
+    assert dme._lib.dme_dre_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+    assert b"positive definite" in dme._lib.dme_last_error()
+    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1

@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Tolerances: kernel-level FP64 results 1e-12..1e-13 relative; every P
+comparison uses the QR-stacked relative Frobenius metric (oracle.lowrank.rel_diff) with the
+north-star bound 1e-10 (BASELINE.json north_star: "within relative Frobenius error 1e-10").
+"""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+pytestmark = pytest.mark.gpu
+
+from oracle import exact, flows, lowrank, quadrature  # noqa: E402
+from oracle.schemes import OracleOptions, OracleSolver  # noqa: E402
+from workloads import make_config, heat2d_matrix, convdiff2d_matrix  # noqa: E402
+
+TOL_P = 1e-10
+
+
+@pytest.fixture(scope="module")
+def dme():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1805_08990_b200 as m
+    return m
+
+
+def _solver(dme, prob, h, **kw):
+    return dme.Solver(**dme.problem_kwargs(prob), h=h, **kw)
+
+
+# ------------------------------------------------------------------ DMMA GEMM
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (130, 9, 37), (300, 77, 1000),
+                                   (257, 64, 2049), (1000, 200, 513), (129, 129, 129)])
+def test_matmul_vs_numpy(dme, M, N, K):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.standard_normal((M, K))
+    B = rng.standard_normal((K, N))
+    C = dme.matmul(A, B)
+    ref = A @ B
+    scale = np.abs(A) @ np.abs(B)
+    assert np.all(np.abs(C - ref) <= 1e-14 * K * scale + 1e-300)
+
+
+# ------------------------------------------------------------------ expm (Padé-13 + squaring)
+@pytest.mark.parametrize("nx,dim,h", [(100, 1, 1e-3), (12, 2, 5e-3), (33, 2, 5e-3)])
+def test_expm_heat_closed_form(dme, nx, dim, h):
+    prob = make_config(1, n=nx) if dim == 1 else make_config(2, nx=nx)
+    s = _solver(dme, prob, h)
+    for which, t in ((0, h / 2), (1, h)):
+        E = s.debug_get_exp(which)
+        ref = exact.heat_expm_closed_form(nx, t, dim)
+        assert np.abs(E - ref).max() <= 1e-13 * np.abs(ref).max(), (which, np.abs(E - ref).max())
+    st = s.stats()
+    A = prob.A
+    assert st["squarings"] == quadrature.squarings(A, h / 2)
+
+
+def test_expm_nonsymmetric_transpose_guard(dme):
+    prob = make_config(3, nx=14)
+    h = 5e-3
+    s = _solver(dme, prob, h)
+    E = s.debug_get_exp(0)
+    ref = sla.expm((h / 2) * prob.A.T)
+    assert np.abs(E - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert np.abs(E - sla.expm((h / 2) * prob.A)).max() > 1e-6
+
+
+# ------------------------------------------------------------------ quadrature factors
+@pytest.mark.parametrize("cfg,kw", [(5, dict(nx=12)), (3, dict(nx=10)), (2, dict(nx=9))])
+def test_integral_factor_vs_oracle(dme, cfg, kw):
+    prob = make_config(cfg, **kw)
+    h = 5e-3
+    q = 5 if cfg == 2 else 14
+    sp = 4 if cfg == 2 else 1
+    s = _solver(dme, prob, h, quad_nodes=q, quad_subpanels=sp)
+    op = flows.Operator(prob.A, "expm")
+    delta = quadrature.panel_width(prob.A, h, sp)
+    assert abs(s.stats()["panel_width"] - delta) <= 1e-15 * delta
+    LQ = prob.C.T
+    for which, tau in ((0, h / 2), (1, h)):
+        Lg = s.debug_get_integral(which)
+        Lo, Do = flows.build_integral(op, tau, delta, q, LQ, np.eye(LQ.shape[1]), 1e-16)
+        d = lowrank.rel_diff(Lg, np.eye(Lg.shape[1]), Lo, Do)
+        assert d <= 1e-12, (which, d)
+
+
+# ------------------------------------------------------------------ single flows
+def _state_after(dme, prob, h, flow, tau, L):
+    s = _solver(dme, prob, h)
+    s.debug_set_factor(L)
+    s.debug_apply(flow, tau)
+    return s.get_factor()
+
+
+def test_flows_vs_oracle(dme):
+    prob = make_config(4, nx=9)  # has B, S; P0 = 0
+    prob.L0 = np.random.default_rng(1).random((prob.n, 4))
+    prob.D0 = np.eye(4)
+    h = 5e-3
+    L = np.random.default_rng(2).random((prob.n, 6))
+    D = np.eye(6)
+    op = flows.Operator(prob.A, "expm")
+    LQ, DQ = prob.C.T, np.eye(prob.C.shape[0])
+    delta = quadrature.panel_width(prob.A, h)
+    cases = {
+        ("T1", h / 2): flows.T1(op, h / 2, L, D),
+        ("T1", h): flows.T1(op, h, L, D),
+        ("T2", h / 2): flows.T2(h / 2, L, D, LQ, DQ, 1e-16, None),
+        ("T3", h): flows.T3(h, L, D, prob.B, prob.R),
+        ("T4", h): flows.T4(h, L, D, prob.S, 2, 1e-16, None),
+        ("T4_euler", h): flows.T4(h, L, D, prob.S, 1, 1e-16, None),
+        ("T12", h / 2): flows.T12(op, h / 2, L, D, *flows.build_integral(
+            op, h / 2, delta, 14, LQ, DQ, 1e-16), 1e-16, None),
+        ("compress", 0.0): lowrank.column_compression(L, D, 1e-16),
+    }
+    for (flow, tau), (Lo, Do) in cases.items():
+        Lg, Dg = _state_after(dme, prob, h, flow, tau, L)
+        d = lowrank.rel_diff(Lg, Dg, Lo, Do)
+        assert d <= 1e-12, (flow, tau, d)
+
+
+def test_compress_rank_and_cap(dme):
+    prob = make_config(2, nx=8)
+    n = prob.n
+    rng = np.random.default_rng(3)
+    G = rng.standard_normal((n, 5))
+    L = np.hstack([G, G @ rng.standard_normal((5, 7)), G[:, :2]])  # numerical rank 5, 14 columns
+    Lg, Dg = _state_after(dme, prob, 5e-3, "compress", 0.0, L)
+    assert Lg.shape[1] == 5
+    assert lowrank.rel_diff(Lg, Dg, L, np.eye(L.shape[1])) <= 1e-13
+    s = _solver(dme, prob, 5e-3, rank_cap=3)
+    s.debug_set_factor(L)
+    s.debug_apply("compress", 0.0)
+    assert s.get_factor()[0].shape[1] == 3
+
+
+# ------------------------------------------------------------------ whole schemes
+SCHEME_CASES = [
+    (1, dict(n=100), "lie", "F1F2", 0.1, 40, {}),
+    (1, dict(n=100), "strang", "F1F2", 0.1, 40, {}),
+    (2, dict(nx=20), "strang", "F12", 0.5, 20, dict(quad_nodes=5, quad_subpanels=4)),
+    (2, dict(nx=20), "strang", "F1F2", 0.5, 20, {}),
+    (3, dict(nx=16), "strang", "F12F3", 0.5, 20, {}),
+    (3, dict(nx=16), "strang", "F1F2F3", 0.5, 20, {}),
+    (3, dict(nx=16), "strang", "F1F3F2", 0.5, 20, {}),
+    (3, dict(nx=16), "lie", "F12F3", 0.5, 20, {}),
+    (4, dict(nx=12), "strang", "F12F3F4", 0.5, 20, {}),
+    (4, dict(nx=12), "lie", "F12F3F4", 0.5, 20, {}),
+    (4, dict(nx=12), "strang", "F1F2F3F4", 0.5, 20, {}),
+    (4, dict(nx=12, dle=True), "strang", "F12F4", 0.5, 20, {}),
+    (4, dict(nx=12, dle=True), "strang", "F1F4F2", 0.5, 20, {}),
+    (5, dict(nx=24), "strang", "F12F3", 0.5, 20, dict(rank_cap=64)),
+]
+
+
+@pytest.mark.parametrize("cfg,kw,scheme,comp,T,N,opts", SCHEME_CASES)
+def test_scheme_vs_oracle(dme, cfg, kw, scheme, comp, T, N, opts):
+    prob = make_config(cfg, **kw)
+    h = T / N
+    s = _solver(dme, prob, h, **opts)
+    s.split_step(scheme, comp, N)
+    Lg, Dg = s.get_factor()
+    oo = OracleOptions(rank_cap=opts.get("rank_cap"), quad_nodes=opts.get("quad_nodes", 14),
+                       quad_subpanels=opts.get("quad_subpanels", 1))
+    orc = OracleSolver(prob, h, oo)
+    orc.step(scheme, comp, N)
+    Lo, Do = orc.factor()
+    d = lowrank.rel_diff(Lg, Dg, Lo, Do)
+    assert d <= TOL_P, (d, Lg.shape[1], Lo.shape[1])
+    P = Lg @ Dg @ Lg.T
+    assert np.allclose(P, P.T)
