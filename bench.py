@@ -1,0 +1,291 @@
+#!/usr/bin/env python
+"""bench.py — split steps/sec and time-to-T of the FP64 DRE at n = 10000 (BASELINE.json config 5).
+
+Workload (BASELINE.json configs[4]): 2D heat FD, n_x = 100 (n = 10^4), Q = C^T C with
+C 2 x n, P0 rank 5, B n x 1, R = 1 (uniform [0,1] seeded factors, workloads.make_config(5)),
+Strang F12F3 (T12(h/2) T3(h) T12(h/2)), rank cap 64, tol 1e-16, h = 0.005
+(T = 1/2, N_t = 100). One "step" = one Strang F12F3 step = the whole hot path (two E_{h/2} L
+passes, two compressions, one Riccati flow). E_{h/2} is 800 MB > L2 (126 MB): every pass streams
+it from HBM, no L2 flush needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (rows of E sharded, NCCL all-gather)
+
+Prints ONE JSON line (rank 0). `value` = steps/s (K steps / max-over-ranks device time).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "split steps/sec & time-to-T, n=10000 DRE FP64"
+UNIT = "steps/s"
+FP64_PEAK_TFLOPS = 36.6   # measured DMMA microbenchmark on this pool's B200 (profiles/r01_peaks_fp64.json)
+H, NT, RANK_CAP = 0.005, 100, 64
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def _traffic():
+    """dram bytes per E-pass launch from the committed ncu --set full capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "epass_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        try:
+            rows = [l.split(",") for l in open(self.path) if l.strip()]
+            sm = [float(r[0]) for r in rows]
+            out["sm_mhz"] = statistics.median(sm) if sm else None
+            out["sm_max_mhz"] = float(rows[0][1]) if rows else None
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for i, nm in enumerate(names):
+                if any(r[3 + i].strip() == "Active" for r in rows):
+                    out["reasons"].append(nm)
+            out["samples"] = len(rows)
+        except Exception:
+            pass
+        return out
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(prob, steps: int):
+    """The oracle (dense E_tau L products, SVD compression) timed on this host's cores."""
+    from oracle.schemes import OracleOptions, OracleSolver
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    orc = OracleSolver(prob, H, OracleOptions(rank_cap=RANK_CAP), dense_apply=True)
+    orc.step("strang", "F12F3", 1)          # builds E_{h/2}, L_I(h/2) (not timed)
+    t1 = time.perf_counter()
+    orc.step("strang", "F12F3", steps)
+    t2 = time.perf_counter()
+    return {"value": steps / (t2 - t1), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{steps} Strang F12F3 steps of config 5 (n={prob.n}) after a warm-up step; "
+                      f"oracle setup {t1 - t0:.1f}s untimed; NumPy/OpenBLAS threads = all cores"}
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    from workloads import make_config
+    prob = make_config(5)
+    cb = cpu_baseline(prob, max(1, args.steps))
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config5: DRE 2D heat n=10000, Strang F12F3, rank cap 64, h=0.005"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1805_08990_b200 as dme
+    from workloads import make_config
+
+    prob = make_config(5, nx=args.nx)
+    uid = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(dme.unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        uid = bytes(buf.cpu().numpy().tobytes())
+    kw = dict(h=H, rank_cap=RANK_CAP, world_size=world, world_rank=rank, nccl_uid=uid)
+
+    # ------------------------------------------------------------ device-resident timed region
+    torch.cuda.synchronize()
+    t_init0 = time.perf_counter()
+    s = dme.Solver(**dme.problem_kwargs(prob), **kw)
+    torch.cuda.synchronize()
+    init_wall = time.perf_counter() - t_init0
+    s.split_step("strang", "F12F3", args.warmup)
+    torch.cuda.synchronize()
+    s.set_profiling(True)
+    launches0 = s.stats()["kernel_launches"]
+    stream = s.stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        s.split_step("strang", "F12F3", args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    st = s.stats()
+    launches = st["kernel_launches"] - launches0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = args.steps / (ms * 1e-3)
+    rank_now = st["rank"]
+    init_dev = st["init_seconds"]
+    s.close()
+    del s
+    torch.cuda.empty_cache()
+
+    # ------------------------------------------------------------ roofline of the dominant kernel
+    ep_s, ep_f, ep_b, npass = (st["prof_epass_seconds"], st["prof_epass_flops"],
+                               st["prof_epass_bytes"], st["prof_passes"])
+    achieved_tf = ep_f / ep_s / 1e12 if ep_s > 0 else None
+    achieved_gbs = ep_b / ep_s / 1e9 if ep_s > 0 else None
+    peaks = _peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    tr = _traffic()
+    roofline = {"bound": "tensor", "kernel": "gemm_nt (E_{h/2} L, FP64 DMMA)",
+                "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": (achieved_tf / FP64_PEAK_TFLOPS) if achieved_tf else None,
+                "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_peaks_fp64.json); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm_peak,
+                             "frac": (achieved_gbs / hbm_peak) if achieved_gbs else None},
+                "algorithmic_per_launch": {"flops": ep_f / max(npass, 1), "bytes": ep_b / max(npass, 1)},
+                "share_of_step": ep_s / (ms * 1e-3) if ms > 0 else None,
+                "gram_share": st["prof_gram_seconds"] / (ms * 1e-3),
+                "small_eig_share": st["prof_small_seconds"] / (ms * 1e-3),
+                "apply_share": st["prof_apply_seconds"] / (ms * 1e-3),
+                "passes_timed": npass}
+
+    # ------------------------------------------------------------ end to end through the public API
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        s2 = dme.Solver(**dme.problem_kwargs(prob), **kw)          # H2D of A, C, B, R, L0
+        s2.split_step("strang", "F12F3", NT)
+        L, D = s2.get_factor()                                      # D2H of the factor
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        h2d = sum(a.nbytes for a in (prob.A, prob.C, prob.B, prob.R, prob.L0, prob.D0) if a is not None)
+        e2e = {"value": NT / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d / NT,
+               "d2h_bytes_per_step": (L.nbytes + D.nbytes) / NT, "time_to_T_s": t_e2e,
+               "what": "N_t=100 steps/(wall time of dme_dre_init from host arrays + 100 steps + "
+                       "dme_get_factor to host): time-to-T end to end"}
+        s2.close()
+        del s2
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cb = cpu_baseline(prob, 2)
+        except Exception as ex:  # reported, never fatal
+            cb = {"error": repr(ex)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "config5: DRE 2D heat n=10000 (n_x=100), Strang F12F3, "
+                                       "rank cap 64, tol 1e-16, h=0.005 (T=0.5, N_t=100)",
+                           "n": prob.n, "rank_after_timed_steps": rank_now,
+                           "l2": "inputs larger than L2 (E_{h/2} = 800 MB streamed per pass)",
+                           "parallelism": f"rows of E sharded over {world} GPU(s)"},
+                "time_to_T_s": init_dev + NT * ms_step * 1e-3,
+                "init_s": init_dev, "init_wall_s": init_wall,
+                "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nx", type=int, default=100, help="(debug) grid size; default = config 5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

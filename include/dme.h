@@ -116,6 +116,17 @@ typedef struct {
   int64_t e_passes;         /* number of E*L actions (T1/T12/T4 passes)                        */
   int64_t compressions;
   double init_seconds;      /* host wall time of the init call                                 */
+  int64_t kernel_launches;  /* kernels launched by the library in this process so far          */
+  /* device-time accounting, filled only while profiling is on (dme_set_profiling) */
+  int64_t prof_passes;      /* E*L / S*L passes timed                                          */
+  double prof_epass_seconds;/* summed CUDA-event duration of those passes                      */
+  double prof_epass_flops;  /* algorithmic flops of those passes: 2 * rows * n * k each        */
+  double prof_epass_bytes;  /* algorithmic bytes: 8 * rows * n each (the dense matrix, read once) */
+  double prof_gram_seconds; /* Gram matrices Zc^T Zc (and Zc^T B)                              */
+  double prof_small_seconds;/* one-CTA eigen-compression / Riccati kernel                      */
+  double prof_apply_seconds;/* Zc * Tm                                                         */
+  int64_t eig_fallbacks;    /* fast eigen-compressions that failed the orthogonality check and
+                               were redone by the Jacobi kernel                                 */
 } dme_stats;
 
 void dme_default_options(dme_options* opt);
@@ -139,6 +150,8 @@ dme_status dme_split_step(dme_ctx* ctx, dme_scheme scheme, dme_composition comp,
  * with P = L D L^T. Returns DME_ERR_CAPACITY (and sets *r) when r > capacity_cols. */
 dme_status dme_get_factor(dme_ctx* ctx, int64_t* r, double* L, double* D, int64_t capacity_cols);
 dme_status dme_get_stats(dme_ctx* ctx, dme_stats* st);
+/* Turn CUDA-event timing of the kernel classes on (1) or off (0); resets the prof_* counters. */
+dme_status dme_set_profiling(dme_ctx* ctx, int32_t on);
 dme_status dme_destroy(dme_ctx* ctx);
 
 /* ---- test hooks (same semantics as the step, one flow at a time) ----------------------------- */

@@ -21,8 +21,11 @@ class Operator:
                       for 1D (n = nx) or 2D (n = nx^2, index i*nx+j) problems
     """
 
-    def __init__(self, A, method="auto", heat_nx=None, heat_dim=None):
+    def __init__(self, A, method="auto", heat_nx=None, heat_dim=None, dense_apply=False):
         self.A = np.asarray(A, dtype=np.float64)
+        # dense_apply: T1/T12 actions multiply by the dense matrix exp(tau A^T) (the north star's
+        # dense-E formulation); quadrature node actions keep the exact structured route.
+        self.dense_apply = dense_apply
         n = self.A.shape[0]
         if method == "auto":
             if heat_nx is not None:
@@ -51,7 +54,7 @@ class Operator:
             return self.Vx @ X
         nx = self.nx
         Y = X.T.reshape(-1, nx, nx)
-        return np.einsum("ai,kij,jb->kab", self.Vx, Y, self.Vx).reshape(-1, nx * nx).T
+        return np.matmul(np.matmul(self.Vx, Y), self.Vx).reshape(-1, nx * nx).T
 
     def _from_eig(self, Y):
         return self._to_eig(Y)  if self.method == "heat" else self.V @ Y
@@ -66,6 +69,23 @@ class Operator:
                     np.eye(self.A.shape[0])))
         return self._E[t]
 
+    def E_dense(self, t):
+        """Dense exp(t A^T); for the 2D heat hint via the closed-form 1D factor E1 (x) E1."""
+        if self.method == "heat" and self.dim == 2:
+            if ("k", t) not in self._E:
+                j = np.arange(1, self.nx + 1)
+                lx = -4.0 * (self.nx + 1) ** 2 * np.sin(j * np.pi / (2 * (self.nx + 1))) ** 2
+                E1 = (self.Vx * np.exp(t * lx)[None, :]) @ self.Vx
+                self._E[("k", t)] = np.kron(E1, E1)
+            return self._E[("k", t)]
+        return self.E(t)
+
+    def apply_step(self, t, X):
+        """exp(t A^T) X for the step flows T1 / T12 (dense product when dense_apply)."""
+        if self.dense_apply and X.shape[1]:
+            return self.E_dense(t) @ X
+        return self.apply(t, X)
+
     def apply(self, t, X):
         """exp(t A^T) X."""
         if X.shape[1] == 0:
@@ -78,7 +98,7 @@ class Operator:
 def T1(op, tau, L, D):
     """Linear flow F1(P) = A^T P + P A: T1(tau) P0 = e^{tau A^T} P0 e^{tau A}
     (P:L110); factorised as (e^{tau A^T} L) D (e^{tau A^T} L)^T (eq:F_sol_LDL)."""
-    return op.apply(tau, L), D
+    return op.apply_step(tau, L), D
 
 
 def T2(tau, L, D, LQ, DQ, tol, cap):
@@ -133,5 +153,5 @@ def T12(op, tau, L, D, LI, DI, tol, cap):
     """Affine flow F12(P) = A^T P + P A + Q, exact solution eq:full with the
     integral replaced by the precomputed quadrature factor: Alg. 2 loop
     L <- [exp(tau A^T) L, L_I], D <- blkdiag(D, D_I), column compression."""
-    L2, D2 = lowrank.concat(op.apply(tau, L), D, LI, DI, 1.0)
+    L2, D2 = lowrank.concat(op.apply_step(tau, L), D, LI, DI, 1.0)
     return lowrank.column_compression(L2, D2, tol, cap)

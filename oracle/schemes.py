@@ -49,11 +49,11 @@ class OracleOptions:
 class OracleSolver:
     """Runs a splitting scheme on a workloads.Problem in LDL^T form."""
 
-    def __init__(self, prob, h, opts=OracleOptions(), method="auto"):
+    def __init__(self, prob, h, opts=OracleOptions(), method="auto", dense_apply=False):
         self.p = prob
         self.h = h
         self.o = opts
-        self.op = flows.Operator(prob.A, method, prob.heat_nx, prob.heat_dim)
+        self.op = flows.Operator(prob.A, method, prob.heat_nx, prob.heat_dim, dense_apply)
         n = prob.n
         if prob.C is not None and prob.C.shape[0] > 0:
             self.LQ, self.DQ = prob.C.T.copy(), np.eye(prob.C.shape[0])   # Q = C^T C (G11)

@@ -56,7 +56,11 @@ class _Stats(ctypes.Structure):
                 ("quad_panels", ctypes.c_int32), ("panel_width", ctypes.c_double),
                 ("pade_min_pivot", ctypes.c_double), ("last_drop", ctypes.c_double),
                 ("e_passes", ctypes.c_int64), ("compressions", ctypes.c_int64),
-                ("init_seconds", ctypes.c_double)]
+                ("init_seconds", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
+                ("prof_passes", ctypes.c_int64), ("prof_epass_seconds", ctypes.c_double),
+                ("prof_epass_flops", ctypes.c_double), ("prof_epass_bytes", ctypes.c_double),
+                ("prof_gram_seconds", ctypes.c_double), ("prof_small_seconds", ctypes.c_double),
+                ("prof_apply_seconds", ctypes.c_double), ("eig_fallbacks", ctypes.c_int64)]
 
 
 _ctx_p = ctypes.c_void_p
@@ -72,6 +76,7 @@ for _name, _args in {
     "dme_split_step": [_ctx_p, ctypes.c_int, ctypes.c_int, ctypes.c_int64],
     "dme_get_factor": [_ctx_p, ctypes.POINTER(ctypes.c_int64), _dp, _dp, ctypes.c_int64],
     "dme_get_stats": [_ctx_p, ctypes.POINTER(_Stats)],
+    "dme_set_profiling": [_ctx_p, ctypes.c_int32],
     "dme_destroy": [_ctx_p],
     "dme_debug_apply": [_ctx_p, ctypes.c_int32, ctypes.c_double],
     "dme_debug_set_factor": [_ctx_p, ctypes.c_int64, _dp],
@@ -85,7 +90,7 @@ for _name, _args in {
 
 EXPORTED = ["dme_default_options", "dme_status_string", "dme_last_error", "dme_workspace_size",
             "dme_get_unique_id", "dme_dle_init", "dme_dre_init", "dme_split_step",
-            "dme_get_factor", "dme_get_stats", "dme_destroy", "dme_debug_apply",
+            "dme_get_factor", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
             "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_get_integral",
             "dme_debug_matmul"]
 
@@ -188,6 +193,9 @@ class Solver:
         s = _Stats()
         _check(_lib.dme_get_stats(self._ctx, ctypes.byref(s)), "dme_get_stats")
         return {f: getattr(s, f) for f, _ in _Stats._fields_}
+
+    def set_profiling(self, on: bool):
+        _check(_lib.dme_set_profiling(self._ctx, 1 if on else 0), "dme_set_profiling")
 
     # ---------------------------------------------------------------- test hooks
     def debug_apply(self, flow: str, tau: float):

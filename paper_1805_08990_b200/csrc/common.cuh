@@ -21,7 +21,13 @@ struct CudaError : std::runtime_error {
       throw ::dme::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " @ " +  \
                              __FILE__ + ":" + std::to_string(__LINE__));                 \
   } while (0)
-#define DME_KCHECK() DME_CUDA(cudaGetLastError())
+void note_launch();            // counts every kernel launch of the library
+int64_t launch_count();
+#define DME_KCHECK()                    \
+  do {                                  \
+    ::dme::note_launch();               \
+    DME_CUDA(cudaGetLastError());       \
+  } while (0)
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

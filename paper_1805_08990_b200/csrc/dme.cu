@@ -49,6 +49,7 @@ const double PADE_B[14] = {64764752532480000.0, 32382376266240000.0, 77717703038
 const double THETA13 = 5.371920351148152;
 
 constexpr int64_t KMAX = SMALL_K_MAX;  // column capacity of every factor buffer
+constexpr double GRAM_FLOOR = 1e-14;    // effective relative truncation floor of the Gram eigen-compression
 
 // Gauss-Legendre nodes/weights on [0,1] by Newton on P_q (Golub-Welsch-free; own implementation)
 void gauss_legendre01(int q, std::vector<double>& c, std::vector<double>& w) {
@@ -119,7 +120,13 @@ struct dme_ctx {
   std::vector<double> lrinv_host;
   dme_stats stats{};
   bool poisoned = false;
+  bool force_jacobi = false;
   ncclComm_t comm = nullptr;
+  // profiling: (start, stop, class, flops, bytes) event records drained at sync points
+  bool profile = false;
+  struct Rec { cudaEvent_t a, b; int cls; double flops, bytes; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
 };
 
 namespace {
@@ -285,6 +292,59 @@ void check_psd_host(const double* D, int64_t r) {
 
 void sync(dme_ctx* c) { DME_CUDA(cudaStreamSynchronize(c->st)); }
 
+// ------------------------------------------------------------------ profiling (CUDA events)
+enum { PROF_EPASS = 0, PROF_GRAM = 1, PROF_SMALL = 2, PROF_APPLY = 3 };
+cudaEvent_t take_event(dme_ctx* c) {
+  if (c->pool.empty()) {
+    cudaEvent_t e;
+    DME_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = c->pool.back();
+  c->pool.pop_back();
+  return e;
+}
+struct ProfScope {
+  dme_ctx* c;
+  dme_ctx::Rec r{};
+  ProfScope(dme_ctx* cc, int cls, double flops = 0, double bytes = 0) : c(cc) {
+    if (!c->profile) return;
+    r.a = take_event(c);
+    r.b = take_event(c);
+    r.cls = cls;
+    r.flops = flops;
+    r.bytes = bytes;
+    DME_CUDA(cudaEventRecord(r.a, c->st));
+  }
+  ~ProfScope() {
+    if (!c->profile) return;
+    cudaEventRecord(r.b, c->st);
+    c->pending.push_back(r);
+  }
+};
+void drain_profile(dme_ctx* c) {
+  for (auto& r : c->pending) {
+    DME_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0;
+    DME_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    const double s = ms * 1e-3;
+    switch (r.cls) {
+      case PROF_EPASS:
+        c->stats.prof_passes++;
+        c->stats.prof_epass_seconds += s;
+        c->stats.prof_epass_flops += r.flops;
+        c->stats.prof_epass_bytes += r.bytes;
+        break;
+      case PROF_GRAM: c->stats.prof_gram_seconds += s; break;
+      case PROF_SMALL: c->stats.prof_small_seconds += s; break;
+      default: c->stats.prof_apply_seconds += s; break;
+    }
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->pending.clear();
+}
+
 // ------------------------------------------------------------------ building blocks
 // out (col-major, ldo) = alpha * E * X  (E: n x n row-major, X: n x k col-major), sharded over ranks
 void epass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t ldo,
@@ -296,12 +356,14 @@ void epass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out,
     g.A = E; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
     g.M = c->n; g.N = k; g.K = c->n; g.alpha = alpha;
     g.out = out; g.out_rs = 1; g.out_cs = ldo;
+    ProfScope ps(c, PROF_EPASS, 2.0 * c->n * c->n * k, 8.0 * c->n * c->n);
     gemm_nt(g, c->gs, c->st);
     return;
   }
   // row shard: local rows into this rank's staging block (nloc x k, col-major), allgather, unpack
   double* mine = c->stage + (size_t)c->rank * c->nloc * k;
   if (c->rows_loc > 0) {
+    ProfScope ps(c, PROF_EPASS, 2.0 * c->rows_loc * c->n * k, 8.0 * c->rows_loc * c->n);
     GemmNTArgs g;
     g.A = E + c->row0 * c->ldn; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
     g.M = c->rows_loc; g.N = k; g.K = c->n; g.alpha = alpha;
@@ -324,6 +386,7 @@ int64_t compress(dme_ctx* c, const double* Zc, int64_t k, double* out, bool t3, 
   DME_REQUIRE(k <= KMAX, DME_ERR_DIM, "factor width exceeds the small-system limit (224)");
   c->stats.compressions += do_compress ? 1 : 0;
   if (do_compress) {
+    ProfScope ps(c, PROF_GRAM);
     GemmNTArgs g;
     g.A = Zc; g.lda = c->ldn; g.B = Zc; g.ldb = c->ldn;
     g.M = k; g.N = k; g.K = c->n;
@@ -331,6 +394,7 @@ int64_t compress(dme_ctx* c, const double* Zc, int64_t k, double* out, bool t3, 
     gemm_nt(g, c->gs, c->st);
   }
   if (t3) {
+    ProfScope ps(c, PROF_GRAM);
     GemmNTArgs g;
     g.A = Zc; g.lda = c->ldn; g.B = c->Bcol; g.ldb = c->ldn;
     g.M = k; g.N = c->m; g.K = c->n;
@@ -341,7 +405,9 @@ int64_t compress(dme_ctx* c, const double* Zc, int64_t k, double* out, bool t3, 
   a.k = (int)k;
   a.compress = do_compress ? 1 : 0;
   a.G = c->G; a.ldg = KMAX;
-  a.tol = c->opt.trunc_tol;
+  // The Gram matrix resolves eigenvalues of P only down to ~k*eps*theta_max: directions below the
+  // floor are numerically zero for this formulation (reading G7').
+  a.tol = std::max(c->opt.trunc_tol, GRAM_FLOOR);
   a.cap = c->rank_cap;
   a.t3 = t3 ? 1 : 0;
   a.m = (int)c->m;
@@ -352,14 +418,32 @@ int64_t compress(dme_ctx* c, const double* Zc, int64_t k, double* out, bool t3, 
   a.V = c->Vg; a.ldv = KMAX;
   a.r_out = c->r_dev;
   a.stats = c->sstats;
-  compress_t3(a, c->st);
   int r_host = 0;
-  double st_host[3];
+  double st_host[5] = {0, 0, 0, 0, 0};
+  const bool fast = do_compress && k <= FAST_K_MAX && !c->force_jacobi;
+  {
+    ProfScope ps(c, PROF_SMALL);
+    if (fast) eig_fast(a, c->st); else compress_t3(a, c->st);
+  }
   DME_CUDA(cudaMemcpyAsync(&r_host, c->r_dev, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  DME_CUDA(cudaMemcpyAsync(st_host, c->sstats, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  DME_CUDA(cudaMemcpyAsync(st_host, c->sstats, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   sync(c);
+  if (fast && r_host < 0) {  // near-degenerate cluster: orthogonality check failed -> Jacobi
+    c->stats.eig_fallbacks++;
+    {
+      ProfScope ps(c, PROF_SMALL);
+      compress_t3(a, c->st);
+    }
+    DME_CUDA(cudaMemcpyAsync(&r_host, c->r_dev, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    DME_CUDA(cudaMemcpyAsync(st_host, c->sstats, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  }
   if (do_compress) c->stats.last_drop = st_host[2];
-  if (r_host > 0) tall_small(Zc, c->ldn, c->Tm, KMAX, out, c->ldn, c->n, r_host, k, c->st);
+  if (r_host > 0) {
+    ProfScope ps(c, PROF_APPLY);
+    tall_small(Zc, c->ldn, c->Tm, KMAX, out, c->ldn, c->n, r_host, k, c->st);
+  }
+  if (c->profile) drain_profile(c);
   return r_host;
 }
 
@@ -843,13 +927,29 @@ dme_status dme_get_factor(dme_ctx* c, int64_t* r, double* L, double* D, int64_t 
 
 dme_status dme_get_stats(dme_ctx* c, dme_stats* st) {
   if (!c || !st) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
-  c->stats.rank = c->r;
-  *st = c->stats;
-  return DME_OK;
+  return guarded(c, [&] {
+    drain_profile(c);
+    c->stats.rank = c->r;
+    c->stats.kernel_launches = launch_count();
+    *st = c->stats;
+  });
+}
+
+dme_status dme_set_profiling(dme_ctx* c, int32_t on) {
+  if (!c) { g_last_error = "NULL ctx"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    drain_profile(c);
+    c->profile = on != 0;
+    c->stats.prof_passes = 0;
+    c->stats.prof_epass_seconds = c->stats.prof_epass_flops = c->stats.prof_epass_bytes = 0;
+    c->stats.prof_gram_seconds = c->stats.prof_small_seconds = c->stats.prof_apply_seconds = 0;
+  });
 }
 
 dme_status dme_destroy(dme_ctx* c) {
   if (!c) return DME_OK;
+  for (auto& r : c->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c->pool) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return DME_OK;

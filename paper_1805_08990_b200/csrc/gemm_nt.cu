@@ -17,6 +17,7 @@
 #include "gemm_nt.h"
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 
 namespace dme {
@@ -324,6 +325,12 @@ CUtensorMap make_tmap_3d(const double* base, uint64_t d0, uint64_t d1, uint64_t 
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
   return m;
 }
+
+namespace {
+std::atomic<int64_t> g_launches{0};
+}
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {
   static int n = [] {

@@ -130,6 +130,7 @@ void lu_nopiv_solve_right(double* Q, double* P, int64_t n, int64_t ld, double* Q
     attr = true;
   }
   init_minpiv<<<1, 1, 0, st>>>(minpiv_dev);
+  DME_KCHECK();
   auto Linv = [&](int64_t b) { return inv + (size_t)b * 3 * NB * NB; };
   auto LinvT = [&](int64_t b) { return inv + (size_t)b * 3 * NB * NB + NB * NB; };
   auto UinvT = [&](int64_t b) { return inv + (size_t)b * 3 * NB * NB + 2 * NB * NB; };

@@ -5,7 +5,8 @@
 namespace dme {
 
 constexpr int SMALL_K_MAX = 224;          // packed k(k+1)/2 doubles fit in 201 KB of shared memory
-constexpr int SMALL_M_MAX = 8;            // columns of B handled by the fused Riccati flow
+constexpr int SMALL_M_MAX = 8;
+constexpr int FAST_K_MAX = 160;           // fast tridiagonal eigen-compression: k x (k|1) in smem            // columns of B handled by the fused Riccati flow
 constexpr int SMALL_SMEM_MAX = SMALL_K_MAX * (SMALL_K_MAX + 1) / 2 * 8;
 
 struct SmallArgs {
@@ -27,9 +28,11 @@ struct SmallArgs {
   double* Tm = nullptr;      // out: k x r column-major, leading dim ldt
   int64_t ldt = 0;
   int* r_out = nullptr;      // out: new rank (device)
-  double* stats = nullptr;   // out: [rank, max diag G, max remaining pivot / max diag]
+  double* stats = nullptr;   // out: [rank, theta_max, largest dropped / theta_max, fallback, orth err]
+  double orth_tol = 1e-12;   // fast path: max weighted |W^T W - I| before falling back to Jacobi
 };
 
-void compress_t3(const SmallArgs& a, cudaStream_t st);
+void compress_t3(const SmallArgs& a, cudaStream_t st);  // Jacobi (any k <= SMALL_K_MAX)
+void eig_fast(const SmallArgs& a, cudaStream_t st);     // k <= FAST_K_MAX; *r_out = -1 => fall back
 
 }  // namespace dme

@@ -170,3 +170,33 @@ def test_scheme_vs_oracle(dme, cfg, kw, scheme, comp, T, N, opts):
     assert d <= TOL_P, (d, Lg.shape[1], Lo.shape[1])
     P = Lg @ Dg @ Lg.T
     assert np.allclose(P, P.T)
+
+
+@pytest.mark.parametrize("case", ["graded", "degenerate", "wide"])
+def test_compress_eigen_paths(dme, case):
+    """Fast tridiagonal eigen-compression (k <= 160) and its Jacobi fallback (exact degeneracy,
+    k > 160) against the oracle's SVD + diagonalisation."""
+    prob = make_config(2, nx=14)
+    n = prob.n
+    rng = np.random.default_rng({"graded": 5, "degenerate": 6, "wide": 7}[case])
+    if case == "graded":     # k = 90, spectrum graded over 16 decades
+        L = rng.standard_normal((n, 90)) * np.logspace(0, -8, 90)[None, :]
+    elif case == "degenerate":  # orthogonal columns with repeated norms -> repeated eigenvalues
+        Q, _ = np.linalg.qr(rng.standard_normal((n, 40)))
+        L = Q * np.repeat([1.0, 0.5, 0.25, 0.125], 10)[None, :]
+    else:                    # k = 180 > FAST_K_MAX: Jacobi path
+        L = rng.standard_normal((n, 180)) * np.logspace(0, -6, 180)[None, :]
+    s = _solver(dme, prob, 5e-3)
+    f0 = s.stats()["eig_fallbacks"]
+    s.debug_set_factor(L)
+    s.debug_apply("compress", 0.0)
+    Lg, Dg = s.get_factor()
+    Lo, Do = lowrank.column_compression(L, np.eye(L.shape[1]), 1e-16)
+    assert lowrank.rel_diff(Lg, Dg, Lo, Do) <= 1e-13
+    G = Lg.T @ Lg  # compressed columns are orthogonal (W orthogonal): G diagonal
+    off = G - np.diag(np.diag(G))
+    assert np.abs(off).max() <= 1e-12 * np.abs(G).max()
+    if case == "degenerate":
+        assert s.stats()["eig_fallbacks"] >= f0 + 1
+    if case == "graded":
+        assert s.stats()["eig_fallbacks"] == f0
