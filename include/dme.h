@@ -100,6 +100,9 @@ typedef struct {
   const void* nccl_uid;   /* 128-byte ncclUniqueId from dme_get_unique_id on rank 0           */
   void* workspace;        /* device buffer, >= dme_workspace_size bytes, 256-byte aligned     */
   size_t workspace_bytes;
+  int32_t no_fsal;        /* 0 (default): within one dme_split_step call, merge the trailing
+                             T1/T12(h/2) of a Strang step with the leading one of the next step
+                             (first-same-as-last); 1: apply every sub-step as written           */
 } dme_options;
 
 typedef struct {
@@ -168,6 +171,9 @@ dme_status dme_debug_get_exp(dme_ctx* ctx, int32_t which, double* E);
 /* Copy L_I(h/2) (which = 0) or L_I(h) (which = 1), P_I = L_I L_I^T, n x q, to the host. */
 dme_status dme_debug_get_integral(dme_ctx* ctx, int32_t which, int64_t* q, double* L,
                                   int64_t capacity_cols);
+/* Copy the 16 diagnostic doubles of the last small-system kernel (rank, theta_max, drop ratio,
+ * fallback flag, orthogonality error, -, -, -, per-phase clock cycles of the fast eigen path). */
+dme_status dme_debug_small_stats(dme_ctx* ctx, double* out16);
 /* C (M x N) = A (M x K) * B (K x N) through the library's DMMA GEMM (host buffers). */
 dme_status dme_debug_matmul(int64_t M, int64_t N, int64_t K, const double* A, const double* B,
                             double* C);

@@ -46,7 +46,8 @@ class _Options(ctypes.Structure):
                 ("quad_subpanels", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("world_size", ctypes.c_int32),
                 ("world_rank", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
-                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("no_fsal", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -84,6 +85,7 @@ for _name, _args in {
     "dme_debug_get_integral": [_ctx_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), _dp,
                                ctypes.c_int64],
     "dme_debug_matmul": [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp],
+    "dme_debug_small_stats": [_ctx_p, _dp],
 }.items():
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = ctypes.c_int
@@ -92,7 +94,7 @@ EXPORTED = ["dme_default_options", "dme_status_string", "dme_last_error", "dme_w
             "dme_get_unique_id", "dme_dle_init", "dme_dre_init", "dme_split_step",
             "dme_get_factor", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
             "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_get_integral",
-            "dme_debug_matmul"]
+            "dme_debug_small_stats", "dme_debug_matmul"]
 
 
 class DmeError(RuntimeError):
@@ -139,7 +141,7 @@ class Solver:
 
     def __init__(self, A, C=None, L0=None, D0=None, B=None, R=None, S=None, *, h, trunc_tol=1e-16,
                  rank_cap=0, quad_nodes=14, quad_subpanels=1, device=None, stream=None,
-                 world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None):
+                 world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None, fsal=True):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1805_08990_b200.Solver needs a CUDA device (no CPU fallback)")
@@ -161,7 +163,7 @@ class Solver:
                        quad_subpanels=quad_subpanels, device=dev.index,
                        stream=self.stream.cuda_stream, world_size=world_size,
                        world_rank=world_rank, nccl_uid=ctypes.cast(uid, ctypes.c_void_p) if uid else None,
-                       workspace=None, workspace_bytes=0)
+                       workspace=None, workspace_bytes=0, no_fsal=0 if fsal else 1)
         nbytes = ctypes.c_size_t(0)
         _check(_lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(opt), ctypes.byref(nbytes)),
                "dme_workspace_size")
@@ -217,6 +219,11 @@ class Solver:
         _check(_lib.dme_debug_get_integral(self._ctx, which, ctypes.byref(q), _ptr(L), q.value),
                "integral")
         return L
+
+    def debug_small_stats(self):
+        out = np.zeros(16)
+        _check(_lib.dme_debug_small_stats(self._ctx, _ptr(out)), "dme_debug_small_stats")
+        return out
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -121,6 +121,7 @@ struct dme_ctx {
   dme_stats stats{};
   bool poisoned = false;
   bool force_jacobi = false;
+  bool fsal = true;
   ncclComm_t comm = nullptr;
   // profiling: (start, stop, class, flops, bytes) event records drained at sync points
   bool profile = false;
@@ -195,6 +196,7 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   int64_t cap = o->rank_cap > 0 ? o->rank_cap : c->n;
   c->rank_cap = (int32_t)std::min<int64_t>(cap, KMAX);
   c->h = o->h;
+  c->fsal = o->no_fsal == 0;
 }
 
 bool all_finite(const double* x, size_t cnt) {
@@ -894,9 +896,29 @@ dme_status dme_split_step(dme_ctx* c, dme_scheme scheme, dme_composition comp, i
     DME_REQUIRE(nsteps >= 0, DME_ERR_INVALID, "nsteps must be >= 0");
     auto seq = step_sequence(scheme, comp, c->h);
     check_capable(c, seq);
-    for (int64_t s = 0; s < nsteps; ++s) {
-      run_sequence(c, seq);
+    // FSAL: under Strang, the trailing A(h/2) of a step and the leading A(h/2) of the next are one
+    // A(h) when A is a semigroup flow computed exactly (T1: E_{h/2}^2 = E_h; T12: the ladder rule
+    // gives I(h) = I(h/2) + E_{h/2} I(h/2) E_{h/2}^T exactly), so nsteps steps run as
+    //   A(h/2) X [A(h) X]^{nsteps-1} A(h/2)   (X = the middle flows) — half the E passes.
+    const bool merge = c->fsal && scheme == DME_STRANG && seq.size() > 1 && nsteps > 1 &&
+                       seq.front().flow == seq.back().flow &&
+                       (seq.front().flow == DME_FLOW_T1 || seq.front().flow == DME_FLOW_T12);
+    if (merge) {
+      std::vector<Op> first(seq.begin(), seq.end() - 1), mid(seq.begin() + 1, seq.end() - 1);
+      std::vector<Op> body{{seq.front().flow, c->h}};
+      body.insert(body.end(), mid.begin(), mid.end());
+      run_sequence(c, first);
       c->stats.steps++;
+      for (int64_t s = 1; s < nsteps; ++s) {
+        run_sequence(c, body);
+        c->stats.steps++;
+      }
+      run_sequence(c, {seq.back()});
+    } else {
+      for (int64_t s = 0; s < nsteps; ++s) {
+        run_sequence(c, seq);
+        c->stats.steps++;
+      }
     }
     c->stats.t = c->stats.steps * c->h;
     c->stats.rank = c->r;
@@ -1016,6 +1038,14 @@ dme_status dme_debug_get_integral(dme_ctx* c, int32_t which, int64_t* q, double*
     sync(c);
     for (int64_t j = 0; j < qq; ++j)
       for (int64_t i = 0; i < c->n; ++i) L[i * qq + j] = tmp[(size_t)j * c->n + i];
+  });
+}
+
+dme_status dme_debug_small_stats(dme_ctx* c, double* out16) {
+  if (!c || !out16) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    DME_CUDA(cudaMemcpyAsync(out16, c->sstats, 16 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
   });
 }
 

@@ -68,6 +68,8 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = a.k;
   const int ld = k | 1;
+  long long t_ph[8];
+  t_ph[0] = clock64();
 
   // ---------------------------------------------------------------- load G (symmetrised)
   for (int e_ = tid; e_ < k * k; e_ += NT) {
@@ -162,6 +164,7 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
   }
   __syncthreads();
 
+  t_ph[1] = clock64();
   // ---------------------------------------------------------------- 2. eigenvalues (multisection)
   // largest eigenvalue: 256 probes per round (8 bits), transition found in parallel
   {
@@ -184,6 +187,7 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
     if (tid == 0) s_tmax = 0.5 * (s_lo_t + s_hi_t);
     __syncthreads();
   }
+  t_ph[2] = clock64();
   // rank: eigenvalues > tol * theta_max (at most cap)
   if (tid == 0) {
     const double tmax = s_tmax;
@@ -240,6 +244,7 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
     __syncthreads();
   }
 
+  t_ph[3] = clock64();
   // ---------------------------------------------------------------- 3. twisted-factorisation vectors
   // thread c < r: eigenvector of lam[c]; D+ stored in V[:, c], D- in Tm[:, c] (scratch, col-major)
   if (tid < r) {
@@ -289,6 +294,7 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
   }
   __syncthreads();
 
+  t_ph[4] = clock64();
   // ---------------------------------------------------------------- 4. W = Q Z (warp-owned columns)
   {
     double z[MAXC][RCH];
@@ -345,6 +351,7 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
   }
   __syncthreads();
 
+  t_ph[5] = clock64();
   // ---------------------------------------------------------------- 5. orthogonality check
   {
     double mx = 0.0;
@@ -378,6 +385,9 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
     __syncthreads();
   }
   if (tid == 0 && a.stats && r < k && s_tmax > 0.0) a.stats[2] = fabs(lam[r]) / s_tmax;
+  t_ph[6] = clock64();
+  if (tid == 0 && a.stats)
+    for (int i = 0; i < 6; ++i) a.stats[8 + i] = (double)(t_ph[i + 1] - t_ph[i]);
   if (s_bad) {
     if (tid == 0) *a.r_out = -1;  // caller falls back to the Jacobi kernel
     return;

@@ -42,6 +42,8 @@ struct Params {
   double* partial;
   int* counters;
   int b_nloc;  // >0: B tensor map is 3-D {nloc, N, G}; k -> (k % nloc, k / nloc)
+  int slices;  // >0: split-K slice mode (few tiles, long K): CTA b = (tile b % T, slice b / T),
+               //     partials reduced by splitk_reduce_kernel; 0: Stream-K with last-arriver fixup
 };
 
 __device__ __forceinline__ long long iter_begin(long long c, const Params& p) {
@@ -79,7 +81,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const long long beg = iter_begin(blockIdx.x, p), end = iter_begin(blockIdx.x + 1, p);
+  long long beg, end;
+  if (p.slices > 0) {
+    const int T = p.tiles_m * p.tiles_n;
+    const long long tile = blockIdx.x % T, sl = blockIdx.x / T;
+    beg = tile * p.kiters + sl * p.kiters / p.slices;
+    end = tile * p.kiters + (sl + 1) * p.kiters / p.slices;
+  } else {
+    beg = iter_begin(blockIdx.x, p);
+    end = iter_begin(blockIdx.x + 1, p);
+  }
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -160,7 +171,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // -------------------------------------------------------------- epilogue
     const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
     bool do_store = true;
-    if (!(beg <= tile_beg && end >= tile_end)) {
+    if (p.slices > 0) {
+      // slice mode: publish the partial (fragment order); splitk_reduce_kernel sums in slice order
+      double* myslot = p.partial + (size_t)blockIdx.x * (BM * BN);
+#pragma unroll
+      for (int i = 0; i < ACC; ++i) myslot[i * NUM_CONSUMERS + tid] = acc[i];
+      do_store = false;
+    } else if (!(beg <= tile_beg && end >= tile_end)) {
       // tile split between CTAs: publish this piece, last arriver reduces in k-order
       const int c_first = cta_of(tile_beg, p), c_last = cta_of(tile_end - 1, p);
       const int np = c_last - c_first + 1, me = (int)blockIdx.x - c_first;
@@ -210,6 +227,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// out = epilogue(sum over slices, in slice order, of the fragment-order partials)
+template <int BN, int WM, int WN>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const Params p) {
+  constexpr int MT = BM / WM / 8, NTW = BN / WN / 8, ACC = MT * NTW * 2;
+  const int T = p.tiles_m * p.tiles_n;
+  const long long total = (long long)T * ACC * NUM_CONSUMERS;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int tid = (int)(e % NUM_CONSUMERS);
+    const int i = (int)((e / NUM_CONSUMERS) % ACC);
+    const int tile = (int)(e / ((long long)NUM_CONSUMERS * ACC));
+    double acc = 0.0;
+    for (int sl = 0; sl < p.slices; ++sl)
+      acc += __ldcg(p.partial + (size_t)(sl * T + tile) * (BM * BN) + i * NUM_CONSUMERS + tid);
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp % WM, wn = warp / WM;
+    const int el = i & 1, mn = i >> 1, mi = mn / NTW, ni = mn % NTW;
+    const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+    const long long row = (long long)tm * BM + wm * (BM / WM) + mi * 8 + g;
+    const long long col = (long long)tn * BN + wn * (BN / WN) + ni * 8 + t * 2 + el;
+    if (row < p.M && col < p.N) {
+      double v = p.alpha * acc;
+      if (p.beta != 0.0) v += p.beta * p.cin[row * p.cin_rs + col * p.cin_cs];
+      if (row == col) v += p.gamma;
+      p.out[row * p.out_rs + col * p.out_cs] = v;
+    }
+  }
+}
+
 template <int BN, int WM, int WN>
 void launch(const GemmNTArgs& a, const Params& p0, GemmScratch& ws, cudaStream_t st) {
   constexpr int STAGES = stages_for<BN>();
@@ -232,6 +278,13 @@ void launch(const GemmNTArgs& a, const Params& p0, GemmScratch& ws, cudaStream_t
   }
   gemm_nt_kernel<BN, WM, WN><<<p.grid, NUM_THREADS, smem, st>>>(tmA, tmB, p);
   DME_KCHECK();
+  if (p.slices > 0) {
+    constexpr int ACC = (BM / WM / 8) * (BN / WN / 8) * 2;
+    const long long total = (long long)p.tiles_m * p.tiles_n * ACC * NUM_CONSUMERS;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 4 * num_sms());
+    splitk_reduce_kernel<BN, WM, WN><<<blocks, 256, 0, st>>>(p);
+    DME_KCHECK();
+  }
 }
 
 }  // namespace
@@ -249,13 +302,24 @@ void gemm_nt(const GemmNTArgs& a, GemmScratch& ws, cudaStream_t st) {
   p.N = (int)a.N;
   p.K = (int)a.K;
   p.kiters = (int)ceil_div(a.K, BK);
-  // BN = 128 would need > 168 registers/thread (9 warps -> 3 per SMSP): N > 64 uses 64-wide N tiles
-  int BN = a.N <= 8 ? 8 : a.N <= 16 ? 16 : a.N <= 32 ? 32 : 64;
+  // BN = 128 would need > 168 registers/thread (9 warps -> 3 per SMSP): N > 64 uses 64-wide N tiles.
+  // Narrow N (the factor width k) gets a tile that wastes < 8 columns of DMMA work.
+  int BN = a.N <= 8 ? 8 : a.N <= 16 ? 16 : a.N <= 24 ? 24 : a.N <= 32 ? 32 : a.N <= 40 ? 40
+         : a.N <= 48 ? 48 : a.N <= 56 ? 56 : 64;
   p.tiles_m = (int)ceil_div(a.M, BM);
   p.tiles_n = (int)ceil_div(a.N, BN);
   p.total = (long long)p.tiles_m * p.tiles_n * p.kiters;
-  const long long want = std::max<long long>(1, p.total / 4);
-  p.grid = (int)std::min<long long>(std::min<long long>(num_sms(), ws.max_grid), want);
+  const int sms = std::min<int>(num_sms(), ws.max_grid);
+  const long long tiles = (long long)p.tiles_m * p.tiles_n;
+  p.slices = 0;
+  if (tiles * 4 <= sms && p.kiters >= 16) {
+    // few output tiles over a long K (Gram matrices Zc^T Zc): parallel split-K reduction
+    p.slices = (int)std::min<long long>(sms / tiles, p.kiters / 8);
+    p.grid = (int)(tiles * p.slices);
+  } else {
+    const long long want = std::max<long long>(1, p.total / 4);
+    p.grid = (int)std::min<long long>(sms, want);
+  }
   p.alpha = a.alpha;
   p.beta = a.beta;
   p.gamma = a.gamma;
@@ -272,7 +336,11 @@ void gemm_nt(const GemmNTArgs& a, GemmScratch& ws, cudaStream_t st) {
   switch (BN) {
     case 8: launch<8, 8, 1>(a, p, ws, st); break;
     case 16: launch<16, 8, 1>(a, p, ws, st); break;
+    case 24: launch<24, 8, 1>(a, p, ws, st); break;
     case 32: launch<32, 4, 2>(a, p, ws, st); break;
+    case 40: launch<40, 8, 1>(a, p, ws, st); break;
+    case 48: launch<48, 4, 2>(a, p, ws, st); break;
+    case 56: launch<56, 8, 1>(a, p, ws, st); break;
     default: launch<64, 4, 2>(a, p, ws, st); break;
   }
 }

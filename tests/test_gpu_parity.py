@@ -200,3 +200,18 @@ def test_compress_eigen_paths(dme, case):
         assert s.stats()["eig_fallbacks"] >= f0 + 1
     if case == "graded":
         assert s.stats()["eig_fallbacks"] == f0
+
+
+@pytest.mark.parametrize("comp", ["F12F3", "F1F2F3"])
+def test_fsal_matches_unmerged(dme, comp):
+    """First-same-as-last merging inside one split_step call equals the sub-step-by-sub-step run."""
+    prob = make_config(3, nx=12)
+    h = 0.02
+    a = _solver(dme, prob, h, fsal=True)
+    b = _solver(dme, prob, h, fsal=False)
+    a.split_step("strang", comp, 10)
+    b.split_step("strang", comp, 10)
+    La, Da = a.get_factor()
+    Lb, Db = b.get_factor()
+    assert lowrank.rel_diff(La, Da, Lb, Db) <= 1e-12
+    assert a.stats()["e_passes"] < b.stats()["e_passes"]
