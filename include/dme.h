@@ -141,6 +141,12 @@ dme_status dme_workspace_size(const dme_problem* prob, const dme_options* opt, s
 /* 128-byte NCCL unique id (rank 0 calls it and broadcasts the bytes). */
 dme_status dme_get_unique_id(void* uid128);
 
+/* Row shard of rank `rank` among `world` ranks (host-only, no device): rows [*row0, *row0 + *rows)
+ * of E are owned by the rank; every rank's staging block has *nloc rows (n_loc = ceil(n/world)
+ * rounded up to 16; the last ranks may own fewer or no rows). */
+dme_status dme_shard_rows(int64_t n, int32_t world, int32_t rank, int64_t* row0, int64_t* rows,
+                          int64_t* nloc);
+
 /* Build the context: upload, Padé-13 expm of (h/2)A^T and its square, quadrature factors,
  * compression of P0. dle_init requires m == 0; dre_init requires m >= 1. Collective. */
 dme_status dme_dle_init(const dme_problem* prob, const dme_options* opt, dme_ctx** ctx);

@@ -72,6 +72,8 @@ for _name, _args in {
     "dme_workspace_size": [ctypes.POINTER(_Problem), ctypes.POINTER(_Options),
                            ctypes.POINTER(ctypes.c_size_t)],
     "dme_get_unique_id": [ctypes.c_void_p],
+    "dme_shard_rows": [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                       ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)],
     "dme_dle_init": [ctypes.POINTER(_Problem), ctypes.POINTER(_Options), ctypes.POINTER(_ctx_p)],
     "dme_dre_init": [ctypes.POINTER(_Problem), ctypes.POINTER(_Options), ctypes.POINTER(_ctx_p)],
     "dme_split_step": [_ctx_p, ctypes.c_int, ctypes.c_int, ctypes.c_int64],
@@ -91,7 +93,7 @@ for _name, _args in {
     getattr(_lib, _name).restype = ctypes.c_int
 
 EXPORTED = ["dme_default_options", "dme_status_string", "dme_last_error", "dme_workspace_size",
-            "dme_get_unique_id", "dme_dle_init", "dme_dre_init", "dme_split_step",
+            "dme_get_unique_id", "dme_shard_rows", "dme_dle_init", "dme_dre_init", "dme_split_step",
             "dme_get_factor", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
             "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_get_integral",
             "dme_debug_small_stats", "dme_debug_matmul"]
@@ -128,6 +130,14 @@ class Options:
     rank_cap: int = 0
     quad_nodes: int = 14
     quad_subpanels: int = 1
+
+
+def shard_rows(n: int, world: int, rank: int):
+    """(row0, rows, nloc) of the E row shard owned by `rank` (host logic of the C library)."""
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.dme_shard_rows(n, world, rank, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
+           "dme_shard_rows")
+    return a.value, b.value, c.value
 
 
 def unique_id() -> bytes:

@@ -177,6 +177,14 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   c->D0d = P.take<double>((size_t)std::max<int64_t>(c->r0 * c->r0, 1));
 }
 
+void shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, int64_t* nloc) {
+  int64_t nl = (n + world - 1) / world;
+  nl = (nl + 15) / 16 * 16;
+  *nloc = nl;
+  *row0 = std::min<int64_t>(n, (int64_t)rank * nl);
+  *rows = std::min<int64_t>(nl, n - *row0);
+}
+
 void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->n = pr->n;
   c->ldn = (pr->n + 15) / 16 * 16;
@@ -187,10 +195,7 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->opt = *o;
   c->world = o->world_size > 0 ? o->world_size : 1;
   c->rank = o->world_rank;
-  c->nloc = (c->n + c->world - 1) / c->world;
-  c->nloc = (c->nloc + 15) / 16 * 16;
-  c->row0 = std::min<int64_t>(c->n, (int64_t)c->rank * c->nloc);
-  c->rows_loc = std::min<int64_t>(c->nloc, c->n - c->row0);
+  shard_rows(c->n, c->world, c->rank, &c->row0, &c->rows_loc, &c->nloc);
   c->qn = o->quad_nodes > 0 ? o->quad_nodes : 14;
   c->subpanels = o->quad_subpanels > 0 ? o->quad_subpanels : 1;
   int64_t cap = o->rank_cap > 0 ? o->rank_cap : c->n;
@@ -871,6 +876,15 @@ dme_status dme_workspace_size(const dme_problem* pr, const dme_options* o, size_
     Planner P;
     plan_buffers(&c, P);
     *bytes = P.off + 512;
+  });
+}
+
+dme_status dme_shard_rows(int64_t n, int32_t world, int32_t rank, int64_t* row0, int64_t* rows,
+                          int64_t* nloc) {
+  return guarded(nullptr, [&] {
+    DME_REQUIRE(n > 0 && world >= 1 && rank >= 0 && rank < world && row0 && rows && nloc,
+                DME_ERR_INVALID, "bad shard arguments");
+    shard_rows(n, world, rank, row0, rows, nloc);
   });
 }
 

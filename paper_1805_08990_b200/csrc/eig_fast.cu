@@ -3,16 +3,20 @@
 // Same contract as the Jacobi kernel in small.cu (G = Zc^T Zc = W Theta W^T, Tm = W_kept, fused T3),
 // computed with O(k) synchronisation steps instead of O(k * sweeps):
 //   1. Householder tridiagonalisation Q^T G Q = T (LAPACK dsytd2 recurrences; G kept in shared memory,
-//      one warp per row for the symmetric mat-vec and the rank-2 update; reflectors stay in place).
+//      one warp per row for the symmetric mat-vec and the rank-2 update, all rows of a warp and all
+//      column chunks unrolled so loads and shuffle reductions overlap; reflectors stay in place).
 //   2. Eigenvalues of T by multisection on Sturm counts; the count uses the determinant recurrence
 //      p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2} (no division: one dependent DFMA per element,
-//      backward stable like the ratio form), with power-of-ten rescaling against over/underflow.
-//      Only the kept eigenvalues (the top min(cap, #theta > tol*theta_max)) are refined.
+//      backward stable like the ratio form), signs and exponents read with integer ops, power-of-2
+//      rescaling every 4 elements. Only the kept eigenvalues (the top min(cap, #theta >
+//      tol*theta_max)) plus the first dropped one are refined.
 //   3. Eigenvectors of T by the twisted factorisation (Parlett-Dhillon): top-down D+ and bottom-up D-
-//      pivots, twist index argmin |gamma_i|, two product recurrences; one thread per eigenvector.
+//      pivots, twist index argmin |gamma_i|, ratio pass then product pass; one thread per vector.
 //   4. Back-transformation W = Q Z, one warp per column block with Z held in registers.
-//   5. Orthogonality check max|W^T W - I|: near-degenerate clusters (where the twisted vectors are
-//      not orthogonal) are reported in stats[3] and the caller falls back to the Jacobi kernel.
+//   5. Orthogonality check, weighted by sqrt(theta_i theta_j)/theta_max (the size of the error it
+//      causes in P): near-degenerate clusters, where the twisted vectors are not orthogonal, make
+//      *r_out = -1 and the caller falls back to the Jacobi kernel.
+// Templated on the size class FK (96 or 160) so every per-lane array has a compile-time extent.
 #include "common.cuh"
 #include "small.h"
 #include "small_common.cuh"
@@ -23,56 +27,78 @@ namespace dme {
 
 namespace {
 
-using namespace smallk;
+constexpr int ENT = 512;  // threads of the fast eigen kernel (16 warps, up to 128 registers each)
+constexpr int NW = ENT / 32;
 
-constexpr int FK = FAST_K_MAX;
-constexpr int RCH = (FK + 31) / 32;   // row chunks per lane in the back-transformation
-constexpr int MAXC = (FK + 31) / 32;  // columns per warp in the back-transformation
-
-// number of eigenvalues of T (d, e2 = e^2, normalised) smaller than x
-__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int k, double x) {
+// number of eigenvalues of T (d, e2 = e^2, normalised to ||T|| <= 1) smaller than x
+__device__ __forceinline__ int sturm_count(const double* __restrict__ d,
+                                           const double* __restrict__ e2, int k, double x) {
   double p2 = 1.0, p1 = d[0] - x;
-  bool neg_prev = p1 < 0.0 || (p1 == 0.0);
-  int cnt = neg_prev ? 1 : 0;
-  for (int i = 1; i < k; ++i) {
-    double p = fma(d[i] - x, p1, -e2[i - 1] * p2);
-    const bool neg = p < 0.0 || (p == 0.0 && !neg_prev);
-    cnt += (neg != neg_prev);
+  int neg_prev = p1 <= 0.0;
+  int cnt = neg_prev;
+  int i = 1;
+  for (; i + 3 < k; i += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double p = fma(d[i + u] - x, p1, -e2[i + u - 1] * p2);
+      const long long b = __double_as_longlong(p);
+      const int neg = (b < 0) | ((((unsigned long long)b << 1) == 0ull) & !neg_prev);
+      cnt += neg ^ neg_prev;
+      neg_prev = neg;
+      p2 = p1;
+      p1 = p;
+    }
+    const int ex1 = (int)((__double_as_longlong(p1) >> 52) & 0x7ff);
+    const int ex2 = (int)((__double_as_longlong(p2) >> 52) & 0x7ff);
+    if (ex1 > 1023 + 400 || ex2 > 1023 + 400) {
+      p1 *= 0x1p-400;
+      p2 *= 0x1p-400;
+    } else if (ex1 < 1023 - 400 && ex2 < 1023 - 400) {
+      p1 *= 0x1p400;
+      p2 *= 0x1p400;
+    }
+  }
+  for (; i < k; ++i) {
+    const double p = fma(d[i] - x, p1, -e2[i - 1] * p2);
+    const long long b = __double_as_longlong(p);
+    const int neg = (b < 0) | ((((unsigned long long)b << 1) == 0ull) & !neg_prev);
+    cnt += neg ^ neg_prev;
     neg_prev = neg;
     p2 = p1;
     p1 = p;
-    const double ap = fabs(p);
-    if (ap > 1e150) {
-      p1 *= 1e-150;
-      p2 *= 1e-150;
-    } else if (ap < 1e-150 && fabs(p2) < 1e-150) {
-      p1 *= 1e150;
-      p2 *= 1e150;
-    }
   }
   return cnt;
 }
 
-__global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
-  extern __shared__ double A[];          // k x ld, full symmetric, ld odd
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int FK>
+__global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
+  constexpr int RCH = (FK + 31) / 32;      // column chunks per lane
+  constexpr int RPW = (FK + NW - 1) / NW;  // rows per warp
+  extern __shared__ double A[];            // k x ld, full symmetric, ld odd
   __shared__ double d[FK], e[FK], e2[FK], tau[FK], vec[FK], pv[FK];
-  __shared__ double lam[FK];             // kept eigenvalues, descending (normalised)
-  __shared__ double lo_s[FK], hi_s[FK];
-  __shared__ int cnt_s[1024];
-  __shared__ double red[32];
+  __shared__ double lam[FK + 1];           // kept eigenvalues (+1 dropped), descending (normalised)
+  __shared__ double lo_s[FK + 1], hi_s[FK + 1], slam[FK + 1];
+  __shared__ int cnt_s[ENT];
+  __shared__ double red[NW];
   __shared__ int s_r, s_bad;
-  __shared__ double s_scale, s_lo, s_hi, s_tmax, s_orth, s_lo_t, s_hi_t;
+  __shared__ double s_scale, s_lo, s_hi, s_tmax, s_lo_t, s_hi_t;
   __shared__ double Gam[SMALL_M_MAX * SMALL_M_MAX];
   __shared__ double Phi[SMALL_M_MAX * SMALL_M_MAX];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = a.k;
   const int ld = k | 1;
-  long long t_ph[8];
+  long long t_ph[7];
   t_ph[0] = clock64();
 
   // ---------------------------------------------------------------- load G (symmetrised)
-  for (int e_ = tid; e_ < k * k; e_ += NT) {
+  for (int e_ = tid; e_ < k * k; e_ += ENT) {
     const int i = e_ % k, j = e_ / k;
     A[i * ld + j] = 0.5 * (a.G[i + (size_t)j * a.ldg] + a.G[j + (size_t)i * a.ldg]);
   }
@@ -82,24 +108,31 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
   for (int j = 0; j + 2 < k; ++j) {
     const int m = k - j - 1;
     if (warp == 0) {
+      double xs[RCH];
       double xn2 = 0.0;
-      for (int i = 1 + lane; i < m; i += 32) {
-        const double x = A[(j + 1 + i) * ld + j];
-        xn2 += x * x;
+#pragma unroll
+      for (int u = 0; u < RCH; ++u) {
+        const int i = lane + 32 * u;
+        xs[u] = i < m ? A[(j + 1 + i) * ld + j] : 0.0;
+        if (i >= 1) xn2 = fma(xs[u], xs[u], xn2);
       }
-      for (int o = 16; o; o >>= 1) xn2 += __shfl_xor_sync(0xffffffffu, xn2, o);
-      const double alpha = A[(j + 1) * ld + j];
+      xn2 = warp_sum(xn2);
+      const double alpha = __shfl_sync(0xffffffffu, xs[0], 0);
       double t = 0.0, beta = alpha, scal = 0.0;
       if (xn2 > 0.0) {
         beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        t = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
+        const double amb = alpha - beta;
+        scal = 1.0 / amb;
+        t = -amb / beta;  // (beta - alpha) / beta
       }
-      for (int i = lane; i < m; i += 32) {
-        double v = i == 0 ? 1.0 : A[(j + 1 + i) * ld + j] * scal;
-        if (t == 0.0) v = (i == 0) ? 1.0 : 0.0;
-        vec[i] = v;
-        if (i > 0) A[(j + 1 + i) * ld + j] = v;  // reflector kept below the subdiagonal
+#pragma unroll
+      for (int u = 0; u < RCH; ++u) {
+        const int i = lane + 32 * u;
+        if (i < m) {
+          const double v = (i == 0) ? 1.0 : (t == 0.0 ? 0.0 : xs[u] * scal);
+          vec[i] = v;
+          if (i > 0) A[(j + 1 + i) * ld + j] = v;  // reflector kept below the subdiagonal
+        }
       }
       if (lane == 0) {
         tau[j] = t;
@@ -110,24 +143,61 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
     __syncthreads();
     const double tj = tau[j];
     if (tj == 0.0) continue;  // uniform branch
-    // p = tau * A22 v
-    for (int i = warp; i < m; i += NT / 32) {
-      const double* row = A + (j + 1 + i) * ld + (j + 1);
-      double acc = 0.0;
-      for (int l = lane; l < m; l += 32) acc += row[l] * vec[l];
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) pv[i] = tj * acc;
+    // p = tau * A22 v   (all rows of this warp and all chunks unrolled)
+    {
+      double vl[RCH];
+#pragma unroll
+      for (int u = 0; u < RCH; ++u) vl[u] = (lane + 32 * u < m) ? vec[lane + 32 * u] : 0.0;
+      double acc[RPW];
+#pragma unroll
+      for (int t = 0; t < RPW; ++t) {
+        const int i = warp + NW * t;
+        acc[t] = 0.0;
+        if (i < m) {
+          const double* row = A + (j + 1 + i) * ld + (j + 1);
+#pragma unroll
+          for (int u = 0; u < RCH; ++u)
+            if (lane + 32 * u < m) acc[t] = fma(row[lane + 32 * u], vl[u], acc[t]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < RPW; ++t) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+      if (lane == 0) {
+#pragma unroll
+        for (int t = 0; t < RPW; ++t)
+          if (warp + NW * t < m) pv[warp + NW * t] = tj * acc[t];
+      }
     }
     __syncthreads();
-    // K = tau/2 p^T v ; A22 -= v w^T + w v^T with w = p - K v
-    double dot = 0.0;
-    for (int l = lane; l < m; l += 32) dot += pv[l] * vec[l];
-    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    const double K = 0.5 * tj * dot;
-    for (int i = warp; i < m; i += NT / 32) {
-      double* row = A + (j + 1 + i) * ld + (j + 1);
-      const double vi = vec[i], wi = pv[i] - K * vi;
-      for (int l = lane; l < m; l += 32) row[l] -= vi * (pv[l] - K * vec[l]) + wi * vec[l];
+    // K = tau/2 p^T v ;  A22 -= v w^T + w v^T  with w = p - K v
+    {
+      double vl[RCH], wl[RCH];
+      double dot = 0.0;
+#pragma unroll
+      for (int u = 0; u < RCH; ++u) {
+        const int l = lane + 32 * u;
+        vl[u] = l < m ? vec[l] : 0.0;
+        wl[u] = l < m ? pv[l] : 0.0;
+        dot = fma(wl[u], vl[u], dot);
+      }
+      const double K = 0.5 * tj * warp_sum(dot);
+#pragma unroll
+      for (int u = 0; u < RCH; ++u) wl[u] -= K * vl[u];
+#pragma unroll
+      for (int t = 0; t < RPW; ++t) {
+        const int i = warp + NW * t;
+        if (i < m) {
+          double* row = A + (j + 1 + i) * ld + (j + 1);
+          const double vi = vec[i], wi = pv[i] - K * vi;
+#pragma unroll
+          for (int u = 0; u < RCH; ++u) {
+            const int l = lane + 32 * u;
+            if (l < m) row[l] -= vi * wl[u] + wi * vl[u];
+          }
+        }
+      }
     }
     __syncthreads();
   }
@@ -140,22 +210,23 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
     // normalisation by a Gershgorin bound of ||T||
     double nrm = 0.0, lo = 1e300, hi = -1e300;
     for (int i = 0; i < k; ++i) {
-      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < k ? fabs(e[i]) : 0.0);
-      nrm = fmax(nrm, fabs(d[i]) + r);
+      const double rr = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < k ? fabs(e[i]) : 0.0);
+      nrm = fmax(nrm, fabs(d[i]) + rr);
     }
     if (!(nrm > 0.0)) nrm = 1.0;
     s_scale = nrm;
+    const double inv = 1.0 / nrm;
     for (int i = 0; i < k; ++i) {
-      d[i] /= nrm;
+      d[i] *= inv;
       if (i + 1 < k) {
-        e[i] /= nrm;
+        e[i] *= inv;
         e2[i] = e[i] * e[i];
       }
     }
     for (int i = 0; i < k; ++i) {
-      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < k ? fabs(e[i]) : 0.0);
-      lo = fmin(lo, d[i] - r);
-      hi = fmax(hi, d[i] + r);
+      const double rr = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < k ? fabs(e[i]) : 0.0);
+      lo = fmin(lo, d[i] - rr);
+      hi = fmax(hi, d[i] + rr);
     }
     s_lo = lo - 1e-14;
     s_hi = hi + 1e-14;
@@ -163,8 +234,8 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
     s_hi_t = s_hi;
   }
   __syncthreads();
-
   t_ph[1] = clock64();
+
   // ---------------------------------------------------------------- 2. eigenvalues (multisection)
   // largest eigenvalue: 256 probes per round (8 bits), transition found in parallel
   {
@@ -192,20 +263,16 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
   if (tid == 0) {
     const double tmax = s_tmax;
     int r = 0;
-    if (tmax > 0.0) {
-      const int below = sturm_count(d, e2, k, a.tol * tmax);
-      r = k - below;
-    }
+    if (tmax > 0.0) r = k - sturm_count(d, e2, k, a.tol * tmax);
     if (r > a.cap) r = a.cap;
     if (r < 0) r = 0;
     s_r = r;
   }
   __syncthreads();
   const int r = s_r;
-  // refine the top r (+1 dropped, for stats) eigenvalues: ascending index jj = k-1-c
-  const int nr = r < k ? r + 1 : r;
+  const int nr = r < k ? r + 1 : r;  // + the first dropped one, for the stats
   {
-    int P = nr > 0 ? 256 / nr : 1;
+    int P = nr > 0 ? 200 / nr : 1;
     P = P < 1 ? 1 : (P > 16 ? 16 : P);
     const int grp = tid / P, t = tid % P;
     const bool act = grp < nr;
@@ -215,17 +282,12 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
       hi_s[grp] = s_hi;
     }
     __syncthreads();
-    const double width0 = s_hi - s_lo;
-    int nit = 0;
-    {
-      const double bits = log2((double)P + 1.0);
-      nit = (int)ceil(log2(width0 / 4e-16 + 1.0) / bits) + 1;
-    }
+    const double bits = log2((double)P + 1.0);
+    const int nit = (int)ceil(log2((s_hi - s_lo) / 4e-16 + 1.0) / bits) + 1;
     for (int it = 0; it < nit; ++it) {
       if (act) {
         const double a0 = lo_s[grp], b0 = hi_s[grp];
-        const double x = a0 + (b0 - a0) * (t + 1) / (P + 1.0);
-        cnt_s[tid] = sturm_count(d, e2, k, x);
+        cnt_s[tid] = sturm_count(d, e2, k, a0 + (b0 - a0) * (t + 1) / (P + 1.0));
       }
       __syncthreads();
       if (act && t == 0) {
@@ -240,13 +302,16 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
       }
       __syncthreads();
     }
-    if (act && t == 0) lam[grp] = 0.5 * (lo_s[grp] + hi_s[grp]);
+    if (act && t == 0) {
+      lam[grp] = 0.5 * (lo_s[grp] + hi_s[grp]);
+      slam[grp] = sqrt(fabs(lam[grp]));
+    }
     __syncthreads();
   }
-
   t_ph[3] = clock64();
+
   // ---------------------------------------------------------------- 3. twisted-factorisation vectors
-  // thread c < r: eigenvector of lam[c]; D+ stored in V[:, c], D- in Tm[:, c] (scratch, col-major)
+  // thread c < r: eigenvector of lam[c]; D+ in V[:, c], D- in Tm[:, c] (global scratch)
   if (tid < r) {
     const int c = tid;
     const double lm = lam[c];
@@ -271,120 +336,160 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
     }
     int tw = 0;
     double best = 1e300;
+#pragma unroll 8
     for (int i = 0; i < k; ++i) {
       const double g = Dp[i] + Dm[i] - (d[i] - lm);
       if (fabs(g) < best) { best = fabs(g); tw = i; }
     }
-    // z into V[:, c]: z_tw = 1, upward with D+, downward with D-
+    // ratios first (independent divisions), then the product chains
+#pragma unroll 8
+    for (int i = 0; i < tw; ++i) Dp[i] = -e[i] / Dp[i];
+#pragma unroll 8
+    for (int i = tw + 1; i < k; ++i) Dm[i] = -e[i - 1] / Dm[i];
     double zi = 1.0, nrm2 = 1.0;
     for (int i = tw - 1; i >= 0; --i) {
-      zi = -(e[i] / Dp[i]) * zi;
-      nrm2 += zi * zi;
-      Dp[i] = zi;  // overwrite: Dp[i] no longer needed
+      zi *= Dp[i];
+      nrm2 = fma(zi, zi, nrm2);
+      Dp[i] = zi;
     }
     zi = 1.0;
     for (int i = tw + 1; i < k; ++i) {
-      zi = -(e[i - 1] / Dm[i]) * zi;
-      nrm2 += zi * zi;
+      zi *= Dm[i];
+      nrm2 = fma(zi, zi, nrm2);
       Dp[i] = zi;
     }
     Dp[tw] = 1.0;
     const double inv = 1.0 / sqrt(nrm2);
+#pragma unroll 8
     for (int i = 0; i < k; ++i) Dp[i] *= inv;
   }
   __syncthreads();
-
   t_ph[4] = clock64();
+
   // ---------------------------------------------------------------- 4. W = Q Z (warp-owned columns)
   {
-    double z[MAXC][RCH];
-    int ncol = 0;
+    constexpr int CP = 4;  // columns per warp per pass (register budget)
+    const double sc = s_scale;
+    for (int pass = 0; pass * NW * CP < r; ++pass) {
+      double z[CP][RCH];
 #pragma unroll
-    for (int cc = 0; cc < MAXC; ++cc) {
-      const int c = warp + 32 * cc;
+      for (int cc = 0; cc < CP; ++cc) {
+        const int c = warp + NW * (pass * CP + cc);
 #pragma unroll
-      for (int t = 0; t < RCH; ++t) {
-        const int i = lane + 32 * t;
-        z[cc][t] = (c < r && i < k) ? a.V[i + (size_t)c * a.ldv] : 0.0;
-      }
-      ncol += (c < r);
-    }
-    if (ncol > 0) {
-      for (int j = k - 3; j >= 0; --j) {
-        const double tj = tau[j];
-        if (tj == 0.0) continue;
-        // v: 1 at row j+1, A[i][j] for rows i >= j+2
-        double vr[RCH];
-#pragma unroll
-        for (int t = 0; t < RCH; ++t) {
-          const int i = lane + 32 * t;
-          vr[t] = (i == j + 1) ? 1.0 : ((i > j + 1 && i < k) ? A[i * ld + j] : 0.0);
-        }
-#pragma unroll
-        for (int cc = 0; cc < MAXC; ++cc) {
-          if (cc >= ncol) break;
-          double s = 0.0;
-#pragma unroll
-          for (int t = 0; t < RCH; ++t) s += vr[t] * z[cc][t];
-          for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          s *= tj;
-#pragma unroll
-          for (int t = 0; t < RCH; ++t) z[cc][t] -= s * vr[t];
+        for (int u = 0; u < RCH; ++u) {
+          const int i = lane + 32 * u;
+          z[cc][u] = (c < r && i < k) ? a.V[i + (size_t)c * a.ldv] : 0.0;
         }
       }
-    }
-    __syncthreads();  // all reflector reads from A done before A is reused
+      if (warp + NW * pass * CP < r) {
+        for (int j = k - 3; j >= 0; --j) {
+          const double tj = tau[j];
+          if (tj == 0.0) continue;
+          double vr[RCH];
 #pragma unroll
-    for (int cc = 0; cc < MAXC; ++cc) {
-      const int c = warp + 32 * cc;
-      if (c < r) {
+          for (int u = 0; u < RCH; ++u) {
+            const int i = lane + 32 * u;
+            vr[u] = (i == j + 1) ? 1.0 : ((i > j + 1 && i < k) ? A[i * ld + j] : 0.0);
+          }
+          double s[CP];
 #pragma unroll
-        for (int t = 0; t < RCH; ++t) {
-          const int i = lane + 32 * t;
-          if (i < k) {
-            a.Tm[i + (size_t)c * a.ldt] = z[cc][t] * (a.sqrt_scale ? sqrt(fmax(lam[c] * s_scale, 0.0)) : 1.0);
-            A[c * ld + i] = z[cc][t];  // W^T row-major copy for the check
+          for (int cc = 0; cc < CP; ++cc) {
+            s[cc] = 0.0;
+#pragma unroll
+            for (int u = 0; u < RCH; ++u) s[cc] = fma(vr[u], z[cc][u], s[cc]);
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int cc = 0; cc < CP; ++cc) s[cc] += __shfl_xor_sync(0xffffffffu, s[cc], o);
+#pragma unroll
+          for (int cc = 0; cc < CP; ++cc) {
+            const double f = tj * s[cc];
+#pragma unroll
+            for (int u = 0; u < RCH; ++u) z[cc][u] -= f * vr[u];
+          }
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < CP; ++cc) {
+        const int c = warp + NW * (pass * CP + cc);
+        if (c < r) {
+          const double f = a.sqrt_scale ? sqrt(fmax(lam[c] * sc, 0.0)) : 1.0;
+#pragma unroll
+          for (int u = 0; u < RCH; ++u) {
+            const int i = lane + 32 * u;
+            if (i < k) a.Tm[i + (size_t)c * a.ldt] = z[cc][u] * f;
           }
         }
       }
     }
+    __syncthreads();  // all reflector reads from A done before A is reused
+    // W^T (row-major) into shared memory for the check (unscaled)
+    for (int e_ = tid; e_ < k * r; e_ += ENT) {
+      const int i = e_ % k, c = e_ / k;
+      const double f = a.sqrt_scale ? sqrt(fmax(lam[c] * sc, 0.0)) : 1.0;
+      A[c * ld + i] = f > 0.0 ? a.Tm[i + (size_t)c * a.ldt] / f : 0.0;
+    }
   }
   __syncthreads();
-
   t_ph[5] = clock64();
-  // ---------------------------------------------------------------- 5. orthogonality check
+
+  // ---------------------------------------------------------------- 5. weighted orthogonality check
   {
+    // 4x4 blocks of W^T W (upper block triangle), one block per thread
+    constexpr int TB = 4;
+    const int nb = (r + TB - 1) / TB;
     double mx = 0.0;
-    for (int p = warp; p < r * r; p += NT / 32) {
-      const int c1 = p % r, c2 = p / r;
-      if (c1 > c2) continue;
-      double acc = 0.0;
-      for (int i = lane; i < k; i += 32) acc += A[c1 * ld + i] * A[c2 * ld + i];
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      // weighted by sqrt(theta_1 theta_2)/theta_max: the error this causes in P = Zc W W^T Zc^T
-      // (tiny-eigenvalue vectors are only determined to eps*||T||/gap, harmlessly so)
-      const double w = sqrt(fabs(lam[c1] * lam[c2])) / fmax(fabs(lam[0]), 1e-300);
-      mx = fmax(mx, fabs(acc - (c1 == c2 ? 1.0 : 0.0)) * (c1 == c2 ? 1.0 : w));
+    for (int blk = tid; blk < nb * nb; blk += ENT) {
+      const int bi = blk % nb, bj = blk / nb;
+      if (bi > bj) continue;
+      double acc[TB][TB];
+#pragma unroll
+      for (int x = 0; x < TB; ++x)
+#pragma unroll
+        for (int y = 0; y < TB; ++y) acc[x][y] = 0.0;
+      for (int i = 0; i < k; ++i) {
+        double wa[TB], wb[TB];
+#pragma unroll
+        for (int x = 0; x < TB; ++x) {
+          const int c1 = bi * TB + x, c2 = bj * TB + x;
+          wa[x] = c1 < r ? A[c1 * ld + i] : 0.0;
+          wb[x] = c2 < r ? A[c2 * ld + i] : 0.0;
+        }
+#pragma unroll
+        for (int x = 0; x < TB; ++x)
+#pragma unroll
+          for (int y = 0; y < TB; ++y) acc[x][y] = fma(wa[x], wb[y], acc[x][y]);
+      }
+#pragma unroll
+      for (int x = 0; x < TB; ++x)
+#pragma unroll
+        for (int y = 0; y < TB; ++y) {
+          const int c1 = bi * TB + x, c2 = bj * TB + y;
+          if (c1 < r && c2 < r && c1 <= c2) {
+            const double w = (c1 == c2) ? 1.0 : slam[c1] * slam[c2] / fmax(fabs(lam[0]), 1e-300);
+            mx = fmax(mx, fabs(acc[x][y] - (c1 == c2 ? 1.0 : 0.0)) * w);
+          }
+        }
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) red[warp] = mx;
     __syncthreads();
     if (tid == 0) {
       double m = 0.0;
-      for (int w = 0; w < NT / 32; ++w) m = fmax(m, red[w]);
-      s_orth = m;
+      for (int w = 0; w < NW; ++w) m = fmax(m, red[w]);
       s_bad = !(m <= a.orth_tol);  // NaN-safe
       if (a.stats) {
-        const double sc = s_scale;
         a.stats[0] = (double)r;
-        a.stats[1] = s_tmax * sc;
-        a.stats[2] = 0.0;  // filled below if something was dropped
+        a.stats[1] = s_tmax * s_scale;
+        a.stats[2] = (r < k && s_tmax > 0.0) ? fabs(lam[r]) / s_tmax : 0.0;
         a.stats[3] = s_bad ? 1.0 : 0.0;
         a.stats[4] = m;
       }
     }
     __syncthreads();
   }
-  if (tid == 0 && a.stats && r < k && s_tmax > 0.0) a.stats[2] = fabs(lam[r]) / s_tmax;
   t_ph[6] = clock64();
   if (tid == 0 && a.stats)
     for (int i = 0; i < 6; ++i) a.stats[8 + i] = (double)(t_ph[i + 1] - t_ph[i]);
@@ -394,27 +499,33 @@ __global__ void __launch_bounds__(NT, 1) eig_fast_kernel(SmallArgs a) {
   }
   if (a.t3 && r > 0) {
     __syncthreads();
-    t3_fuse(a, k, r, A, Gam, Phi);
+    smallk::t3_fuse(a, k, r, A, Gam, Phi);
   }
   if (tid == 0) *a.r_out = r;
 }
 
-}  // namespace
+template <int FK>
+void launch_fast(const SmallArgs& a, cudaStream_t st) {
+  const size_t floor_b = sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX;
+  const size_t need = sizeof(double) * (size_t)FK * (FK | 1);
+  size_t smem = sizeof(double) * (size_t)a.k * (a.k | 1);
+  if (smem < floor_b) smem = floor_b;
+  static bool attr = false;
+  if (!attr) {
+    DME_CUDA(cudaFuncSetAttribute(eig_fast_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(need > floor_b ? need : floor_b)));
+    attr = true;
+  }
+  eig_fast_kernel<FK><<<1, ENT, smem, st>>>(a);
+  DME_KCHECK();
+}
 
-size_t eig_fast_smem(int k) { return sizeof(double) * (size_t)k * (k | 1) + 64; }
+}  // namespace
 
 void eig_fast(const SmallArgs& a, cudaStream_t st) {
   if (a.k > FAST_K_MAX || a.k < 1) throw std::runtime_error("eig_fast: k out of range");
-  size_t smem = eig_fast_smem(a.k);
-  if (smem < sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX) smem = sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX;
-  static bool attr = false;
-  if (!attr) {
-    DME_CUDA(cudaFuncSetAttribute(eig_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)eig_fast_smem(FAST_K_MAX)));
-    attr = true;
-  }
-  eig_fast_kernel<<<1, NT, smem, st>>>(a);
-  DME_KCHECK();
+  if (a.k <= 96) launch_fast<96>(a, st);
+  else launch_fast<FAST_K_MAX>(a, st);
 }
 
 }  // namespace dme

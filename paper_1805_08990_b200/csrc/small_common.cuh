@@ -66,7 +66,7 @@ __device__ inline void t3_fuse(const SmallArgs& a, int k, int r, double* S, doub
     double* Fs = S;                                  // the packed area is free now:
     double* Wd = S + SMALL_K_MAX * SMALL_M_MAX;      // F (r x m), W / U (k x m)
     // W = Tm^T H  (r x m),  H = Zc^T B  (k x m)
-    for (int e = tid; e < r * m; e += NT) {
+    for (int e = tid; e < r * m; e += (int)blockDim.x) {
       const int c = e % r, mu = e / r;
       double acc = 0.0;
       for (int i = 0; i < k; ++i) acc += a.Tm[i + (size_t)c * a.ldt] * a.H[i + (size_t)mu * a.ldh];
@@ -74,7 +74,7 @@ __device__ inline void t3_fuse(const SmallArgs& a, int k, int r, double* S, doub
     }
     __syncthreads();
     // F = sqrt(tau) W Linv^T   (Linv = L_R^{-1}, m x m row-major)
-    for (int e = tid; e < r * m; e += NT) {
+    for (int e = tid; e < r * m; e += (int)blockDim.x) {
       const int c = e / m, mu = e % m;
       double acc = 0.0;
       for (int nu2 = 0; nu2 < m; ++nu2) acc += Wd[c * m + nu2] * a.LRinv[mu * m + nu2];
@@ -98,14 +98,14 @@ __device__ inline void t3_fuse(const SmallArgs& a, int k, int r, double* S, doub
     }
     __syncthreads();
     // U = Tm F (k x m), then Tm <- Tm + U Gamma F^T
-    for (int e = tid; e < k * m; e += NT) {
+    for (int e = tid; e < k * m; e += (int)blockDim.x) {
       const int i = e / m, mu = e % m;
       double acc = 0.0;
       for (int c = 0; c < r; ++c) acc += a.Tm[i + (size_t)c * a.ldt] * Fs[c * m + mu];
       Wd[i * m + mu] = acc;
     }
     __syncthreads();
-    for (int e = tid; e < k * r; e += NT) {
+    for (int e = tid; e < k * r; e += (int)blockDim.x) {
       const int i = e % k, c = e / k;
       double acc = 0.0;
       for (int mu = 0; mu < m; ++mu) {
