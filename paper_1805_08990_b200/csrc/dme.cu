@@ -108,8 +108,12 @@ struct dme_ctx {
   double *Zc12h = nullptr, *Zc12f = nullptr, *Zc2 = nullptr, *Z = nullptr, *Ztmp = nullptr;
   double *G = nullptr, *H = nullptr, *Tm = nullptr, *Vg = nullptr, *LRinv = nullptr, *sstats = nullptr;
   double *norm_dev = nullptr, *red_scratch = nullptr, *stage = nullptr;
+  double *LA = nullptr;  // look-ahead operand [E_h L_I(h) | E_h Y]  (ldn x KMAX)
   int* r_dev = nullptr;
-  GemmScratch gs;
+  GemmScratch gs, gs2;   // scratch of the main stream and of the look-ahead stream
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_gram = nullptr, ev_ahead = nullptr;
+  bool lookahead = true;
   // init-only device buffers
   double *Aup = nullptr, *X0 = nullptr, *BT = nullptr, *X2 = nullptr, *X4 = nullptr, *X6 = nullptr;
   double *T1 = nullptr, *U = nullptr, *V = nullptr, *lu_scr = nullptr, *Wa = nullptr, *Wb = nullptr;
@@ -158,6 +162,11 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   c->gs.max_tiles = 1 << 16;
   c->gs.partial = P.take<double>(GemmScratch::partial_doubles(c->gs.max_grid));
   c->gs.counters = P.take<int>((size_t)c->gs.max_tiles);
+  c->gs2.max_grid = 256;
+  c->gs2.max_tiles = 1 << 16;
+  c->gs2.partial = P.take<double>(GemmScratch::partial_doubles(c->gs2.max_grid));
+  c->gs2.counters = P.take<int>((size_t)c->gs2.max_tiles);
+  c->LA = P.take<double>(fk);
   if (c->world > 1) c->stage = P.take<double>((size_t)c->world * c->nloc * KMAX);
   // init-only
   c->Aup = P.take<double>(nn);
@@ -313,19 +322,21 @@ cudaEvent_t take_event(dme_ctx* c) {
 }
 struct ProfScope {
   dme_ctx* c;
+  cudaStream_t s;
   dme_ctx::Rec r{};
-  ProfScope(dme_ctx* cc, int cls, double flops = 0, double bytes = 0) : c(cc) {
+  ProfScope(dme_ctx* cc, int cls, double flops = 0, double bytes = 0, cudaStream_t ss = nullptr)
+      : c(cc), s(ss ? ss : cc->st) {
     if (!c->profile) return;
     r.a = take_event(c);
     r.b = take_event(c);
     r.cls = cls;
     r.flops = flops;
     r.bytes = bytes;
-    DME_CUDA(cudaEventRecord(r.a, c->st));
+    DME_CUDA(cudaEventRecord(r.a, s));
   }
   ~ProfScope() {
     if (!c->profile) return;
-    cudaEventRecord(r.b, c->st);
+    cudaEventRecord(r.b, s);
     c->pending.push_back(r);
   }
 };
@@ -354,8 +365,8 @@ void drain_profile(dme_ctx* c) {
 
 // ------------------------------------------------------------------ building blocks
 // out (col-major, ldo) = alpha * E * X  (E: n x n row-major, X: n x k col-major), sharded over ranks
-void epass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t ldo,
-           double alpha) {
+void epass_on(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t ldo,
+              double alpha, cudaStream_t st, GemmScratch& gs) {
   if (k <= 0) return;
   c->stats.e_passes++;
   if (c->world == 1) {
@@ -363,52 +374,63 @@ void epass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out,
     g.A = E; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
     g.M = c->n; g.N = k; g.K = c->n; g.alpha = alpha;
     g.out = out; g.out_rs = 1; g.out_cs = ldo;
-    ProfScope ps(c, PROF_EPASS, 2.0 * c->n * c->n * k, 8.0 * c->n * c->n);
-    gemm_nt(g, c->gs, c->st);
+    ProfScope ps(c, PROF_EPASS, 2.0 * c->n * c->n * k, 8.0 * c->n * c->n, st);
+    gemm_nt(g, gs, st);
     return;
   }
   // row shard: local rows into this rank's staging block (nloc x k, col-major), allgather, unpack
   double* mine = c->stage + (size_t)c->rank * c->nloc * k;
   if (c->rows_loc > 0) {
-    ProfScope ps(c, PROF_EPASS, 2.0 * c->rows_loc * c->n * k, 8.0 * c->rows_loc * c->n);
+    ProfScope ps(c, PROF_EPASS, 2.0 * c->rows_loc * c->n * k, 8.0 * c->rows_loc * c->n, st);
     GemmNTArgs g;
     g.A = E + c->row0 * c->ldn; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
     g.M = c->rows_loc; g.N = k; g.K = c->n; g.alpha = alpha;
     g.out = mine; g.out_rs = 1; g.out_cs = c->nloc;
-    gemm_nt(g, c->gs, c->st);
+    gemm_nt(g, gs, st);
   }
-  DME_NCCL(ncclAllGather(mine, c->stage, (size_t)c->nloc * k, ncclDouble, c->comm, c->st));
+  DME_NCCL(ncclAllGather(mine, c->stage, (size_t)c->nloc * k, ncclDouble, c->comm, st));
   for (int gr = 0; gr < c->world; ++gr) {
     const int64_t r0 = std::min<int64_t>(c->n, (int64_t)gr * c->nloc);
     const int64_t rows = std::min<int64_t>(c->nloc, c->n - r0);
     if (rows > 0)
-      copy_cols(out + r0, ldo, c->stage + (size_t)gr * c->nloc * k, c->nloc, rows, k, 1.0, c->st);
+      copy_cols(out + r0, ldo, c->stage + (size_t)gr * c->nloc * k, c->nloc, rows, k, 1.0, st);
   }
 }
 
-// Compress the factor Zc (n x k, col-major ldn) into out (n x r); optionally fuse T3(tau3).
-int64_t compress(dme_ctx* c, const double* Zc, int64_t k, double* out, bool t3, double tau3,
-                 bool do_compress = true) {
-  if (k <= 0) return 0;
-  DME_REQUIRE(k <= KMAX, DME_ERR_DIM, "factor width exceeds the small-system limit (224)");
+void epass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t ldo,
+           double alpha) {
+  epass_on(c, E, X, k, out, ldo, alpha, c->st, c->gs);
+}
+
+// Launch the Gram matrix (extended by B when T3 is fused: the B columns are copied next to the
+// factor, so G_ext = [Zc, B]^T [Zc, B] yields G and H = Zc^T B in one pass) and the small kernel.
+// Zc must have KMAX columns of capacity.
+void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bool do_compress,
+                     SmallArgs& a, bool& fast, cudaEvent_t after_gram = nullptr) {
+  DME_REQUIRE(k <= KMAX && (!t3 || k + c->m <= KMAX), DME_ERR_DIM,
+              "factor width exceeds the small-system limit (224)");
   c->stats.compressions += do_compress ? 1 : 0;
+  a = SmallArgs();
   if (do_compress) {
+    const int64_t kk = t3 ? k + c->m : k;
+    if (t3) copy_cols(Zc + k * c->ldn, c->ldn, c->Bcol, c->ldn, c->n, c->m, 1.0, c->st);
     ProfScope ps(c, PROF_GRAM);
     GemmNTArgs g;
     g.A = Zc; g.lda = c->ldn; g.B = Zc; g.ldb = c->ldn;
-    g.M = k; g.N = k; g.K = c->n;
+    g.M = kk; g.N = kk; g.K = c->n;
     g.out = c->G; g.out_rs = 1; g.out_cs = KMAX;
     gemm_nt(g, c->gs, c->st);
-  }
-  if (t3) {
+    a.H = c->G + k * KMAX;
+  } else if (t3) {
     ProfScope ps(c, PROF_GRAM);
     GemmNTArgs g;
     g.A = Zc; g.lda = c->ldn; g.B = c->Bcol; g.ldb = c->ldn;
     g.M = k; g.N = c->m; g.K = c->n;
     g.out = c->H; g.out_rs = 1; g.out_cs = KMAX;
     gemm_nt(g, c->gs, c->st);
+    a.H = c->H;
   }
-  SmallArgs a;
+  if (after_gram) DME_CUDA(cudaEventRecord(after_gram, c->st));
   a.k = (int)k;
   a.compress = do_compress ? 1 : 0;
   a.G = c->G; a.ldg = KMAX;
@@ -418,20 +440,22 @@ int64_t compress(dme_ctx* c, const double* Zc, int64_t k, double* out, bool t3, 
   a.cap = c->rank_cap;
   a.t3 = t3 ? 1 : 0;
   a.m = (int)c->m;
-  a.H = c->H; a.ldh = KMAX;
+  a.ldh = KMAX;
   a.LRinv = c->LRinv;
   a.tau = tau3;
   a.Tm = c->Tm; a.ldt = KMAX;
   a.V = c->Vg; a.ldv = KMAX;
   a.r_out = c->r_dev;
   a.stats = c->sstats;
+  fast = do_compress && k <= FAST_K_MAX && !c->force_jacobi;
+  ProfScope ps(c, PROF_SMALL);
+  if (fast) eig_fast(a, c->st); else compress_t3(a, c->st);
+}
+
+// Wait for the small kernel (main stream only), fall back to Jacobi if the fast path refused.
+int64_t compress_finish(dme_ctx* c, const SmallArgs& a, bool fast, bool do_compress) {
   int r_host = 0;
   double st_host[5] = {0, 0, 0, 0, 0};
-  const bool fast = do_compress && k <= FAST_K_MAX && !c->force_jacobi;
-  {
-    ProfScope ps(c, PROF_SMALL);
-    if (fast) eig_fast(a, c->st); else compress_t3(a, c->st);
-  }
   DME_CUDA(cudaMemcpyAsync(&r_host, c->r_dev, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   DME_CUDA(cudaMemcpyAsync(st_host, c->sstats, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   sync(c);
@@ -446,6 +470,17 @@ int64_t compress(dme_ctx* c, const double* Zc, int64_t k, double* out, bool t3, 
     sync(c);
   }
   if (do_compress) c->stats.last_drop = st_host[2];
+  return r_host;
+}
+
+// Compress the factor Zc (n x k, col-major ldn) into out (n x r); optionally fuse T3(tau3).
+int64_t compress(dme_ctx* c, double* Zc, int64_t k, double* out, bool t3, double tau3,
+                 bool do_compress = true) {
+  if (k <= 0) return 0;
+  SmallArgs a;
+  bool fast = false;
+  compress_launch(c, Zc, k, t3, tau3, do_compress, a, fast);
+  const int64_t r_host = compress_finish(c, a, fast, do_compress);
   if (r_host > 0) {
     ProfScope ps(c, PROF_APPLY);
     tall_small(Zc, c->ldn, c->Tm, KMAX, out, c->ldn, c->n, r_host, k, c->st);
@@ -567,6 +602,50 @@ void run_sequence(dme_ctx* c, const std::vector<Op>& seq) {
   }
 }
 
+// Merged Strang F12F3 body [T12(h) with T3(h) fused] x nb, pipelined: the compression of step t
+// (Gram on all SMs, then the one-CTA eigen kernel) overlaps the look-ahead E pass of step t+1 on the
+// other SMs, using E_h Z_{t+1} = E_h (Zc_t Tm_t) = [E_h L_I(h) | E_h Y_t] Tm_t  (Y_t = E_h Z_t is
+// the factor part of Zc_t; E_h L_I(h) is precomputed at init). Exact reassociation of the same
+// products; only the last body step materialises the state Z.
+void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
+  if (nb <= 0) return;
+  const int64_t ld = c->ldn, q = c->qf, n = c->n;
+  double* Zc = c->Zc12f;
+  epass(c, c->E_full, c->Z, c->r, Zc + q * ld, ld, 1.0);
+  for (int64_t it = 0; it < nb; ++it) {
+    const int64_t k = q + c->r;
+    const bool ahead = c->lookahead && it + 1 < nb;
+    SmallArgs a;
+    bool fast = false;
+    if (ahead) {
+      // the look-ahead pass starts once the Gram has been read (the eigen kernel needs 1 SM,
+      // the pass is launched on #SM - 1 persistent CTAs)
+      compress_launch(c, Zc, k, true, h, true, a, fast, c->ev_gram);
+      DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_gram, 0));
+      epass_on(c, c->E_full, Zc + q * ld, c->r, c->LA + q * ld, ld, 1.0, c->st2, c->gs2);
+      DME_CUDA(cudaEventRecord(c->ev_ahead, c->st2));
+    } else {
+      compress_launch(c, Zc, k, true, h, true, a, fast);
+    }
+    const int64_t rn = compress_finish(c, a, fast, true);
+    if (ahead) {
+      DME_CUDA(cudaStreamWaitEvent(c->st, c->ev_ahead, 0));
+      if (rn > 0) {
+        ProfScope ps(c, PROF_APPLY);
+        tall_small(c->LA, ld, c->Tm, KMAX, Zc + q * ld, ld, n, rn, k, c->st);
+      }
+    } else if (rn > 0) {
+      ProfScope ps(c, PROF_APPLY);
+      tall_small(Zc, ld, c->Tm, KMAX, c->Ztmp, ld, n, rn, k, c->st);
+      swapZ(c);
+    }
+    c->r = rn;
+    c->stats.max_rank = std::max<int64_t>(c->stats.max_rank, c->r);
+    c->stats.steps++;
+    if (c->profile) drain_profile(c);
+  }
+}
+
 // ------------------------------------------------------------------ init: expm + quadrature
 void matmul_sq(dme_ctx* c, const double* X, const double* Y, double* out) {
   // out = X * Y  (n x n row-major): B operand rows = columns of Y = rows of Y^T
@@ -592,6 +671,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   const int64_t n = c->n, ld = c->ldn;
   cudaStream_t st = c->st;
   DME_CUDA(cudaMemsetAsync(c->gs.counters, 0, sizeof(int) * c->gs.max_tiles, st));
+  DME_CUDA(cudaMemsetAsync(c->gs2.counters, 0, sizeof(int) * c->gs2.max_tiles, st));
   // ---------------------------------------------------------------- upload (H2D boundary)
   DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, cudaMemcpyHostToDevice, st));
   if (c->has_S)
@@ -718,6 +798,8 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   ladder_double(c, c->Zc12f, qf, c->E_half);
   c->qf = qf;
   matmul_sq(c, c->E_half, c->E_half, c->E_full);
+  // look-ahead operand: E_h L_I(h) stays in the leading columns of LA
+  epass(c, c->E_full, c->Zc12f, c->qf, c->LA, ld, 1.0);
   c->stats.q_half = c->qh;
   c->stats.q_full = c->qf;
 
@@ -789,6 +871,11 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     if (pr->r0 > 0 && pr->D0) check_psd_host(pr->D0, pr->r0);
     DME_CUDA(cudaSetDevice(o->device));
     c->st = reinterpret_cast<cudaStream_t>(o->stream);
+    int lo_pri = 0, hi_pri = 0;
+    DME_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+    DME_CUDA(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, lo_pri));
+    DME_CUDA(cudaEventCreateWithFlags(&c->ev_gram, cudaEventDisableTiming));
+    DME_CUDA(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming));
     Planner sizing;
     plan_buffers(c, sizing);
     DME_REQUIRE(o->workspace && o->workspace_bytes >= sizing.off + 256, DME_ERR_CAPACITY,
@@ -796,6 +883,7 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     Planner P;
     P.base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(o->workspace) + 255) & ~uintptr_t(255));
     plan_buffers(c, P);
+    c->gs2.max_grid = std::max(1, num_sms() - 1);  // leave one SM to the eigen kernel
     if (c->world > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, o->nccl_uid, sizeof(uid));
@@ -923,9 +1011,13 @@ dme_status dme_split_step(dme_ctx* c, dme_scheme scheme, dme_composition comp, i
       body.insert(body.end(), mid.begin(), mid.end());
       run_sequence(c, first);
       c->stats.steps++;
-      for (int64_t s = 1; s < nsteps; ++s) {
-        run_sequence(c, body);
-        c->stats.steps++;
+      if (comp == DME_F12F3 && c->dre) {
+        run_f12f3_body(c, nsteps - 1, c->h);  // pipelined (look-ahead E pass)
+      } else {
+        for (int64_t s = 1; s < nsteps; ++s) {
+          run_sequence(c, body);
+          c->stats.steps++;
+        }
       }
       run_sequence(c, {seq.back()});
     } else {
@@ -987,6 +1079,9 @@ dme_status dme_destroy(dme_ctx* c) {
   for (auto& r : c->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->pool) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->ev_gram) cudaEventDestroy(c->ev_gram);
+  if (c->ev_ahead) cudaEventDestroy(c->ev_ahead);
   delete c;
   return DME_OK;
 }
