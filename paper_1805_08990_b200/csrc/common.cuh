@@ -84,6 +84,14 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+// Fragment row g (0..7) of an m8n8k4 operand -> row of the 128B-swizzled tile, chosen so that each
+// half-warp (g = 0..3 / 4..7) touches 8 distinct 16-byte chunks under SWIZZLE_128B (chunk ^ (row&7)).
+__device__ __forceinline__ int frag_perm(int g) { return ((g & 3) << 1) | (g >> 2); }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -129,8 +129,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   // ------------------------------------------------------------------ DMMA consumers
   const int g = lane >> 2, t = lane & 3;
+  const int pg = frag_perm(g);
   const int wm = warp % WM, wn = warp / WM;
   const int wm_base = wm * (BM / WM), wn_base = wn * (BN / WN);
+  const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
+  // per-thread byte offsets inside a stage (swizzle: chunk ^ (row & 7) with row & 7 == pg)
+  uint32_t offA[MT], offB[NTW];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi) offA[mi] = (wm_base + mi * 8 + pg) * 128;
+#pragma unroll
+  for (int ni = 0; ni < NTW; ++ni) offB[ni] = (wn_base + ni * 8 + pg) * 128;
   double acc[ACC];
   int stage = 0;
   uint32_t phase = 0;
@@ -143,20 +151,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int i = 0; i < ACC; ++i) acc[i] = 0.0;
     for (; it < stop; ++it) {
       mbar_wait(&full[stage], phase);
-      const unsigned char* a = sA + stage * A_STAGE_BYTES;
-      const unsigned char* b = sB + stage * B_STAGE_BYTES;
+      const uint32_t a = sA_u + stage * A_STAGE_BYTES;
+      const uint32_t b = sB_u + stage * B_STAGE_BYTES;
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
-        // element (r, c) of a 128B-swizzled tile: r*128 + (((c>>1) ^ (r&7)) << 4) + (c&1)*8,
-        // here c = 4*ks + t and r & 7 == g for every fragment row.
-        const int off = ((((ks << 1) + (t >> 1)) ^ g) << 4) + ((t & 1) << 3);
+        const uint32_t off = ((((ks << 1) + (t >> 1)) ^ pg) << 4) + ((t & 1) << 3);
         double af[MT], bf[NTW];
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi)
-          af[mi] = *reinterpret_cast<const double*>(a + (wm_base + mi * 8 + g) * 128 + off);
+        for (int mi = 0; mi < MT; ++mi) af[mi] = lds_f64(a + offA[mi] + off);
 #pragma unroll
-        for (int ni = 0; ni < NTW; ++ni)
-          bf[ni] = *reinterpret_cast<const double*>(b + (wn_base + ni * 8 + g) * 128 + off);
+        for (int ni = 0; ni < NTW; ++ni) bf[ni] = lds_f64(b + offB[ni] + off);
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
@@ -214,8 +218,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int ni = 0; ni < NTW; ++ni)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const long long row = (long long)tm * BM + wm_base + mi * 8 + g;
-            const long long col = (long long)tn * BN + wn_base + ni * 8 + t * 2 + e;
+            const long long row = (long long)tm * BM + wm_base + mi * 8 + pg;
+            const long long col = (long long)tn * BN + wn_base + ni * 8 + frag_perm(t * 2 + e);
             if (row < p.M && col < p.N) {
               double v = p.alpha * acc[(mi * NTW + ni) * 2 + e];
               if (p.beta != 0.0) v += p.beta * p.cin[row * p.cin_rs + col * p.cin_cs];
@@ -245,8 +249,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const Params p) {
     const int wm = warp % WM, wn = warp / WM;
     const int el = i & 1, mn = i >> 1, mi = mn / NTW, ni = mn % NTW;
     const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
-    const long long row = (long long)tm * BM + wm * (BM / WM) + mi * 8 + g;
-    const long long col = (long long)tn * BN + wn * (BN / WN) + ni * 8 + t * 2 + el;
+    const long long row = (long long)tm * BM + wm * (BM / WM) + mi * 8 + frag_perm(g);
+    const long long col = (long long)tn * BN + wn * (BN / WN) + ni * 8 + frag_perm(t * 2 + el);
     if (row < p.M && col < p.N) {
       double v = p.alpha * acc;
       if (p.beta != 0.0) v += p.beta * p.cin[row * p.cin_rs + col * p.cin_cs];
