@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   constexpr int RCH = (FK + 31) / 32;      // column chunks per lane
   constexpr int RPW = (FK + NW - 1) / NW;  // rows per warp
   extern __shared__ double A[];            // k x ld, full symmetric, ld odd
-  __shared__ double d[FK], e[FK], e2[FK], tau[FK], vec[FK], pv[FK];
+  __shared__ double d[FK], e[FK], e2[FK], tau[FK], vec[FK], pv[FK], pv2[FK];
   __shared__ double lam[FK + 1];           // kept eigenvalues (+1 dropped), descending (normalised)
   __shared__ double lo_s[FK + 1], hi_s[FK + 1], slam[FK + 1];
   __shared__ int cnt_s[ENT];
@@ -105,99 +105,102 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   __syncthreads();
 
   // ---------------------------------------------------------------- 1. tridiagonalisation
+  // Step j: reflector H_j = I - tau_j v v^T built from ROW j (= column j, symmetric storage) and
+  // stored back into row j (v_0 = 1 implicit). Two barriers per step: [mat-vec by columns] |
+  // [rank-2 update; warp 0 updates row j+1 first and builds the next reflector from it (look-ahead)].
+  auto householder = [&](int j, double* vv) {  // warp 0 only
+    const int m = k - j - 1;
+    double xs[RCH];
+    double xn2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < RCH; ++u) {
+      const int i = lane + 32 * u;
+      xs[u] = i < m ? A[j * ld + j + 1 + i] : 0.0;
+      if (i >= 1) xn2 = fma(xs[u], xs[u], xn2);
+    }
+    xn2 = warp_sum(xn2);
+    const double alpha = __shfl_sync(0xffffffffu, xs[0], 0);
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      const double amb = alpha - beta;
+      scal = 1.0 / amb;
+      t = -amb / beta;  // (beta - alpha) / beta
+    }
+#pragma unroll
+    for (int u = 0; u < RCH; ++u) {
+      const int i = lane + 32 * u;
+      if (i < m) {
+        const double v = (i == 0) ? 1.0 : (t == 0.0 ? 0.0 : xs[u] * scal);
+        vv[i] = v;
+        if (i > 0) A[j * ld + j + 1 + i] = v;  // reflector kept in row j
+      }
+    }
+    if (lane == 0) {
+      tau[j] = t;
+      e[j] = beta;
+      d[j] = A[j * ld + j];
+    }
+  };
+  if (k > 2 && warp == 0) householder(0, vec);
+  __syncthreads();
   for (int j = 0; j + 2 < k; ++j) {
     const int m = k - j - 1;
-    if (warp == 0) {
-      double xs[RCH];
-      double xn2 = 0.0;
-#pragma unroll
-      for (int u = 0; u < RCH; ++u) {
-        const int i = lane + 32 * u;
-        xs[u] = i < m ? A[(j + 1 + i) * ld + j] : 0.0;
-        if (i >= 1) xn2 = fma(xs[u], xs[u], xn2);
-      }
-      xn2 = warp_sum(xn2);
-      const double alpha = __shfl_sync(0xffffffffu, xs[0], 0);
-      double t = 0.0, beta = alpha, scal = 0.0;
-      if (xn2 > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        const double amb = alpha - beta;
-        scal = 1.0 / amb;
-        t = -amb / beta;  // (beta - alpha) / beta
-      }
-#pragma unroll
-      for (int u = 0; u < RCH; ++u) {
-        const int i = lane + 32 * u;
-        if (i < m) {
-          const double v = (i == 0) ? 1.0 : (t == 0.0 ? 0.0 : xs[u] * scal);
-          vec[i] = v;
-          if (i > 0) A[(j + 1 + i) * ld + j] = v;  // reflector kept below the subdiagonal
-        }
-      }
-      if (lane == 0) {
-        tau[j] = t;
-        e[j] = beta;
-        d[j] = A[j * ld + j];
-      }
-    }
-    __syncthreads();
+    const double* vj = (j & 1) ? pv2 : vec;  // double-buffered reflector
+    double* vn = (j & 1) ? vec : pv2;
     const double tj = tau[j];
-    if (tj == 0.0) continue;  // uniform branch
-    // p = tau * A22 v   (all rows of this warp and all chunks unrolled)
-    {
-      double vl[RCH];
-#pragma unroll
-      for (int u = 0; u < RCH; ++u) vl[u] = (lane + 32 * u < m) ? vec[lane + 32 * u] : 0.0;
-      double acc[RPW];
-#pragma unroll
-      for (int t = 0; t < RPW; ++t) {
-        const int i = warp + NW * t;
-        acc[t] = 0.0;
-        if (i < m) {
-          const double* row = A + (j + 1 + i) * ld + (j + 1);
-#pragma unroll
-          for (int u = 0; u < RCH; ++u)
-            if (lane + 32 * u < m) acc[t] = fma(row[lane + 32 * u], vl[u], acc[t]);
+    // p = tau A22 v by columns (A symmetric): thread i sums A[l][i] v_l over the trailing rows l
+    if (tj != 0.0) {
+      for (int i = tid; i < m; i += ENT) {
+        const double* col = A + (j + 1) * ld + (j + 1 + i);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int l = 0;
+        for (; l + 3 < m; l += 4) {
+          s0 = fma(col[(l + 0) * ld], vj[l + 0], s0);
+          s1 = fma(col[(l + 1) * ld], vj[l + 1], s1);
+          s2 = fma(col[(l + 2) * ld], vj[l + 2], s2);
+          s3 = fma(col[(l + 3) * ld], vj[l + 3], s3);
         }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1)
-#pragma unroll
-        for (int t = 0; t < RPW; ++t) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
-      if (lane == 0) {
-#pragma unroll
-        for (int t = 0; t < RPW; ++t)
-          if (warp + NW * t < m) pv[warp + NW * t] = tj * acc[t];
+        for (; l < m; ++l) s0 = fma(col[l * ld], vj[l], s0);
+        pv[i] = tj * ((s0 + s1) + (s2 + s3));
       }
     }
     __syncthreads();
-    // K = tau/2 p^T v ;  A22 -= v w^T + w v^T  with w = p - K v
-    {
-      double vl[RCH], wl[RCH];
+    if (tj != 0.0) {
+      // K = tau/2 p^T v (every warp, redundantly), w = p - K v
       double dot = 0.0;
 #pragma unroll
       for (int u = 0; u < RCH; ++u) {
         const int l = lane + 32 * u;
-        vl[u] = l < m ? vec[l] : 0.0;
-        wl[u] = l < m ? pv[l] : 0.0;
-        dot = fma(wl[u], vl[u], dot);
+        if (l < m) dot = fma(pv[l], vj[l], dot);
       }
       const double K = 0.5 * tj * warp_sum(dot);
+      if (warp == 0) {
+        // row j+1 (trailing row 0) first, then the next reflector from it
+        const double v0 = vj[0], w0 = pv[0] - K * v0;
 #pragma unroll
-      for (int u = 0; u < RCH; ++u) wl[u] -= K * vl[u];
-#pragma unroll
-      for (int t = 0; t < RPW; ++t) {
-        const int i = warp + NW * t;
-        if (i < m) {
-          double* row = A + (j + 1 + i) * ld + (j + 1);
-          const double vi = vec[i], wi = pv[i] - K * vi;
-#pragma unroll
-          for (int u = 0; u < RCH; ++u) {
-            const int l = lane + 32 * u;
-            if (l < m) row[l] -= vi * wl[u] + wi * vl[u];
+        for (int u = 0; u < RCH; ++u) {
+          const int l = lane + 32 * u;
+          if (l < m) A[(j + 1) * ld + j + 1 + l] -= v0 * (pv[l] - K * vj[l]) + w0 * vj[l];
+        }
+        __syncwarp();
+        if (j + 3 < k) householder(j + 1, vn);
+      } else {
+        // rows 1..m-1 of the trailing block by the other warps: thread per column l, rows strided
+        const int t2 = tid - 32, nt2 = ENT - 32;
+        const int rg = nt2 / m;  // row groups
+        const int l = t2 % m, grp = t2 / m;
+        if (grp < rg) {
+          const double vl = vj[l], wl = pv[l] - K * vl;
+          for (int i = 1 + grp; i < m; i += rg) {
+            const double vi = vj[i], wi = pv[i] - K * vi;
+            double* a_ = A + (j + 1 + i) * ld + (j + 1 + l);
+            *a_ -= vi * wl + wi * vl;
           }
         }
       }
+    } else if (warp == 0 && j + 3 < k) {
+      householder(j + 1, vn);
     }
     __syncthreads();
   }
@@ -283,7 +286,9 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
     }
     __syncthreads();
     const double bits = log2((double)P + 1.0);
-    const int nit = (int)ceil(log2((s_hi - s_lo) / 4e-16 + 1.0) / bits) + 1;
+    // absolute accuracy 1e-13 ||T||: enough for the twisted vectors (their error ~ |dlambda| / gap
+    // only matters weighted by theta)
+    const int nit = (int)ceil(log2((s_hi - s_lo) / 1e-13 + 1.0) / bits) + 1;
     for (int it = 0; it < nit; ++it) {
       if (act) {
         const double a0 = lo_s[grp], b0 = hi_s[grp];
@@ -311,57 +316,75 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   t_ph[3] = clock64();
 
   // ---------------------------------------------------------------- 3. twisted-factorisation vectors
-  // thread c < r: eigenvector of lam[c]; D+ in V[:, c], D- in Tm[:, c] (global scratch)
-  if (tid < r) {
-    const int c = tid;
+  // lane pair (2c, 2c+1) per eigenvector: the even lane runs the top-down pivots D+, the odd lane the
+  // bottom-up pivots D- (two independent division chains), then each runs one product chain.
+  // D+ in V[:, c], D- in Tm[:, c] (global scratch), the vector into V[:, c].
+  if (tid < 2 * r) {
+    const unsigned msk = __activemask();  // lane pairs are always complete (2r is even)
+    const int c = tid >> 1, side = tid & 1;
     const double lm = lam[c];
     double* Dp = a.V + (size_t)c * a.ldv;
     double* Dm = a.Tm + (size_t)c * a.ldt;
     const double pivmin = 1e-290;
-    double x = d[0] - lm;
-    if (fabs(x) < pivmin) x = -pivmin;
-    Dp[0] = x;
-    for (int i = 1; i < k; ++i) {
-      x = (d[i] - lm) - e2[i - 1] / x;
+    if (side == 0) {
+      double x = d[0] - lm;
       if (fabs(x) < pivmin) x = -pivmin;
-      Dp[i] = x;
-    }
-    x = d[k - 1] - lm;
-    if (fabs(x) < pivmin) x = -pivmin;
-    Dm[k - 1] = x;
-    for (int i = k - 2; i >= 0; --i) {
-      x = (d[i] - lm) - e2[i] / x;
+      Dp[0] = x;
+      for (int i = 1; i < k; ++i) {
+        x = (d[i] - lm) - e2[i - 1] / x;
+        if (fabs(x) < pivmin) x = -pivmin;
+        Dp[i] = x;
+      }
+    } else {
+      double x = d[k - 1] - lm;
       if (fabs(x) < pivmin) x = -pivmin;
-      Dm[i] = x;
+      Dm[k - 1] = x;
+      for (int i = k - 2; i >= 0; --i) {
+        x = (d[i] - lm) - e2[i] / x;
+        if (fabs(x) < pivmin) x = -pivmin;
+        Dm[i] = x;
+      }
     }
-    int tw = 0;
+    __syncwarp(msk);
+    __threadfence_block();
+    // twist index: argmin |gamma_i|, the two lanes scan halves
+    const int h0 = side ? k / 2 : 0, h1 = side ? k : k / 2;
+    int tw = h0;
     double best = 1e300;
-#pragma unroll 8
-    for (int i = 0; i < k; ++i) {
+    for (int i = h0; i < h1; ++i) {
       const double g = Dp[i] + Dm[i] - (d[i] - lm);
       if (fabs(g) < best) { best = fabs(g); tw = i; }
     }
-    // ratios first (independent divisions), then the product chains
-#pragma unroll 8
-    for (int i = 0; i < tw; ++i) Dp[i] = -e[i] / Dp[i];
-#pragma unroll 8
-    for (int i = tw + 1; i < k; ++i) Dm[i] = -e[i - 1] / Dm[i];
-    double zi = 1.0, nrm2 = 1.0;
-    for (int i = tw - 1; i >= 0; --i) {
-      zi *= Dp[i];
-      nrm2 = fma(zi, zi, nrm2);
-      Dp[i] = zi;
+    const double ob = __shfl_xor_sync(msk, best, 1);
+    const int ot = __shfl_xor_sync(msk, tw, 1);
+    if (ob < best || (ob == best && ot < tw)) { best = ob; tw = ot; }
+    // ratios then products: even lane i < tw (with D+), odd lane i > tw (with D-)
+    double nrm2 = 0.0;
+    if (side == 0) {
+      for (int i = 0; i < tw; ++i) Dp[i] = -e[i] / Dp[i];
+      double zi = 1.0;
+      for (int i = tw - 1; i >= 0; --i) {
+        zi *= Dp[i];
+        nrm2 = fma(zi, zi, nrm2);
+        Dp[i] = zi;
+      }
+    } else {
+      for (int i = tw + 1; i < k; ++i) Dm[i] = -e[i - 1] / Dm[i];
+      double zi = 1.0;
+      for (int i = tw + 1; i < k; ++i) {
+        zi *= Dm[i];
+        nrm2 = fma(zi, zi, nrm2);
+        Dp[i] = zi;
+      }
     }
-    zi = 1.0;
-    for (int i = tw + 1; i < k; ++i) {
-      zi *= Dm[i];
-      nrm2 = fma(zi, zi, nrm2);
-      Dp[i] = zi;
-    }
-    Dp[tw] = 1.0;
-    const double inv = 1.0 / sqrt(nrm2);
-#pragma unroll 8
-    for (int i = 0; i < k; ++i) Dp[i] *= inv;
+    nrm2 += __shfl_xor_sync(msk, nrm2, 1);
+    __syncwarp(msk);
+    __threadfence_block();
+    if (side == 0) Dp[tw] = 1.0;
+    __syncwarp(msk);
+    __threadfence_block();
+    const double inv = 1.0 / sqrt(1.0 + nrm2);
+    for (int i = side; i < k; i += 2) Dp[i] *= inv;
   }
   __syncthreads();
   t_ph[4] = clock64();
@@ -389,7 +412,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
 #pragma unroll
           for (int u = 0; u < RCH; ++u) {
             const int i = lane + 32 * u;
-            vr[u] = (i == j + 1) ? 1.0 : ((i > j + 1 && i < k) ? A[i * ld + j] : 0.0);
+            vr[u] = (i == j + 1) ? 1.0 : ((i > j + 1 && i < k) ? A[j * ld + i] : 0.0);
           }
           double s[CP];
 #pragma unroll
