@@ -106,7 +106,7 @@ struct dme_ctx {
   // persistent device buffers
   double *E_half = nullptr, *E_full = nullptr, *S = nullptr, *Bcol = nullptr, *LQ = nullptr;
   double *Zc12h = nullptr, *Zc12f = nullptr, *Zc2 = nullptr, *Z = nullptr, *Ztmp = nullptr;
-  double *G = nullptr, *H = nullptr, *Tm = nullptr, *Vg = nullptr, *LRinv = nullptr, *sstats = nullptr;
+  double *G = nullptr, *H = nullptr, *Tm = nullptr, *Vg = nullptr, *Es = nullptr, *LRinv = nullptr, *sstats = nullptr;
   double *norm_dev = nullptr, *red_scratch = nullptr, *stage = nullptr;
   double *LA = nullptr;  // look-ahead operand [E_h L_I(h) | E_h Y]  (ldn x KMAX)
   int* r_dev = nullptr;
@@ -153,6 +153,7 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   c->H = P.take<double>((size_t)KMAX * SMALL_M_MAX);
   c->Tm = P.take<double>((size_t)KMAX * KMAX);
   c->Vg = P.take<double>((size_t)KMAX * KMAX);
+  c->Es = P.take<double>(eig_split_scratch_doubles());
   c->LRinv = P.take<double>(SMALL_M_MAX * SMALL_M_MAX);
   c->sstats = P.take<double>(16);
   c->norm_dev = P.take<double>(16);
@@ -445,11 +446,14 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
   a.tau = tau3;
   a.Tm = c->Tm; a.ldt = KMAX;
   a.V = c->Vg; a.ldv = KMAX;
+  a.Es = c->Es;
   a.r_out = c->r_dev;
   a.stats = c->sstats;
   fast = do_compress && k <= FAST_K_MAX && !c->force_jacobi;
   ProfScope ps(c, PROF_SMALL);
-  if (fast) eig_fast(a, c->st); else compress_t3(a, c->st);
+  if (fast && k >= EIG_SPLIT_MIN) eig_split(a, c->st);
+  else if (fast) eig_fast(a, c->st);
+  else compress_t3(a, c->st);
 }
 
 // Wait for the small kernel (main stream only), fall back to Jacobi if the fast path refused.
@@ -883,7 +887,7 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     Planner P;
     P.base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(o->workspace) + 255) & ~uintptr_t(255));
     plan_buffers(c, P);
-    c->gs2.max_grid = std::max(1, num_sms() - 1);  // leave one SM to the eigen kernel
+    c->gs2.max_grid = std::max(1, num_sms() - EIG_SPLIT_CTAS);  // SMs left to the eigen kernels
     if (c->world > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, o->nccl_uid, sizeof(uid));

@@ -1,0 +1,200 @@
+// Device pieces shared by the one-CTA fast eigen kernel (eig_fast.cu) and the split eigen kernels
+// (eig_split.cu): Sturm counts and the shared-memory Householder tridiagonalisation.
+#pragma once
+#include "common.cuh"
+#include "small.h"
+#include "small_common.cuh"
+
+namespace dme {
+namespace eigk {
+
+constexpr int ENT = 512;  // threads of the eigen kernels (16 warps, up to 128 registers each)
+constexpr int NW = ENT / 32;
+
+// number of eigenvalues of T (d, e2 = e^2, normalised to ||T|| <= 1) smaller than x:
+// sign changes of the leading principal minors p_i of T - xI (an exact zero counts as negative,
+// a measure-zero event that only moves a bisection probe by one count)
+__device__ __forceinline__ int sturm_count(const double* __restrict__ d,
+                                           const double* __restrict__ e2, int k, double x) {
+  double p2 = 1.0, p1 = d[0] - x;
+  bool neg_prev = p1 <= 0.0;
+  int cnt = neg_prev;
+  int i = 1;
+  for (; i + 3 < k; i += 4) {
+    const double d0 = d[i], d1 = d[i + 1], d2 = d[i + 2], d3 = d[i + 3];
+    const double f0 = e2[i - 1], f1 = e2[i], f2 = e2[i + 1], f3 = e2[i + 2];
+    double p;
+    bool ng;
+    p = fma(d0 - x, p1, -f0 * p2); ng = p <= 0.0; cnt += ng != neg_prev; neg_prev = ng; p2 = p1; p1 = p;
+    p = fma(d1 - x, p1, -f1 * p2); ng = p <= 0.0; cnt += ng != neg_prev; neg_prev = ng; p2 = p1; p1 = p;
+    p = fma(d2 - x, p1, -f2 * p2); ng = p <= 0.0; cnt += ng != neg_prev; neg_prev = ng; p2 = p1; p1 = p;
+    p = fma(d3 - x, p1, -f3 * p2); ng = p <= 0.0; cnt += ng != neg_prev; neg_prev = ng; p2 = p1; p1 = p;
+    // growth per element <= 3 (||T|| <= 1): rescale rarely, by an exact power of two
+    const double m1 = fmax(fabs(p1), fabs(p2));
+    if (m1 > 0x1p400) { p1 *= 0x1p-400; p2 *= 0x1p-400; }
+    else if (m1 < 0x1p-400) { p1 *= 0x1p400; p2 *= 0x1p400; }
+  }
+  for (; i < k; ++i) {
+    const double p = fma(d[i] - x, p1, -e2[i - 1] * p2);
+    const bool ng = p <= 0.0;
+    cnt += ng != neg_prev;
+    neg_prev = ng;
+    p2 = p1;
+    p1 = p;
+  }
+  return cnt;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+
+// Householder tridiagonalisation of the symmetric k x k matrix in A (row stride ld, shared
+// memory), in place: d, e (unnormalised) and tau; reflector j kept in row j (v_0 = 1 implicit).
+template <int FK>
+__device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, double* tau,
+                               double* vec, double* pv, double* pv2) {
+  constexpr int RCH = (FK + 31) / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // Step j: reflector H_j = I - tau_j v v^T built from ROW j (= column j, symmetric storage) and
+  // stored back into row j (v_0 = 1 implicit). Two barriers per step: [mat-vec by columns] |
+  // [rank-2 update; warp 0 updates row j+1 first and builds the next reflector from it (look-ahead)].
+  auto householder = [&](int j, double* vv) {  // warp 0 only
+    const int m = k - j - 1;
+    double xs[RCH];
+    double xn2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < RCH; ++u) {
+      const int i = lane + 32 * u;
+      xs[u] = i < m ? A[j * ld + j + 1 + i] : 0.0;
+      if (i >= 1) xn2 = fma(xs[u], xs[u], xn2);
+    }
+    xn2 = warp_sum(xn2);
+    const double alpha = __shfl_sync(0xffffffffu, xs[0], 0);
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      const double amb = alpha - beta;
+      const double inv = 1.0 / (amb * beta);  // one division for both quotients
+      scal = beta * inv;                      // 1 / (alpha - beta)
+      t = -amb * amb * inv;                   // (beta - alpha) / beta
+    }
+#pragma unroll
+    for (int u = 0; u < RCH; ++u) {
+      const int i = lane + 32 * u;
+      if (i < m) {
+        const double v = (i == 0) ? 1.0 : (t == 0.0 ? 0.0 : xs[u] * scal);
+        vv[i] = v;
+        if (i > 0) A[j * ld + j + 1 + i] = v;  // reflector kept in row j
+      }
+    }
+    if (lane == 0) {
+      tau[j] = t;
+      e[j] = beta;
+      d[j] = A[j * ld + j];
+    }
+  };
+  if (k > 2 && warp == 0) householder(0, vec);
+  __syncthreads();
+  for (int j = 0; j + 2 < k; ++j) {
+    const int m = k - j - 1;
+    const double* vj = (j & 1) ? pv2 : vec;  // double-buffered reflector
+    double* vn = (j & 1) ? vec : pv2;
+    const double tj = tau[j];
+    // p = tau A22 v by columns (A symmetric): thread i sums A[l][i] v_l over the trailing rows l
+    if (tj != 0.0) {
+      for (int i = tid; i < m; i += ENT) {
+        const double* col = A + (j + 1) * ld + (j + 1 + i);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int l = 0;
+        for (; l + 3 < m; l += 4) {
+          s0 = fma(col[(l + 0) * ld], vj[l + 0], s0);
+          s1 = fma(col[(l + 1) * ld], vj[l + 1], s1);
+          s2 = fma(col[(l + 2) * ld], vj[l + 2], s2);
+          s3 = fma(col[(l + 3) * ld], vj[l + 3], s3);
+        }
+        for (; l < m; ++l) s0 = fma(col[l * ld], vj[l], s0);
+        pv[i] = tj * ((s0 + s1) + (s2 + s3));
+      }
+    }
+    __syncthreads();
+    if (tj != 0.0) {
+      // K = tau/2 p^T v (every warp, redundantly), w = p - K v
+      double dot = 0.0;
+#pragma unroll
+      for (int u = 0; u < RCH; ++u) {
+        const int l = lane + 32 * u;
+        if (l < m) dot = fma(pv[l], vj[l], dot);
+      }
+      const double K = 0.5 * tj * warp_sum(dot);
+      if (warp == 0) {
+        // row j+1 (trailing row 0) first, then the next reflector from it
+        const double v0 = vj[0], w0 = pv[0] - K * v0;
+#pragma unroll
+        for (int u = 0; u < RCH; ++u) {
+          const int l = lane + 32 * u;
+          if (l < m) A[(j + 1) * ld + j + 1 + l] -= v0 * (pv[l] - K * vj[l]) + w0 * vj[l];
+        }
+        __syncwarp();
+        if (j + 3 < k) householder(j + 1, vn);
+      } else {
+        // rows 1..m-1 of the trailing block by the other warps: thread per column l, rows strided
+        const int t2 = tid - 32, nt2 = ENT - 32;
+        const int rg = nt2 / m;  // row groups
+        const int l = t2 % m, grp = t2 / m;
+        if (grp < rg) {
+          const double vl = vj[l], wl = pv[l] - K * vl;
+          for (int i = 1 + grp; i < m; i += rg) {
+            const double vi = vj[i], wi = pv[i] - K * vi;
+            double* a_ = A + (j + 1 + i) * ld + (j + 1 + l);
+            *a_ -= vi * wl + wi * vl;
+          }
+        }
+      }
+    } else if (warp == 0 && j + 3 < k) {
+      householder(j + 1, vn);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (k >= 2) {
+      d[k - 2] = A[(k - 2) * ld + (k - 2)];
+      e[k - 2] = A[(k - 1) * ld + (k - 2)];
+    }
+    d[k - 1] = A[(k - 1) * ld + (k - 1)];
+  }
+  __syncthreads();
+}
+
+// Normalise T by a Gershgorin bound of ||T||; e2 = e^2; Gershgorin interval [lo, hi]. Thread 0.
+__device__ inline void normalise_tridiagonal(int k, double* d, double* e, double* e2, double* scale,
+                                             double* lo_out, double* hi_out) {
+  double nrm = 0.0, lo = 1e300, hi = -1e300;
+  for (int i = 0; i < k; ++i) {
+    const double rr = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < k ? fabs(e[i]) : 0.0);
+    nrm = fmax(nrm, fabs(d[i]) + rr);
+  }
+  if (!(nrm > 0.0)) nrm = 1.0;
+  *scale = nrm;
+  const double inv = 1.0 / nrm;
+  for (int i = 0; i < k; ++i) {
+    d[i] *= inv;
+    if (i + 1 < k) {
+      e[i] *= inv;
+      e2[i] = e[i] * e[i];
+    }
+  }
+  for (int i = 0; i < k; ++i) {
+    const double rr = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < k ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - rr);
+    hi = fmax(hi, d[i] + rr);
+  }
+  *lo_out = lo - 1e-14;
+  *hi_out = hi + 1e-14;
+}
+
+}  // namespace eigk
+}  // namespace dme

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "small.h"
 #include "small_common.cuh"
+#include "eig_common.cuh"
 
 #include <cmath>
 
@@ -27,54 +28,7 @@ namespace dme {
 
 namespace {
 
-constexpr int ENT = 512;  // threads of the fast eigen kernel (16 warps, up to 128 registers each)
-constexpr int NW = ENT / 32;
-
-// number of eigenvalues of T (d, e2 = e^2, normalised to ||T|| <= 1) smaller than x
-__device__ __forceinline__ int sturm_count(const double* __restrict__ d,
-                                           const double* __restrict__ e2, int k, double x) {
-  double p2 = 1.0, p1 = d[0] - x;
-  int neg_prev = p1 <= 0.0;
-  int cnt = neg_prev;
-  int i = 1;
-  for (; i + 3 < k; i += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double p = fma(d[i + u] - x, p1, -e2[i + u - 1] * p2);
-      const long long b = __double_as_longlong(p);
-      const int neg = (b < 0) | ((((unsigned long long)b << 1) == 0ull) & !neg_prev);
-      cnt += neg ^ neg_prev;
-      neg_prev = neg;
-      p2 = p1;
-      p1 = p;
-    }
-    const int ex1 = (int)((__double_as_longlong(p1) >> 52) & 0x7ff);
-    const int ex2 = (int)((__double_as_longlong(p2) >> 52) & 0x7ff);
-    if (ex1 > 1023 + 400 || ex2 > 1023 + 400) {
-      p1 *= 0x1p-400;
-      p2 *= 0x1p-400;
-    } else if (ex1 < 1023 - 400 && ex2 < 1023 - 400) {
-      p1 *= 0x1p400;
-      p2 *= 0x1p400;
-    }
-  }
-  for (; i < k; ++i) {
-    const double p = fma(d[i] - x, p1, -e2[i - 1] * p2);
-    const long long b = __double_as_longlong(p);
-    const int neg = (b < 0) | ((((unsigned long long)b << 1) == 0ull) & !neg_prev);
-    cnt += neg ^ neg_prev;
-    neg_prev = neg;
-    p2 = p1;
-    p1 = p;
-  }
-  return cnt;
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+using namespace eigk;
 
 template <int FK>
 __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
@@ -105,134 +59,9 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   __syncthreads();
 
   // ---------------------------------------------------------------- 1. tridiagonalisation
-  // Step j: reflector H_j = I - tau_j v v^T built from ROW j (= column j, symmetric storage) and
-  // stored back into row j (v_0 = 1 implicit). Two barriers per step: [mat-vec by columns] |
-  // [rank-2 update; warp 0 updates row j+1 first and builds the next reflector from it (look-ahead)].
-  auto householder = [&](int j, double* vv) {  // warp 0 only
-    const int m = k - j - 1;
-    double xs[RCH];
-    double xn2 = 0.0;
-#pragma unroll
-    for (int u = 0; u < RCH; ++u) {
-      const int i = lane + 32 * u;
-      xs[u] = i < m ? A[j * ld + j + 1 + i] : 0.0;
-      if (i >= 1) xn2 = fma(xs[u], xs[u], xn2);
-    }
-    xn2 = warp_sum(xn2);
-    const double alpha = __shfl_sync(0xffffffffu, xs[0], 0);
-    double t = 0.0, beta = alpha, scal = 0.0;
-    if (xn2 > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-      const double amb = alpha - beta;
-      scal = 1.0 / amb;
-      t = -amb / beta;  // (beta - alpha) / beta
-    }
-#pragma unroll
-    for (int u = 0; u < RCH; ++u) {
-      const int i = lane + 32 * u;
-      if (i < m) {
-        const double v = (i == 0) ? 1.0 : (t == 0.0 ? 0.0 : xs[u] * scal);
-        vv[i] = v;
-        if (i > 0) A[j * ld + j + 1 + i] = v;  // reflector kept in row j
-      }
-    }
-    if (lane == 0) {
-      tau[j] = t;
-      e[j] = beta;
-      d[j] = A[j * ld + j];
-    }
-  };
-  if (k > 2 && warp == 0) householder(0, vec);
-  __syncthreads();
-  for (int j = 0; j + 2 < k; ++j) {
-    const int m = k - j - 1;
-    const double* vj = (j & 1) ? pv2 : vec;  // double-buffered reflector
-    double* vn = (j & 1) ? vec : pv2;
-    const double tj = tau[j];
-    // p = tau A22 v by columns (A symmetric): thread i sums A[l][i] v_l over the trailing rows l
-    if (tj != 0.0) {
-      for (int i = tid; i < m; i += ENT) {
-        const double* col = A + (j + 1) * ld + (j + 1 + i);
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int l = 0;
-        for (; l + 3 < m; l += 4) {
-          s0 = fma(col[(l + 0) * ld], vj[l + 0], s0);
-          s1 = fma(col[(l + 1) * ld], vj[l + 1], s1);
-          s2 = fma(col[(l + 2) * ld], vj[l + 2], s2);
-          s3 = fma(col[(l + 3) * ld], vj[l + 3], s3);
-        }
-        for (; l < m; ++l) s0 = fma(col[l * ld], vj[l], s0);
-        pv[i] = tj * ((s0 + s1) + (s2 + s3));
-      }
-    }
-    __syncthreads();
-    if (tj != 0.0) {
-      // K = tau/2 p^T v (every warp, redundantly), w = p - K v
-      double dot = 0.0;
-#pragma unroll
-      for (int u = 0; u < RCH; ++u) {
-        const int l = lane + 32 * u;
-        if (l < m) dot = fma(pv[l], vj[l], dot);
-      }
-      const double K = 0.5 * tj * warp_sum(dot);
-      if (warp == 0) {
-        // row j+1 (trailing row 0) first, then the next reflector from it
-        const double v0 = vj[0], w0 = pv[0] - K * v0;
-#pragma unroll
-        for (int u = 0; u < RCH; ++u) {
-          const int l = lane + 32 * u;
-          if (l < m) A[(j + 1) * ld + j + 1 + l] -= v0 * (pv[l] - K * vj[l]) + w0 * vj[l];
-        }
-        __syncwarp();
-        if (j + 3 < k) householder(j + 1, vn);
-      } else {
-        // rows 1..m-1 of the trailing block by the other warps: thread per column l, rows strided
-        const int t2 = tid - 32, nt2 = ENT - 32;
-        const int rg = nt2 / m;  // row groups
-        const int l = t2 % m, grp = t2 / m;
-        if (grp < rg) {
-          const double vl = vj[l], wl = pv[l] - K * vl;
-          for (int i = 1 + grp; i < m; i += rg) {
-            const double vi = vj[i], wi = pv[i] - K * vi;
-            double* a_ = A + (j + 1 + i) * ld + (j + 1 + l);
-            *a_ -= vi * wl + wi * vl;
-          }
-        }
-      }
-    } else if (warp == 0 && j + 3 < k) {
-      householder(j + 1, vn);
-    }
-    __syncthreads();
-  }
+  tridiagonalise<FK>(A, k, ld, d, e, tau, vec, pv, pv2);
   if (tid == 0) {
-    if (k >= 2) {
-      d[k - 2] = A[(k - 2) * ld + (k - 2)];
-      e[k - 2] = A[(k - 1) * ld + (k - 2)];
-    }
-    d[k - 1] = A[(k - 1) * ld + (k - 1)];
-    // normalisation by a Gershgorin bound of ||T||
-    double nrm = 0.0, lo = 1e300, hi = -1e300;
-    for (int i = 0; i < k; ++i) {
-      const double rr = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < k ? fabs(e[i]) : 0.0);
-      nrm = fmax(nrm, fabs(d[i]) + rr);
-    }
-    if (!(nrm > 0.0)) nrm = 1.0;
-    s_scale = nrm;
-    const double inv = 1.0 / nrm;
-    for (int i = 0; i < k; ++i) {
-      d[i] *= inv;
-      if (i + 1 < k) {
-        e[i] *= inv;
-        e2[i] = e[i] * e[i];
-      }
-    }
-    for (int i = 0; i < k; ++i) {
-      const double rr = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < k ? fabs(e[i]) : 0.0);
-      lo = fmin(lo, d[i] - rr);
-      hi = fmax(hi, d[i] + rr);
-    }
-    s_lo = lo - 1e-14;
-    s_hi = hi + 1e-14;
+    normalise_tridiagonal(k, d, e, e2, &s_scale, &s_lo, &s_hi);
     s_lo_t = s_lo;
     s_hi_t = s_hi;
   }
@@ -243,7 +72,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   // largest eigenvalue: 256 probes per round (8 bits), transition found in parallel
   {
     constexpr int PB = 256;
-    for (int it = 0; it < 7; ++it) {
+    for (int it = 0; it < 2; ++it) {  // 16 bits: the threshold needs ~3 digits
       const double a0 = s_lo_t, b0 = s_hi_t;
       if (tid < PB) cnt_s[tid] = sturm_count(d, e2, k, a0 + (b0 - a0) * (tid + 1) / (PB + 1.0));
       __syncthreads();
@@ -389,8 +218,39 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   __syncthreads();
   t_ph[4] = clock64();
 
-  // ---------------------------------------------------------------- 4. W = Q Z (warp-owned columns)
-  {
+  // ---------------------------------------------------------------- 4. W = Q Z
+  if (FK <= 96) {
+    // Thread c applies H_{k-3} ... H_0 to its own column z_c, kept in shared memory right after the
+    // reflectors (column-major, odd leading dimension: a warp's columns spread over all banks).
+    const int ldz = k | 1;
+    double* zs = A + (size_t)k * ld;
+    if (tid < r) {
+      const int c = tid;
+      double* z = zs + (size_t)c * ldz;
+      for (int i = 0; i < k; ++i) z[i] = a.V[i + (size_t)c * a.ldv];
+      for (int j = k - 3; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj == 0.0) continue;
+        const double* v = A + j * ld + j + 1;  // v_0 = 1 (implicit), v_i at row j
+        double* zz = z + j + 1;
+        const int m = k - j - 1;
+        double s0 = zz[0], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int i = 1;
+        for (; i + 2 < m; i += 3) {
+          s1 = fma(v[i], zz[i], s1);
+          s2 = fma(v[i + 1], zz[i + 1], s2);
+          s3 = fma(v[i + 2], zz[i + 2], s3);
+        }
+        for (; i < m; ++i) s1 = fma(v[i], zz[i], s1);
+        const double f = tj * ((s0 + s1) + (s2 + s3));
+        zz[0] -= f;
+        for (i = 1; i < m; ++i) zz[i] = fma(-f, v[i], zz[i]);
+      }
+      const double fs = a.sqrt_scale ? sqrt(fmax(lam[c] * s_scale, 0.0)) : 1.0;
+      for (int i = 0; i < k; ++i) a.Tm[i + (size_t)c * a.ldt] = z[i] * fs;
+    }
+  } else {
+    // warp-owned column blocks, Z in registers, one warp reduction per reflector and column
     constexpr int CP = 4;  // columns per warp per pass (register budget)
     const double sc = s_scale;
     for (int pass = 0; pass * NW * CP < r; ++pass) {
@@ -414,20 +274,20 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
             const int i = lane + 32 * u;
             vr[u] = (i == j + 1) ? 1.0 : ((i > j + 1 && i < k) ? A[j * ld + i] : 0.0);
           }
-          double s[CP];
+          double sv[CP];
 #pragma unroll
           for (int cc = 0; cc < CP; ++cc) {
-            s[cc] = 0.0;
+            sv[cc] = 0.0;
 #pragma unroll
-            for (int u = 0; u < RCH; ++u) s[cc] = fma(vr[u], z[cc][u], s[cc]);
+            for (int u = 0; u < RCH; ++u) sv[cc] = fma(vr[u], z[cc][u], sv[cc]);
           }
 #pragma unroll
           for (int o = 16; o; o >>= 1)
 #pragma unroll
-            for (int cc = 0; cc < CP; ++cc) s[cc] += __shfl_xor_sync(0xffffffffu, s[cc], o);
+            for (int cc = 0; cc < CP; ++cc) sv[cc] += __shfl_xor_sync(0xffffffffu, sv[cc], o);
 #pragma unroll
           for (int cc = 0; cc < CP; ++cc) {
-            const double f = tj * s[cc];
+            const double f = tj * sv[cc];
 #pragma unroll
             for (int u = 0; u < RCH; ++u) z[cc][u] -= f * vr[u];
           }
@@ -446,13 +306,13 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
         }
       }
     }
-    __syncthreads();  // all reflector reads from A done before A is reused
-    // W^T (row-major) into shared memory for the check (unscaled)
-    for (int e_ = tid; e_ < k * r; e_ += ENT) {
-      const int i = e_ % k, c = e_ / k;
-      const double f = a.sqrt_scale ? sqrt(fmax(lam[c] * sc, 0.0)) : 1.0;
-      A[c * ld + i] = f > 0.0 ? a.Tm[i + (size_t)c * a.ldt] / f : 0.0;
-    }
+  }
+  __syncthreads();  // all reflector reads from A done before A is reused
+  // W^T (row-major) into shared memory for the check (unscaled)
+  for (int e_ = tid; e_ < k * r; e_ += ENT) {
+    const int i = e_ % k, c = e_ / k;
+    const double f = a.sqrt_scale ? sqrt(fmax(lam[c] * s_scale, 0.0)) : 1.0;
+    A[c * ld + i] = f > 0.0 ? a.Tm[i + (size_t)c * a.ldt] / f : 0.0;
   }
   __syncthreads();
   t_ph[5] = clock64();
@@ -530,11 +390,15 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
 template <int FK>
 void launch_fast(const SmallArgs& a, cudaStream_t st) {
   const size_t floor_b = sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX;
-  const size_t need = sizeof(double) * (size_t)FK * (FK | 1);
-  size_t smem = sizeof(double) * (size_t)a.k * (a.k | 1);
+  auto bytes_for = [](int k) {
+    // reflectors (k x (k|1)) + the back-transformation columns (<= k x (k|1)) for the small class
+    return sizeof(double) * (size_t)k * (k | 1) * (FK <= 96 ? 2 : 1);
+  };
+  size_t smem = bytes_for(a.k);
   if (smem < floor_b) smem = floor_b;
   static bool attr = false;
   if (!attr) {
+    const size_t need = bytes_for(FK);
     DME_CUDA(cudaFuncSetAttribute(eig_fast_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(need > floor_b ? need : floor_b)));
     attr = true;

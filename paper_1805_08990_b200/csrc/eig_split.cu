@@ -1,0 +1,395 @@
+// Split eigen-compression for the hot path (k = r + q_I >= EIG_SPLIT_MIN): the same mathematics as
+// eig_fast.cu (G = W Theta W^T, Tm = W_kept, weighted orthogonality check, fused T3) spread over
+// three launches so the parallel part does not run on a single SM:
+//   TRI (1 CTA)       Householder tridiagonalisation, normalisation, theta_max and the rank r
+//                     (Sturm counts); T and the reflectors go to the global scratch Es.
+//   VEC (EIG_SPLIT_CTAS CTAs)  each CTA owns a contiguous slice of the kept eigenvalues (+ the first
+//                     dropped one, for the stats): multisection with up to 64 probes per eigenvalue,
+//                     twisted-factorisation vectors (lane pairs), back-transformation by the
+//                     reflectors (one warp per column, column in registers), Tm columns written.
+//   FIN (1 CTA)       weighted orthogonality check (fallback flag), stats, fused Riccati flow T3.
+// The look-ahead E pass of the step runs on #SM - EIG_SPLIT_CTAS persistent CTAs meanwhile.
+#include "common.cuh"
+#include "eig_common.cuh"
+#include "small.h"
+#include "small_common.cuh"
+
+#include <cmath>
+
+namespace dme {
+
+namespace {
+
+using namespace eigk;
+
+// global scratch layout (doubles)
+struct EsLayout {
+  static constexpr int HDR = 16;
+  double* base;
+  int KM;  // capacity (SMALL_K_MAX)
+  __host__ __device__ double* hdr() const { return base; }
+  __host__ __device__ double* d() const { return base + HDR; }
+  __host__ __device__ double* e() const { return base + HDR + KM; }
+  __host__ __device__ double* e2() const { return base + HDR + 2 * KM; }
+  __host__ __device__ double* tau() const { return base + HDR + 3 * KM; }
+  __host__ __device__ double* lam() const { return base + HDR + 4 * KM; }  // KM + 1
+  __host__ __device__ double* refl() const { return base + HDR + 5 * KM + 8; }  // k x ld
+  __host__ __device__ double* dp() const { return refl() + (size_t)KM * (KM | 1); }  // KM x KM
+  __host__ __device__ double* dm() const { return dp() + (size_t)KM * KM; }
+};
+
+template <int FK>
+__global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
+  extern __shared__ double A[];
+  __shared__ double d[FK], e[FK], e2[FK], tau[FK], vec[FK], pv[FK], pv2[FK];
+  __shared__ int cnt_s[256];
+  __shared__ double s_scale, s_lo, s_hi, s_lo_t, s_hi_t;
+  const int tid = threadIdx.x;
+  const int k = a.k, ld = k | 1;
+  const EsLayout es{a.Es, SMALL_K_MAX};
+  for (int e_ = tid; e_ < k * k; e_ += ENT) {
+    const int i = e_ % k, j = e_ / k;
+    A[i * ld + j] = 0.5 * (a.G[i + (size_t)j * a.ldg] + a.G[j + (size_t)i * a.ldg]);
+  }
+  __syncthreads();
+  tridiagonalise<FK>(A, k, ld, d, e, tau, vec, pv, pv2);
+  if (tid == 0) {
+    normalise_tridiagonal(k, d, e, e2, &s_scale, &s_lo, &s_hi);
+    s_lo_t = s_lo;
+    s_hi_t = s_hi;
+  }
+  __syncthreads();
+  // theta_max to 16 bits (enough for the threshold; it is refined with the others in VEC)
+  constexpr int PB = 256;
+  for (int it = 0; it < 2; ++it) {
+    const double a0 = s_lo_t, b0 = s_hi_t;
+    if (tid < PB) cnt_s[tid] = sturm_count(d, e2, k, a0 + (b0 - a0) * (tid + 1) / (PB + 1.0));
+    __syncthreads();
+    if (tid < PB) {
+      const bool le = cnt_s[tid] <= k - 1;
+      const bool nxt = (tid + 1 < PB) ? (cnt_s[tid + 1] <= k - 1) : false;
+      if (le && !nxt) {
+        s_lo_t = a0 + (b0 - a0) * (tid + 1) / (PB + 1.0);
+        if (tid + 1 < PB) s_hi_t = a0 + (b0 - a0) * (tid + 2) / (PB + 1.0);
+      }
+      if (tid == 0 && !le) s_hi_t = a0 + (b0 - a0) / (PB + 1.0);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const double tmax = 0.5 * (s_lo_t + s_hi_t);
+    int r = 0;
+    if (tmax > 0.0) r = k - sturm_count(d, e2, k, a.tol * tmax);
+    if (r > a.cap) r = a.cap;
+    if (r < 0) r = 0;
+    double* h = es.hdr();
+    h[0] = s_scale;
+    h[1] = s_lo;
+    h[2] = s_hi;
+    h[3] = tmax;
+    h[4] = (double)r;
+  }
+  for (int i = tid; i < k; i += ENT) {
+    es.d()[i] = d[i];
+    es.e()[i] = e[i];
+    es.e2()[i] = e2[i];
+    es.tau()[i] = tau[i];
+  }
+  double* R = es.refl();
+  for (int e_ = tid; e_ < k * ld; e_ += ENT) R[e_] = A[e_];
+}
+
+template <int FK>
+__global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
+  constexpr int RCH = (FK + 31) / 32;
+  constexpr int MAXE = (FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1;
+  extern __shared__ double R[];  // reflectors, k x ld
+  __shared__ double d[FK], e[FK], e2[FK], tau[FK];
+  __shared__ double lo_s[MAXE], hi_s[MAXE], lam_s[MAXE];
+  __shared__ int cnt_s[ENT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = a.k, ld = k | 1;
+  const EsLayout es{a.Es, SMALL_K_MAX};
+  const double* h = es.hdr();
+  const int r = (int)h[4];
+  const int nr = r < k ? r + 1 : r;
+  const int c0 = (int)((long long)blockIdx.x * nr / gridDim.x);
+  const int c1 = (int)((long long)(blockIdx.x + 1) * nr / gridDim.x);
+  const int nb = c1 - c0;
+  if (nb <= 0) return;
+  const double scale = h[0], glo = h[1], ghi = h[2];
+  for (int i = tid; i < k; i += ENT) {
+    d[i] = es.d()[i];
+    e[i] = es.e()[i];
+    e2[i] = es.e2()[i];
+    tau[i] = es.tau()[i];
+  }
+  for (int e_ = tid; e_ < k * ld; e_ += ENT) R[e_] = es.refl()[e_];
+  __syncthreads();
+
+  // ------------------------------------------------------------ multisection on this slice
+  {
+    int P = ENT / nb;
+    P = P < 1 ? 1 : (P > 64 ? 64 : P);
+    const int grp = tid / P, t = tid % P;
+    const bool act = grp < nb;
+    const int jj = k - 1 - (c0 + grp);  // ascending index
+    if (act && t == 0) {
+      lo_s[grp] = glo;
+      hi_s[grp] = ghi;
+    }
+    __syncthreads();
+    const double bits = log2((double)P + 1.0);
+    const int nit = (int)ceil(log2((ghi - glo) / 1e-13 + 1.0) / bits) + 1;
+    for (int it = 0; it < nit; ++it) {
+      if (act) {
+        const double a0 = lo_s[grp], b0 = hi_s[grp];
+        cnt_s[tid] = sturm_count(d, e2, k, a0 + (b0 - a0) * (t + 1) / (P + 1.0));
+      }
+      __syncthreads();
+      if (act) {
+        // transition between probe t and t+1 (counts are monotone in the probe position)
+        const double a0 = lo_s[grp], b0 = hi_s[grp];
+        const bool le = cnt_s[tid] <= jj;
+        const bool nxt = (t + 1 < P) ? (cnt_s[tid + 1] <= jj) : false;
+        if (le && !nxt) {
+          lo_s[grp] = a0 + (b0 - a0) * (t + 1) / (P + 1.0);
+          if (t + 1 < P) hi_s[grp] = a0 + (b0 - a0) * (t + 2) / (P + 1.0);
+        }
+        if (t == 0 && !le) hi_s[grp] = a0 + (b0 - a0) / (P + 1.0);
+      }
+      __syncthreads();
+    }
+    if (act && t == 0) {
+      lam_s[grp] = 0.5 * (lo_s[grp] + hi_s[grp]);
+      es.lam()[c0 + grp] = lam_s[grp];
+    }
+    __syncthreads();
+  }
+
+  // ------------------------------------------------------------ twisted-factorisation vectors
+  const int cv1 = c1 < r ? c1 : r;  // vectors only for kept eigenvalues
+  const int nv = cv1 - c0;
+  if (tid < 2 * nv) {
+    const unsigned msk = __activemask();
+    const int c = c0 + (tid >> 1), side = tid & 1;
+    const double lm = lam_s[tid >> 1];
+    double* Dp = es.dp() + (size_t)c * SMALL_K_MAX;
+    double* Dm = es.dm() + (size_t)c * SMALL_K_MAX;
+    const double pivmin = 1e-290;
+    if (side == 0) {
+      double x = d[0] - lm;
+      if (fabs(x) < pivmin) x = -pivmin;
+      Dp[0] = x;
+      for (int i = 1; i < k; ++i) {
+        x = (d[i] - lm) - e2[i - 1] / x;
+        if (fabs(x) < pivmin) x = -pivmin;
+        Dp[i] = x;
+      }
+    } else {
+      double x = d[k - 1] - lm;
+      if (fabs(x) < pivmin) x = -pivmin;
+      Dm[k - 1] = x;
+      for (int i = k - 2; i >= 0; --i) {
+        x = (d[i] - lm) - e2[i] / x;
+        if (fabs(x) < pivmin) x = -pivmin;
+        Dm[i] = x;
+      }
+    }
+    __syncwarp(msk);
+    __threadfence_block();
+    const int h0 = side ? k / 2 : 0, h1 = side ? k : k / 2;
+    int tw = h0;
+    double best = 1e300;
+    for (int i = h0; i < h1; ++i) {
+      const double g = Dp[i] + Dm[i] - (d[i] - lm);
+      if (fabs(g) < best) { best = fabs(g); tw = i; }
+    }
+    const double ob = __shfl_xor_sync(msk, best, 1);
+    const int ot = __shfl_xor_sync(msk, tw, 1);
+    if (ob < best || (ob == best && ot < tw)) { best = ob; tw = ot; }
+    double nrm2 = 0.0;
+    if (side == 0) {
+      for (int i = 0; i < tw; ++i) Dp[i] = -e[i] / Dp[i];
+      double zi = 1.0;
+      for (int i = tw - 1; i >= 0; --i) {
+        zi *= Dp[i];
+        nrm2 = fma(zi, zi, nrm2);
+        Dp[i] = zi;
+      }
+    } else {
+      for (int i = tw + 1; i < k; ++i) Dm[i] = -e[i - 1] / Dm[i];
+      double zi = 1.0;
+      for (int i = tw + 1; i < k; ++i) {
+        zi *= Dm[i];
+        nrm2 = fma(zi, zi, nrm2);
+        Dp[i] = zi;
+      }
+    }
+    nrm2 += __shfl_xor_sync(msk, nrm2, 1);
+    __syncwarp(msk);
+    __threadfence_block();
+    if (side == 0) Dp[tw] = 1.0;
+    __syncwarp(msk);
+    __threadfence_block();
+    const double inv = 1.0 / sqrt(1.0 + nrm2);
+    for (int i = side; i < k; i += 2) Dp[i] *= inv;
+  }
+  __syncthreads();
+
+  // ------------------------------------------------------------ W = Q Z, one warp per column
+  for (int cc = warp; cc < nv; cc += NW) {
+    const int c = c0 + cc;
+    const double* zsrc = es.dp() + (size_t)c * SMALL_K_MAX;
+    double z[RCH];
+#pragma unroll
+    for (int u = 0; u < RCH; ++u) {
+      const int i = lane + 32 * u;
+      z[u] = i < k ? zsrc[i] : 0.0;
+    }
+    for (int j = k - 3; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      double vr[RCH];
+      double sv = 0.0;
+#pragma unroll
+      for (int u = 0; u < RCH; ++u) {
+        const int i = lane + 32 * u;
+        vr[u] = (i == j + 1) ? 1.0 : ((i > j + 1 && i < k) ? R[j * ld + i] : 0.0);
+        sv = fma(vr[u], z[u], sv);
+      }
+      sv = warp_sum(sv) * tj;
+#pragma unroll
+      for (int u = 0; u < RCH; ++u) z[u] = fma(-sv, vr[u], z[u]);
+    }
+    const double f = a.sqrt_scale ? sqrt(fmax(lam_s[cc] * scale, 0.0)) : 1.0;
+#pragma unroll
+    for (int u = 0; u < RCH; ++u) {
+      const int i = lane + 32 * u;
+      if (i < k) a.Tm[i + (size_t)c * a.ldt] = z[u] * f;
+    }
+  }
+}
+
+template <int FK>
+__global__ void __launch_bounds__(ENT, 1) eig_fin_kernel(SmallArgs a) {
+  extern __shared__ double A[];  // W^T, r x ld
+  __shared__ double lam[FK + 1], slam[FK + 1];
+  __shared__ double red[NW];
+  __shared__ int s_bad;
+  __shared__ double Gam[SMALL_M_MAX * SMALL_M_MAX];
+  __shared__ double Phi[SMALL_M_MAX * SMALL_M_MAX];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = a.k, ld = k | 1;
+  const EsLayout es{a.Es, SMALL_K_MAX};
+  const double* h = es.hdr();
+  const double scale = h[0], tmax = h[3];
+  const int r = (int)h[4];
+  const int nr = r < k ? r + 1 : r;
+  for (int i = tid; i < nr; i += ENT) {
+    lam[i] = es.lam()[i];
+    slam[i] = sqrt(fabs(lam[i]));
+  }
+  __syncthreads();
+  for (int e_ = tid; e_ < k * r; e_ += ENT) {
+    const int i = e_ % k, c = e_ / k;
+    const double f = a.sqrt_scale ? sqrt(fmax(lam[c] * scale, 0.0)) : 1.0;
+    A[c * ld + i] = f > 0.0 ? a.Tm[i + (size_t)c * a.ldt] / f : 0.0;
+  }
+  __syncthreads();
+  constexpr int TB = 4;
+  const int nbk = (r + TB - 1) / TB;
+  double mx = 0.0;
+  for (int blk = tid; blk < nbk * nbk; blk += ENT) {
+    const int bi = blk % nbk, bj = blk / nbk;
+    if (bi > bj) continue;
+    double acc[TB][TB];
+#pragma unroll
+    for (int x = 0; x < TB; ++x)
+#pragma unroll
+      for (int y = 0; y < TB; ++y) acc[x][y] = 0.0;
+    for (int i = 0; i < k; ++i) {
+      double wa[TB], wb[TB];
+#pragma unroll
+      for (int x = 0; x < TB; ++x) {
+        const int c1 = bi * TB + x, c2 = bj * TB + x;
+        wa[x] = c1 < r ? A[c1 * ld + i] : 0.0;
+        wb[x] = c2 < r ? A[c2 * ld + i] : 0.0;
+      }
+#pragma unroll
+      for (int x = 0; x < TB; ++x)
+#pragma unroll
+        for (int y = 0; y < TB; ++y) acc[x][y] = fma(wa[x], wb[y], acc[x][y]);
+    }
+#pragma unroll
+    for (int x = 0; x < TB; ++x)
+#pragma unroll
+      for (int y = 0; y < TB; ++y) {
+        const int c1 = bi * TB + x, c2 = bj * TB + y;
+        if (c1 < r && c2 < r && c1 <= c2) {
+          const double w = (c1 == c2) ? 1.0 : slam[c1] * slam[c2] / fmax(fabs(lam[0]), 1e-300);
+          mx = fmax(mx, fabs(acc[x][y] - (c1 == c2 ? 1.0 : 0.0)) * w);
+        }
+      }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < NW; ++w) m = fmax(m, red[w]);
+    s_bad = !(m <= a.orth_tol);
+    if (a.stats) {
+      a.stats[0] = (double)r;
+      a.stats[1] = tmax * scale;
+      a.stats[2] = (r < k && tmax > 0.0) ? fabs(lam[r]) / tmax : 0.0;
+      a.stats[3] = s_bad ? 1.0 : 0.0;
+      a.stats[4] = m;
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) *a.r_out = -1;  // caller falls back to the Jacobi kernel
+    return;
+  }
+  if (a.t3 && r > 0) smallk::t3_fuse(a, k, r, A, Gam, Phi);
+  if (tid == 0) *a.r_out = r;
+}
+
+template <int FK>
+void launch_split(const SmallArgs& a, cudaStream_t st) {
+  const size_t floor_b = sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX;
+  const size_t need_max = sizeof(double) * (size_t)FK * (FK | 1);
+  size_t smem = sizeof(double) * (size_t)a.k * (a.k | 1);
+  if (smem < floor_b) smem = floor_b;
+  static bool attr = false;
+  if (!attr) {
+    const int mx = (int)(need_max > floor_b ? need_max : floor_b);
+    DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DME_CUDA(cudaFuncSetAttribute(eig_vec_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DME_CUDA(cudaFuncSetAttribute(eig_fin_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    attr = true;
+  }
+  eig_tri_kernel<FK><<<1, ENT, smem, st>>>(a);
+  DME_KCHECK();
+  eig_vec_kernel<FK><<<EIG_SPLIT_CTAS, ENT, smem, st>>>(a);
+  DME_KCHECK();
+  eig_fin_kernel<FK><<<1, ENT, smem, st>>>(a);
+  DME_KCHECK();
+}
+
+}  // namespace
+
+size_t eig_split_scratch_doubles() {
+  return EsLayout::HDR + 5 * SMALL_K_MAX + 8 + (size_t)SMALL_K_MAX * (SMALL_K_MAX | 1) +
+         2 * (size_t)SMALL_K_MAX * SMALL_K_MAX + 64;
+}
+
+void eig_split(const SmallArgs& a, cudaStream_t st) {
+  if (a.k > FAST_K_MAX || a.k < 3 || !a.Es) throw std::runtime_error("eig_split: k out of range");
+  if (a.k <= 96) launch_split<96>(a, st);
+  else launch_split<FAST_K_MAX>(a, st);
+}
+
+}  // namespace dme

@@ -6,7 +6,9 @@ namespace dme {
 
 constexpr int SMALL_K_MAX = 224;          // packed k(k+1)/2 doubles fit in 201 KB of shared memory
 constexpr int SMALL_M_MAX = 8;
-constexpr int FAST_K_MAX = 160;           // fast tridiagonal eigen-compression: k x (k|1) in smem            // columns of B handled by the fused Riccati flow
+constexpr int FAST_K_MAX = 160;           // fast tridiagonal eigen-compression: k x (k|1) in smem
+constexpr int EIG_SPLIT_MIN = 48;         // k from which the eigen-compression runs as TRI/VEC/FIN
+constexpr int EIG_SPLIT_CTAS = 8;         // CTAs of the VEC kernel (the look-ahead E pass leaves them)            // columns of B handled by the fused Riccati flow
 constexpr int SMALL_SMEM_MAX = SMALL_K_MAX * (SMALL_K_MAX + 1) / 2 * 8;
 
 struct SmallArgs {
@@ -29,10 +31,14 @@ struct SmallArgs {
   int64_t ldt = 0;
   int* r_out = nullptr;      // out: new rank (device)
   double* stats = nullptr;   // out: [rank, theta_max, largest dropped / theta_max, fallback, orth err]
+  double* Es = nullptr;      // split path: global scratch (eig_split_scratch_doubles())
+  int zsmem = 1;             // fast path: back-transformation columns in shared memory when they fit
   double orth_tol = 1e-12;   // fast path: max weighted |W^T W - I| before falling back to Jacobi
 };
 
 void compress_t3(const SmallArgs& a, cudaStream_t st);  // Jacobi (any k <= SMALL_K_MAX)
 void eig_fast(const SmallArgs& a, cudaStream_t st);     // k <= FAST_K_MAX; *r_out = -1 => fall back
+void eig_split(const SmallArgs& a, cudaStream_t st);    // 3 <= k <= FAST_K_MAX, same contract
+size_t eig_split_scratch_doubles();
 
 }  // namespace dme
