@@ -1,6 +1,7 @@
 // Element-wise / reduction / tall-times-small kernels of the DME path.
 #include "aux.h"
 #include "common.cuh"
+#include "gemm_nt.h"
 
 namespace dme {
 
@@ -153,6 +154,42 @@ __global__ void __launch_bounds__(256) tall_small_kernel(const double* A, int64_
       }
 }
 
+// lower triangle <- transpose of the upper triangle (average: symmetric part everywhere)
+__global__ void mirror_kernel(double* X, int64_t n, int64_t ld, int average) {
+  __shared__ double up[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;  // destination block (bi, bj), bi >= bj
+  if (bi < bj) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  // source block (bj, bi) of the upper triangle, transposed through shared memory
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = bj * 32 + y, c = bi * 32 + tx;
+    up[y][tx] = (r < n && c < n) ? X[r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = bi * 32 + y, c = bj * 32 + tx;  // element (r, c), r > c wanted
+    if (r < n && c < n && r > c) {
+      const double t = up[tx][y];  // X[c][r]
+      if (average) {
+        const double v = 0.5 * (X[r * ld + c] + t);
+        X[r * ld + c] = v;
+      } else {
+        X[r * ld + c] = t;
+      }
+    }
+  }
+}
+
+__global__ void mirror_upper_from_lower(double* X, int64_t n, int64_t ld) {
+  // after averaging the lower triangle, copy it back to the upper one
+  const int64_t total = n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    if (i < j) X[i * ld + j] = X[j * ld + i];
+  }
+}
+
 inline int grid_for(int64_t total, int threads = 256) {
   int64_t b = (total + threads - 1) / threads;
   const int64_t cap = (int64_t)num_sms() * 8;
@@ -160,6 +197,16 @@ inline int grid_for(int64_t total, int threads = 256) {
 }
 
 }  // namespace
+
+void mirror_lower(double* X, int64_t n, int64_t ld, bool average, cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
+  mirror_kernel<<<grid, dim3(32, 8), 0, st>>>(X, n, ld, average ? 1 : 0);
+  DME_KCHECK();
+  if (average) {
+    mirror_upper_from_lower<<<grid_for(n * n), 256, 0, st>>>(X, n, ld);
+    DME_KCHECK();
+  }
+}
 
 void transpose_scale(const double* A, int64_t n, int64_t lda, double alpha, double* out,
                      int64_t ldo, cudaStream_t st) {

@@ -125,6 +125,7 @@ struct dme_ctx {
   dme_stats stats{};
   bool poisoned = false;
   bool force_jacobi = false;
+  bool symA = false;  // A == A^T exactly (host check): symmetric Padé products
   bool fsal = true;
   ncclComm_t comm = nullptr;
   // profiling: (start, stop, class, flops, bytes) event records drained at sync points
@@ -163,6 +164,7 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   c->gs.max_tiles = 1 << 16;
   c->gs.partial = P.take<double>(GemmScratch::partial_doubles(c->gs.max_grid));
   c->gs.counters = P.take<int>((size_t)c->gs.max_tiles);
+  c->gs.tile_list = P.take<int2>((size_t)c->gs.max_tiles);
   c->gs2.max_grid = 256;
   c->gs2.max_tiles = 1 << 16;
   c->gs2.partial = P.take<double>(GemmScratch::partial_doubles(c->gs2.max_grid));
@@ -652,13 +654,18 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
 
 // ------------------------------------------------------------------ init: expm + quadrature
 void matmul_sq(dme_ctx* c, const double* X, const double* Y, double* out) {
-  // out = X * Y  (n x n row-major): B operand rows = columns of Y = rows of Y^T
-  transpose_rect(Y, c->n, c->n, c->ldn, c->BT, c->ldn, c->st);
+  // out = X * Y  (n x n row-major): B operand rows = columns of Y = rows of Y^T.
+  // Symmetric A: every factor here is a polynomial in the symmetric X0 (or E = r(X0)), so Y^T = Y
+  // and X Y is symmetric: only the upper tile triangle is computed, then mirrored.
+  const bool sym = c->symA;
+  if (!sym) transpose_rect(Y, c->n, c->n, c->ldn, c->BT, c->ldn, c->st);
   GemmNTArgs g;
-  g.A = X; g.lda = c->ldn; g.B = c->BT; g.ldb = c->ldn;
+  g.A = X; g.lda = c->ldn; g.B = sym ? Y : c->BT; g.ldb = c->ldn;
   g.M = c->n; g.N = c->n; g.K = c->n;
   g.out = out; g.out_rs = c->ldn; g.out_cs = 1;
+  g.sym_upper = sym;
   gemm_nt(g, c->gs, c->st);
+  if (sym) mirror_lower(out, c->n, c->ldn, false, c->st);
 }
 
 // L_I(2w) = compress([L_I(w), E_w L_I(w)])  (exact doubling of the composite rule, reading G6)
@@ -774,6 +781,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   lincomb(c->X4, n, ld, {1.0, c->V}, {-1.0, c->U}, {}, {}, 0.0, st);  // Q = V - U
   lincomb(c->X6, n, ld, {1.0, c->V}, {1.0, c->U}, {}, {}, 0.0, st);   // P = V + U
   lu_nopiv_solve_right(c->X4, c->X6, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 1);
+  if (c->symA) mirror_lower(c->X6, n, ld, true, st);  // exact symmetry of E_delta
   double minpiv = 0;
   DME_CUDA(cudaMemcpyAsync(&minpiv, c->norm_dev + 1, 8, cudaMemcpyDeviceToHost, st));
   sync(c);
@@ -871,6 +879,13 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     c = cp.get();
     fill_dims(c, pr, o);
     c->dre = dre;
+    {
+      bool sym = true;
+      for (int64_t i = 0; i < pr->n && sym; ++i)
+        for (int64_t j = i + 1; j < pr->n; ++j)
+          if (pr->A[i * pr->n + j] != pr->A[j * pr->n + i]) { sym = false; break; }
+      c->symA = sym;
+    }
     if (dre) c->lrinv_host = chol_inverse_lower(pr->R, (int)pr->m);
     if (pr->r0 > 0 && pr->D0) check_psd_host(pr->D0, pr->r0);
     DME_CUDA(cudaSetDevice(o->device));

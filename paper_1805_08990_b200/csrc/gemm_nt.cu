@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <vector>
 #include <mutex>
 
 namespace dme {
@@ -42,6 +43,8 @@ struct Params {
   double* partial;
   int* counters;
   int b_nloc;  // >0: B tensor map is 3-D {nloc, N, G}; k -> (k % nloc, k / nloc)
+  const int2* tile_list;  // non-null: tile t -> (tm, tn) = tile_list[t] (symmetric output: upper tiles)
+  int ntiles;             // number of output tiles (list length, or tiles_m * tiles_n)
   int slices;  // >0: split-K slice mode (few tiles, long K): CTA b = (tile b % T, slice b / T),
                //     partials reduced by splitk_reduce_kernel; 0: Stream-K with last-arriver fixup
 };
@@ -52,6 +55,17 @@ __device__ __forceinline__ long long iter_begin(long long c, const Params& p) {
 __device__ __forceinline__ int cta_of(long long i, const Params& p) {
   // largest c with iter_begin(c) <= i
   return (int)(((i + 1) * p.grid + p.total - 1) / p.total - 1);
+}
+
+__device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, int& tn) {
+  if (p.tile_list) {
+    const int2 c = p.tile_list[tile];
+    tm = c.x;
+    tn = c.y;
+  } else {
+    tm = tile % p.tiles_m;
+    tn = tile / p.tiles_m;
+  }
 }
 
 template <int BN>
@@ -83,7 +97,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = tid >> 5, lane = tid & 31;
   long long beg, end;
   if (p.slices > 0) {
-    const int T = p.tiles_m * p.tiles_n;
+    const int T = p.ntiles;
     const long long tile = blockIdx.x % T, sl = blockIdx.x / T;
     beg = tile * p.kiters + sl * p.kiters / p.slices;
     end = tile * p.kiters + (sl + 1) * p.kiters / p.slices;
@@ -110,7 +124,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       for (long long it = beg; it < end; ++it) {
         const int tile = (int)(it / p.kiters), kk = (int)(it % p.kiters);
-        const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+        int tm, tn;
+        tile_coords(p, tile, tm, tn);
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
         tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kk * BK, tm * BM);
@@ -173,7 +188,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
 
     // -------------------------------------------------------------- epilogue
-    const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+    int tm, tn;
+    tile_coords(p, tile, tm, tn);
     bool do_store = true;
     if (p.slices > 0) {
       // slice mode: publish the partial (fragment order); splitk_reduce_kernel sums in slice order
@@ -235,7 +251,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 template <int BN, int WM, int WN>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const Params p) {
   constexpr int MT = BM / WM / 8, NTW = BN / WN / 8, ACC = MT * NTW * 2;
-  const int T = p.tiles_m * p.tiles_n;
+  const int T = p.ntiles;
   const long long total = (long long)T * ACC * NUM_CONSUMERS;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -248,7 +264,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const Params p) {
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int wm = warp % WM, wn = warp / WM;
     const int el = i & 1, mn = i >> 1, mi = mn / NTW, ni = mn % NTW;
-    const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+    int tm, tn;
+    tile_coords(p, tile, tm, tn);
     const long long row = (long long)tm * BM + wm * (BM / WM) + mi * 8 + frag_perm(g);
     const long long col = (long long)tn * BN + wn * (BN / WN) + ni * 8 + frag_perm(t * 2 + el);
     if (row < p.M && col < p.N) {
@@ -284,7 +301,7 @@ void launch(const GemmNTArgs& a, const Params& p0, GemmScratch& ws, cudaStream_t
   DME_KCHECK();
   if (p.slices > 0) {
     constexpr int ACC = (BM / WM / 8) * (BN / WN / 8) * 2;
-    const long long total = (long long)p.tiles_m * p.tiles_n * ACC * NUM_CONSUMERS;
+    const long long total = (long long)p.ntiles * ACC * NUM_CONSUMERS;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 4 * num_sms());
     splitk_reduce_kernel<BN, WM, WN><<<blocks, 256, 0, st>>>(p);
     DME_KCHECK();
@@ -312,9 +329,23 @@ void gemm_nt(const GemmNTArgs& a, GemmScratch& ws, cudaStream_t st) {
          : a.N <= 48 ? 48 : a.N <= 56 ? 56 : 64;
   p.tiles_m = (int)ceil_div(a.M, BM);
   p.tiles_n = (int)ceil_div(a.N, BN);
-  p.total = (long long)p.tiles_m * p.tiles_n * p.kiters;
+  long long tiles = (long long)p.tiles_m * p.tiles_n;
+  p.tile_list = nullptr;
+  if (a.sym_upper) {
+    // only tiles touching the upper triangle (row <= col); the caller mirrors the lower triangle
+    std::vector<int2> lst;
+    for (int tn = 0; tn < p.tiles_n; ++tn)
+      for (int tm = 0; tm < p.tiles_m; ++tm)
+        if ((long long)tm * BM <= (long long)tn * BN + BN - 1) lst.push_back(make_int2(tm, tn));
+    if ((long long)lst.size() > ws.max_tiles) throw std::runtime_error("gemm_nt: tile list too long");
+    DME_CUDA(cudaMemcpyAsync(ws.tile_list, lst.data(), lst.size() * sizeof(int2),
+                             cudaMemcpyHostToDevice, st));
+    p.tile_list = ws.tile_list;
+    tiles = (long long)lst.size();
+  }
+  p.total = tiles * p.kiters;
+  p.ntiles = (int)tiles;
   const int sms = std::min<int>(num_sms(), ws.max_grid);
-  const long long tiles = (long long)p.tiles_m * p.tiles_n;
   p.slices = 0;
   if (tiles * 4 <= sms && p.kiters >= 16) {
     // few output tiles over a long K (Gram matrices Zc^T Zc): parallel split-K reduction
