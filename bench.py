@@ -161,11 +161,16 @@ def run_ours(args):
     kw = dict(h=H, rank_cap=RANK_CAP, world_size=world, world_rank=rank, nccl_uid=uid)
 
     # ------------------------------------------------------------ device-resident timed region
+    # A (800 MB) resident in HBM before the clock starts (options.big_inputs_on_device); the init
+    # (validation, Padé expm, quadrature ladder, P0 compression) is timed as part of time-to-T.
+    A_dev = torch.from_numpy(prob.A).cuda()
+    kw_dev = dict(dme.problem_kwargs(prob), A=A_dev)
     torch.cuda.synchronize()
     t_init0 = time.perf_counter()
-    s = dme.Solver(**dme.problem_kwargs(prob), **kw)
+    s = dme.Solver(**kw_dev, **kw)
     torch.cuda.synchronize()
     init_wall = time.perf_counter() - t_init0
+    del A_dev, kw_dev
     s.split_step("strang", "F12F3", args.warmup)
     torch.cuda.synchronize()
     s.set_profiling(True)
@@ -226,8 +231,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        # host inputs in pinned memory (the caller's buffers), H2D inside the timed region
+        A_pin = torch.empty(prob.A.shape, dtype=torch.float64, pin_memory=True)
+        A_pin.copy_(torch.from_numpy(prob.A))
+        kw_host = dict(dme.problem_kwargs(prob), A=A_pin.numpy())
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        s2 = dme.Solver(**dme.problem_kwargs(prob), **kw)          # H2D of A, C, B, R, L0
+        s2 = dme.Solver(**kw_host, **kw)                            # H2D of A, C, B, R, L0
         s2.split_step("strang", "F12F3", NT)
         L, D = s2.get_factor()                                      # D2H of the factor
         torch.cuda.synchronize()
@@ -261,8 +271,9 @@ def run_ours(args):
                            "n": prob.n, "rank_after_timed_steps": rank_now,
                            "l2": "inputs larger than L2 (E_{h/2} = 800 MB streamed per pass)",
                            "parallelism": f"rows of E sharded over {world} GPU(s)"},
-                "time_to_T_s": init_dev + NT * ms_step * 1e-3,
-                "init_s": init_dev, "init_wall_s": init_wall,
+                "time_to_T_s": init_wall + NT * ms_step * 1e-3,
+                "time_to_T_what": "init from HBM-resident A (wall, synchronised) + 100 x ms_per_step",
+                "init_s": init_wall, "init_lib_s": init_dev,
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -100,6 +100,9 @@ typedef struct {
   const void* nccl_uid;   /* 128-byte ncclUniqueId from dme_get_unique_id on rank 0           */
   void* workspace;        /* device buffer, >= dme_workspace_size bytes, 256-byte aligned     */
   size_t workspace_bytes;
+  int32_t big_inputs_on_device; /* 1: prob->A and prob->S are DEVICE pointers (same row-major
+                             layout, copied device-to-device at init); every other input stays
+                             a host pointer. 0 (default): all inputs are host pointers          */
   int32_t no_fsal;        /* 0 (default): within one dme_split_step call, merge the trailing
                              T1/T12(h/2) of a Strang step with the leading one of the next step
                              (first-same-as-last); 1: apply every sub-step as written           */

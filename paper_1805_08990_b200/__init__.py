@@ -47,7 +47,7 @@ class _Options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("world_size", ctypes.c_int32),
                 ("world_rank", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("no_fsal", ctypes.c_int32)]
+                ("big_inputs_on_device", ctypes.c_int32), ("no_fsal", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -158,12 +158,26 @@ class Solver:
         self._torch = torch
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.device = dev
-        self._keep = [_f64(A), _f64(C), _f64(B), _f64(R), _f64(S), _f64(L0), _f64(D0)]
-        A_, C_, B_, R_, S_, L0_, D0_ = self._keep
+        # A and S may be CUDA tensors (float64, contiguous): then they are read device-to-device
+        on_dev = isinstance(A, torch.Tensor) and A.is_cuda
+        if on_dev:
+            if A.dtype != torch.float64 or not A.is_contiguous():
+                raise ValueError("device A must be a contiguous float64 CUDA tensor")
+            if S is not None and not (isinstance(S, torch.Tensor) and S.is_cuda and
+                                      S.dtype == torch.float64 and S.is_contiguous()):
+                raise ValueError("with a device A, S must be a contiguous float64 CUDA tensor")
+            dptr = lambda t: None if t is None else ctypes.cast(t.data_ptr(), _dp)
+            self._keep = [A, _f64(C), _f64(B), _f64(R), S, _f64(L0), _f64(D0)]
+            A_, C_, B_, R_, S_, L0_, D0_ = self._keep
+            pA, pS = dptr(A_), dptr(S_)
+        else:
+            self._keep = [_f64(A), _f64(C), _f64(B), _f64(R), _f64(S), _f64(L0), _f64(D0)]
+            A_, C_, B_, R_, S_, L0_, D0_ = self._keep
+            pA, pS = _ptr(A_), _ptr(S_)
         n = A_.shape[0]
         self.n = n
-        pr = _Problem(n=n, A=_ptr(A_), p=0 if C_ is None else C_.shape[0], C=_ptr(C_),
-                      m=0 if B_ is None else B_.shape[1], B=_ptr(B_), R=_ptr(R_), S=_ptr(S_),
+        pr = _Problem(n=n, A=pA, p=0 if C_ is None else C_.shape[0], C=_ptr(C_),
+                      m=0 if B_ is None else B_.shape[1], B=_ptr(B_), R=_ptr(R_), S=pS,
                       r0=0 if L0_ is None else L0_.shape[1], L0=_ptr(L0_), D0=_ptr(D0_))
         self._pr = pr
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
@@ -173,7 +187,8 @@ class Solver:
                        quad_subpanels=quad_subpanels, device=dev.index,
                        stream=self.stream.cuda_stream, world_size=world_size,
                        world_rank=world_rank, nccl_uid=ctypes.cast(uid, ctypes.c_void_p) if uid else None,
-                       workspace=None, workspace_bytes=0, no_fsal=0 if fsal else 1)
+                       workspace=None, workspace_bytes=0, big_inputs_on_device=1 if on_dev else 0,
+                       no_fsal=0 if fsal else 1)
         nbytes = ctypes.c_size_t(0)
         _check(_lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(opt), ctypes.byref(nbytes)),
                "dme_workspace_size")

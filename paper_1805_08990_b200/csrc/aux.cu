@@ -190,6 +190,42 @@ __global__ void mirror_upper_from_lower(double* X, int64_t n, int64_t ld) {
   }
 }
 
+// flags[0] |= any non-finite entry; flags[1] |= any X[i][j] != X[j][i] (bitwise, i < j)
+__global__ void check_square_kernel(const double* __restrict__ X, int64_t n, int64_t ld, int* flags) {
+  __shared__ double up[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  int bad = 0, asym = 0;
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = bi * 32 + y, c = bj * 32 + tx;
+    if (r < n && c < n) {
+      const double v = X[r * ld + c];
+      bad |= !isfinite(v);
+    }
+    // transposed block for the symmetry test
+    const int64_t r2 = bj * 32 + y, c2 = bi * 32 + tx;
+    up[y][tx] = (r2 < n && c2 < n) ? X[r2 * ld + c2] : 0.0;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = bi * 32 + y, c = bj * 32 + tx;
+    if (r < n && c < n && r > c) {
+      const double v = X[r * ld + c], t = up[tx][y];
+      asym |= (__double_as_longlong(v) != __double_as_longlong(t));
+    }
+  }
+  bad = __syncthreads_or(bad);
+  asym = __syncthreads_or(asym);
+  if (tx == 0 && ty == 0) {
+    if (bad) atomicOr(flags, 1);
+    if (asym) atomicOr(flags + 1, 1);
+  }
+}
+
+__global__ void zero_ints(int* p, int cnt) {
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) p[i] = 0;
+}
+
 inline int grid_for(int64_t total, int threads = 256) {
   int64_t b = (total + threads - 1) / threads;
   const int64_t cap = (int64_t)num_sms() * 8;
@@ -197,6 +233,14 @@ inline int grid_for(int64_t total, int threads = 256) {
 }
 
 }  // namespace
+
+void check_square(const double* X, int64_t n, int64_t ld, int* flags2, cudaStream_t st) {
+  zero_ints<<<1, 32, 0, st>>>(flags2, 2);
+  DME_KCHECK();
+  dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
+  check_square_kernel<<<grid, dim3(32, 8), 0, st>>>(X, n, ld, flags2);
+  DME_KCHECK();
+}
 
 void mirror_lower(double* X, int64_t n, int64_t ld, bool average, cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));

@@ -15,6 +15,8 @@ void transpose_scale(const double* A, int64_t n, int64_t lda, double alpha, doub
 // *out = max_i sum_j |A_ij|  (= ||A^T||_1); scratch >= 1024 doubles
 void rowabs_max(const double* A, int64_t n, int64_t lda, double* scratch, double* out,
                 cudaStream_t st);
+// flags2[0] = 1 if X (n x n, row-major ld) has a non-finite entry, flags2[1] = 1 if X != X^T
+void check_square(const double* X, int64_t n, int64_t ld, int* flags2, cudaStream_t st);
 // out = sum_i c_i X_i + diag * I   (n x n, shared leading dim)
 void lincomb(double* out, int64_t n, int64_t ld, LinTerm t0, LinTerm t1, LinTerm t2, LinTerm t3,
              double diag, cudaStream_t st);

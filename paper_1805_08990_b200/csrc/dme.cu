@@ -133,6 +133,14 @@ struct dme_ctx {
   struct Rec { cudaEvent_t a, b; int cls; double flops, bytes; };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
+  ~dme_ctx() {
+    for (auto& r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : pool) cudaEventDestroy(e);
+    if (comm) ncclCommDestroy(comm);
+    if (st2) cudaStreamDestroy(st2);
+    if (ev_gram) cudaEventDestroy(ev_gram);
+    if (ev_ahead) cudaEventDestroy(ev_ahead);
+  }
 };
 
 namespace {
@@ -244,9 +252,8 @@ void validate(const dme_problem* pr, const dme_options* o, bool dre) {
   DME_REQUIRE(o->world_size <= 1 || o->nccl_uid, DME_ERR_INVALID, "nccl_uid required for world_size > 1");
   // input finiteness (host scan; inputs are host arrays)
   const size_t nn = (size_t)pr->n * pr->n;
-  DME_REQUIRE(all_finite(pr->A, nn), DME_ERR_INVALID, "A has non-finite entries");
+  (void)nn;  // A and S (n x n) are checked on the device after the upload (init_all)
   if (pr->p) DME_REQUIRE(all_finite(pr->C, (size_t)pr->p * pr->n), DME_ERR_INVALID, "C non-finite");
-  if (pr->S) DME_REQUIRE(all_finite(pr->S, nn), DME_ERR_INVALID, "S non-finite");
   if (pr->r0) DME_REQUIRE(all_finite(pr->L0, (size_t)pr->n * pr->r0), DME_ERR_INVALID, "L0 non-finite");
   if (pr->m) {
     DME_REQUIRE(all_finite(pr->B, (size_t)pr->n * pr->m) && all_finite(pr->R, (size_t)pr->m * pr->m),
@@ -684,9 +691,24 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   DME_CUDA(cudaMemsetAsync(c->gs.counters, 0, sizeof(int) * c->gs.max_tiles, st));
   DME_CUDA(cudaMemsetAsync(c->gs2.counters, 0, sizeof(int) * c->gs2.max_tiles, st));
   // ---------------------------------------------------------------- upload (H2D boundary)
-  DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, cudaMemcpyHostToDevice, st));
+  // A and S: host memory (pageable or pinned) or, with options.big_inputs_on_device, device memory
+  const cudaMemcpyKind kbig = c->opt.big_inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, kbig, st));
   if (c->has_S)
-    DME_CUDA(cudaMemcpy2DAsync(c->S, ld * 8, pr->S, n * 8, n * 8, n, cudaMemcpyHostToDevice, st));
+    DME_CUDA(cudaMemcpy2DAsync(c->S, ld * 8, pr->S, n * 8, n * 8, n, kbig, st));
+  // device-side validation of the big inputs: finiteness, and the exact symmetry of A that
+  // enables the symmetric Padé products
+  {
+    int flags_host[4] = {0, 0, 0, 0};
+    DME_CUDA(cudaMemsetAsync(c->r_dev, 0, 4 * sizeof(int), st));
+    check_square(c->Aup, n, ld, c->r_dev, st);           // r_dev[0]: non-finite, r_dev[1]: asymmetric
+    if (c->has_S) check_square(c->S, n, ld, c->r_dev + 2, st);
+    DME_CUDA(cudaMemcpyAsync(flags_host, c->r_dev, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    sync(c);
+    DME_REQUIRE(flags_host[0] == 0, DME_ERR_INVALID, "A has non-finite entries");
+    DME_REQUIRE(flags_host[2] == 0, DME_ERR_INVALID, "S has non-finite entries");
+    c->symA = flags_host[1] == 0;
+  }
   if (c->p > 0)  // C (p x n row-major): row i of C = column i of L_Q = C^T
     DME_CUDA(cudaMemcpy2DAsync(c->LQ, ld * 8, pr->C, n * 8, n * 8, c->p, cudaMemcpyHostToDevice, st));
   if (c->m > 0) {
@@ -879,13 +901,7 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     c = cp.get();
     fill_dims(c, pr, o);
     c->dre = dre;
-    {
-      bool sym = true;
-      for (int64_t i = 0; i < pr->n && sym; ++i)
-        for (int64_t j = i + 1; j < pr->n; ++j)
-          if (pr->A[i * pr->n + j] != pr->A[j * pr->n + i]) { sym = false; break; }
-      c->symA = sym;
-    }
+
     if (dre) c->lrinv_host = chol_inverse_lower(pr->R, (int)pr->m);
     if (pr->r0 > 0 && pr->D0) check_psd_host(pr->D0, pr->r0);
     DME_CUDA(cudaSetDevice(o->device));
@@ -1094,14 +1110,7 @@ dme_status dme_set_profiling(dme_ctx* c, int32_t on) {
 }
 
 dme_status dme_destroy(dme_ctx* c) {
-  if (!c) return DME_OK;
-  for (auto& r : c->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
-  for (auto e : c->pool) cudaEventDestroy(e);
-  if (c->comm) ncclCommDestroy(c->comm);
-  if (c->st2) cudaStreamDestroy(c->st2);
-  if (c->ev_gram) cudaEventDestroy(c->ev_gram);
-  if (c->ev_ahead) cudaEventDestroy(c->ev_ahead);
-  delete c;
+  delete c;  // ~dme_ctx releases streams, events and the NCCL communicator
   return DME_OK;
 }
 

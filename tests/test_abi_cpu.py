@@ -53,25 +53,28 @@ def test_workspace_size_host_only():
 
 
 def test_init_rejects_bad_input_without_device():
-    # validation happens before any CUDA call: a NaN in A or a bad h is rejected on the host
+    # host-side validation happens before any CUDA call (A and S, the n x n inputs, are checked for
+    # finiteness on the device after the upload: see tests/test_gpu_edge.py::test_errors)
     import numpy as np
     import paper_1805_08990_b200 as dme
     n = 8
     A = np.eye(n)
-    A[0, 0] = np.nan
     pr = dme._Problem(n=n, A=A.ctypes.data_as(dme._dp), p=0, C=None, m=0, B=None, R=None, S=None,
                       r0=0, L0=None, D0=None)
     o = dme._Options()
     dme._lib.dme_default_options(ctypes.byref(o))
     ctx = ctypes.c_void_p()
-    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
-    A[0, 0] = 1.0
     o.h = -1.0
     assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
     o.h = 0.01
+    C = np.full((1, n), np.nan)
+    pr.p, pr.C = 1, C.ctypes.data_as(dme._dp)
+    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+    pr.p, pr.C = 0, None
     R = np.array([[-1.0]])
     B = np.ones((n, 1))
     pr.m, pr.B, pr.R = 1, B.ctypes.data_as(dme._dp), R.ctypes.data_as(dme._dp)
     assert dme._lib.dme_dre_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
     assert b"positive definite" in dme._lib.dme_last_error()
     assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+    assert dme._lib.dme_split_step(None, 0, 0, 1) == 1

@@ -86,6 +86,13 @@ def test_errors(dme):
     # the context stays usable after validation errors
     s.split_step("strang", "F12", 2)
     assert s.get_factor()[0].shape[1] > 0
+    # non-finite A (checked on the device after the upload) and asymmetric/finite S
+    badA = make_config(2, nx=6)
+    badA.A = badA.A.copy()
+    badA.A[3, 4] = np.nan
+    with pytest.raises(dme.DmeError) as ei:
+        dme.Solver(**dme.problem_kwargs(badA), h=0.01)
+    assert ei.value.code == 1
     # indefinite D0 is rejected at init
     bad = make_config(2, nx=6)
     bad.D0 = np.diag([1.0, -1.0, 1.0, 1.0, 1.0])
@@ -104,3 +111,19 @@ def test_determinism(dme):
         out.append(s.get_factor()[0])
         s.close()
     assert np.array_equal(out[0], out[1])
+
+
+def test_device_resident_inputs(dme):
+    """A (and S) passed as CUDA tensors (options.big_inputs_on_device) give the same result."""
+    import torch
+    prob = make_config(4, nx=10)
+    a = dme.Solver(**dme.problem_kwargs(prob), h=0.02)
+    kw = dme.problem_kwargs(prob)
+    kw["A"] = torch.from_numpy(prob.A).cuda()
+    kw["S"] = torch.from_numpy(prob.S).cuda()
+    b = dme.Solver(**kw, h=0.02)
+    for s in (a, b):
+        s.split_step("strang", "F12F3F4", 5)
+    La, Da = a.get_factor()
+    Lb, Db = b.get_factor()
+    assert np.array_equal(La, Lb)
