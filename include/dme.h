@@ -106,7 +106,16 @@ typedef struct {
   int32_t no_fsal;        /* 0 (default): within one dme_split_step call, merge the trailing
                              T1/T12(h/2) of a Strang step with the leading one of the next step
                              (first-same-as-last); 1: apply every sub-step as written           */
+  int32_t e_pass;         /* kernel of the E_{h/2} L / E_h L passes (dme_e_pass):
+                             DME_EPASS_AUTO (default): int8 tensor cores with exact digit
+                             slicing (Ozaki scheme, 8 x 7-bit digits per operand, int32 exact
+                             accumulation, FP64 assembly; error per entry <= ~2^-54
+                             max_l|E_il| sum_l|L_lj|) when n <= 32768 and the
+                             pass has <= 64 columns, else FP64 DMMA;
+                             DME_EPASS_DMMA: always FP64 DMMA (mma.sync m8n8k4 f64)             */
 } dme_options;
+
+typedef enum { DME_EPASS_AUTO = 0, DME_EPASS_DMMA = 1 } dme_e_pass;
 
 typedef struct {
   double t;                 /* integrated time (steps * h)                                     */
@@ -133,6 +142,7 @@ typedef struct {
   double prof_apply_seconds;/* Zc * Tm                                                         */
   int64_t eig_fallbacks;    /* fast eigen-compressions that failed the orthogonality check and
                                were redone by the Jacobi kernel                                 */
+  int64_t ozaki_passes;     /* E passes run on the int8 tensor cores (options.e_pass)          */
 } dme_stats;
 
 void dme_default_options(dme_options* opt);
@@ -186,6 +196,9 @@ dme_status dme_debug_small_stats(dme_ctx* ctx, double* out16);
 /* C (M x N) = A (M x K) * B (K x N) through the library's DMMA GEMM (host buffers). */
 dme_status dme_debug_matmul(int64_t M, int64_t N, int64_t K, const double* A, const double* B,
                             double* C);
+/* The same product through the int8 digit-slicing kernel of the E pass (N <= 64, K <= 32768). */
+dme_status dme_debug_matmul_ozaki(int64_t M, int64_t N, int64_t K, const double* A, const double* B,
+                                  double* C);
 
 #ifdef __cplusplus
 }

@@ -47,7 +47,8 @@ class _Options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("world_size", ctypes.c_int32),
                 ("world_rank", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("big_inputs_on_device", ctypes.c_int32), ("no_fsal", ctypes.c_int32)]
+                ("big_inputs_on_device", ctypes.c_int32), ("no_fsal", ctypes.c_int32),
+                ("e_pass", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -61,7 +62,8 @@ class _Stats(ctypes.Structure):
                 ("prof_passes", ctypes.c_int64), ("prof_epass_seconds", ctypes.c_double),
                 ("prof_epass_flops", ctypes.c_double), ("prof_epass_bytes", ctypes.c_double),
                 ("prof_gram_seconds", ctypes.c_double), ("prof_small_seconds", ctypes.c_double),
-                ("prof_apply_seconds", ctypes.c_double), ("eig_fallbacks", ctypes.c_int64)]
+                ("prof_apply_seconds", ctypes.c_double), ("eig_fallbacks", ctypes.c_int64),
+                ("ozaki_passes", ctypes.c_int64)]
 
 
 _ctx_p = ctypes.c_void_p
@@ -87,6 +89,7 @@ for _name, _args in {
     "dme_debug_get_integral": [_ctx_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), _dp,
                                ctypes.c_int64],
     "dme_debug_matmul": [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp],
+    "dme_debug_matmul_ozaki": [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp],
     "dme_debug_small_stats": [_ctx_p, _dp],
 }.items():
     getattr(_lib, _name).argtypes = _args
@@ -96,7 +99,7 @@ EXPORTED = ["dme_default_options", "dme_status_string", "dme_last_error", "dme_w
             "dme_get_unique_id", "dme_shard_rows", "dme_dle_init", "dme_dre_init", "dme_split_step",
             "dme_get_factor", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
             "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_get_integral",
-            "dme_debug_small_stats", "dme_debug_matmul"]
+            "dme_debug_small_stats", "dme_debug_matmul", "dme_debug_matmul_ozaki"]
 
 
 class DmeError(RuntimeError):
@@ -146,12 +149,16 @@ def unique_id() -> bytes:
     return buf.raw
 
 
+E_PASS = {"auto": 0, "dmma": 1}
+
+
 class Solver:
     """One problem on one GPU (or one rank of a row-sharded multi-GPU run)."""
 
     def __init__(self, A, C=None, L0=None, D0=None, B=None, R=None, S=None, *, h, trunc_tol=1e-16,
                  rank_cap=0, quad_nodes=14, quad_subpanels=1, device=None, stream=None,
-                 world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None, fsal=True):
+                 world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None, fsal=True,
+                 e_pass="auto"):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1805_08990_b200.Solver needs a CUDA device (no CPU fallback)")
@@ -188,7 +195,7 @@ class Solver:
                        stream=self.stream.cuda_stream, world_size=world_size,
                        world_rank=world_rank, nccl_uid=ctypes.cast(uid, ctypes.c_void_p) if uid else None,
                        workspace=None, workspace_bytes=0, big_inputs_on_device=1 if on_dev else 0,
-                       no_fsal=0 if fsal else 1)
+                       no_fsal=0 if fsal else 1, e_pass=E_PASS[e_pass])
         nbytes = ctypes.c_size_t(0)
         _check(_lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(opt), ctypes.byref(nbytes)),
                "dme_workspace_size")
@@ -260,6 +267,15 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def matmul_ozaki(A, B):
+    """C = A @ B through the int8 digit-slicing (Ozaki) kernel of the E pass (B.shape[1] <= 64)."""
+    A, B = _f64(A), _f64(B)
+    C = np.zeros((A.shape[0], B.shape[1]))
+    _check(_lib.dme_debug_matmul_ozaki(A.shape[0], B.shape[1], A.shape[1], _ptr(A), _ptr(B),
+                                       _ptr(C)), "dme_debug_matmul_ozaki")
+    return C
 
 
 def matmul(A, B):

@@ -106,5 +106,8 @@ CUtensorMap make_tmap_2d(const double* base, uint64_t inner, uint64_t outer,
 CUtensorMap make_tmap_3d(const double* base, uint64_t d0, uint64_t d1, uint64_t d2,
                          uint64_t s1_elems, uint64_t s2_elems, uint32_t b0, uint32_t b1,
                          uint32_t b2, bool swizzle128);
+// 3D byte tensor (int8 digit slices), 128B swizzle; strides in bytes
+CUtensorMap make_tmap_3d_u8(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
+                            uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
 
 }  // namespace dme

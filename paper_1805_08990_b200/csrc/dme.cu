@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -14,6 +15,7 @@
 #include "dme.h"
 #include "gemm_nt.h"
 #include "lu.h"
+#include "ozaki.h"
 #include "small.h"
 
 using namespace dme;
@@ -111,6 +113,14 @@ struct dme_ctx {
   double *LA = nullptr;  // look-ahead operand [E_h L_I(h) | E_h Y]  (ldn x KMAX)
   int* r_dev = nullptr;
   GemmScratch gs, gs2;   // scratch of the main stream and of the look-ahead stream
+  // int8 digit slices for the Ozaki E pass (ozaki.h): rows of E_{h/2} / E_h (local shard, sliced
+  // once at init) and the columns of the pass operand (one buffer per stream)
+  bool oz = false, oz_ready = false;
+  int64_t ozld = 0;
+  int8_t *ozEh = nullptr, *ozEf = nullptr, *ozY = nullptr, *ozY2 = nullptr;
+  int *exEh = nullptr, *exEf = nullptr, *exY = nullptr, *exY2 = nullptr;
+  double *ozpm = nullptr, *ozpm2 = nullptr;  // slicing scratch (row maxima per chunk)
+  OzScratch ozs, ozs2;
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_gram = nullptr, ev_ahead = nullptr;
   bool lookahead = true;
@@ -133,6 +143,7 @@ struct dme_ctx {
   struct Rec { cudaEvent_t a, b; int cls; double flops, bytes; };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
+  cudaEvent_t tl_base = nullptr;  // timeline reference (DME_TIMELINE)
   ~dme_ctx() {
     for (auto& r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : pool) cudaEventDestroy(e);
@@ -140,6 +151,7 @@ struct dme_ctx {
     if (st2) cudaStreamDestroy(st2);
     if (ev_gram) cudaEventDestroy(ev_gram);
     if (ev_ahead) cudaEventDestroy(ev_ahead);
+    if (tl_base) cudaEventDestroy(tl_base);
   }
 };
 
@@ -178,6 +190,27 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   c->gs2.partial = P.take<double>(GemmScratch::partial_doubles(c->gs2.max_grid));
   c->gs2.counters = P.take<int>((size_t)c->gs2.max_tiles);
   c->LA = P.take<double>(fk);
+  if (c->oz) {
+    c->ozld = oz_ldk(n);
+    const int64_t rl = std::max<int64_t>(c->rows_loc, 1);
+    const size_t es = (size_t)OZ_S * rl * c->ozld, ys = (size_t)OZ_S * OZ_NMAX * c->ozld;
+    c->ozEh = P.take<int8_t>(es);
+    c->ozEf = P.take<int8_t>(es);
+    c->ozY = P.take<int8_t>(ys);
+    c->ozY2 = P.take<int8_t>(ys);
+    c->exEh = P.take<int>(rl);
+    c->exEf = P.take<int>(rl);
+    c->exY = P.take<int>(OZ_NMAX);
+    c->exY2 = P.take<int>(OZ_NMAX);
+    c->ozpm = P.take<double>(oz_slice_scratch_doubles(std::max<int64_t>(rl, OZ_NMAX), n));
+    c->ozpm2 = P.take<double>(oz_slice_scratch_doubles(OZ_NMAX, n));
+    for (OzScratch* o : {&c->ozs, &c->ozs2}) {
+      o->max_tiles = ceil_div(rl, 128);
+      o->max_grid = 256;
+      o->partial = P.take<double>(OzScratch::partial_doubles(o->max_tiles, o->max_grid));
+      o->counters = P.take<int>((size_t)o->max_tiles);
+    }
+  }
   if (c->world > 1) c->stage = P.take<double>((size_t)c->world * c->nloc * KMAX);
   // init-only
   c->Aup = P.take<double>(nn);
@@ -222,6 +255,8 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->rank_cap = (int32_t)std::min<int64_t>(cap, KMAX);
   c->h = o->h;
   c->fsal = o->no_fsal == 0;
+  // E pass on the int8 tensor cores (exact digit slicing) unless disabled or out of its range
+  c->oz = o->e_pass != DME_EPASS_DMMA && c->n <= OZ_KMAX && c->rows_loc > 0;
 }
 
 bool all_finite(const double* x, size_t cnt) {
@@ -351,10 +386,19 @@ struct ProfScope {
   }
 };
 void drain_profile(dme_ctx* c) {
+  static const bool timeline = getenv("DME_TIMELINE") != nullptr;
+  static const char* names[] = {"epass", "gram", "small", "apply", "other"};
   for (auto& r : c->pending) {
     DME_CUDA(cudaEventSynchronize(r.b));
     float ms = 0;
     DME_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    if (timeline && c->tl_base) {
+      float t0 = 0, t1 = 0;
+      if (cudaEventElapsedTime(&t0, c->tl_base, r.a) == cudaSuccess &&
+          cudaEventElapsedTime(&t1, c->tl_base, r.b) == cudaSuccess)
+        fprintf(stderr, "[dme timeline] %-6s %10.1f %10.1f us (%.1f)\n", names[r.cls < 5 ? r.cls : 4],
+                t0 * 1e3, t1 * 1e3, (t1 - t0) * 1e3);
+    }
     const double s = ms * 1e-3;
     switch (r.cls) {
       case PROF_EPASS:
@@ -375,10 +419,50 @@ void drain_profile(dme_ctx* c) {
 
 // ------------------------------------------------------------------ building blocks
 // out (col-major, ldo) = alpha * E * X  (E: n x n row-major, X: n x k col-major), sharded over ranks
+// out (rows x k) = alpha * E[rows] * X on the int8 tensor cores; E = E_{h/2} or E_h (sliced)
+void oz_pass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t out_cs,
+             double alpha, cudaStream_t st, bool second) {
+  int8_t* yq = second ? c->ozY2 : c->ozY;
+  int* ye = second ? c->exY2 : c->exY;
+  oz_slice_rows(X, c->ldn, k, c->n, yq, c->ozld, (int64_t)OZ_NMAX * c->ozld, ye,
+                second ? c->ozpm2 : c->ozpm, st);
+  OzGemmArgs g;
+  g.A = E == c->E_full ? c->ozEf : c->ozEh;
+  g.eA = E == c->E_full ? c->exEf : c->exEh;
+  g.lda = c->ozld; g.a_slice_stride = c->rows_loc * c->ozld;
+  g.B = yq; g.eB = ye; g.ldb = c->ozld; g.b_slice_stride = (int64_t)OZ_NMAX * c->ozld;
+  g.M = c->rows_loc; g.N = k; g.K = c->n; g.alpha = alpha;
+  g.out = out; g.out_rs = 1; g.out_cs = out_cs;
+  oz_gemm(g, second ? c->ozs2 : c->ozs, st);
+  c->stats.ozaki_passes++;
+}
+
 void epass_on(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t ldo,
               double alpha, cudaStream_t st, GemmScratch& gs) {
   if (k <= 0) return;
   c->stats.e_passes++;
+  const bool second = &gs == &c->gs2;
+  const bool use_oz = c->oz && c->oz_ready && k <= OZ_NMAX && (E == c->E_half || E == c->E_full);
+  if (use_oz && c->world == 1) {
+    ProfScope ps(c, PROF_EPASS, 2.0 * c->n * c->n * k, 1.0 * OZ_S * c->n * c->n, st);
+    oz_pass(c, E, X, k, out, ldo, alpha, st, second);
+    return;
+  }
+  if (use_oz) {
+    double* mine = c->stage + (size_t)c->rank * c->nloc * k;
+    {
+      ProfScope ps(c, PROF_EPASS, 2.0 * c->rows_loc * c->n * k, 1.0 * OZ_S * c->rows_loc * c->n, st);
+      oz_pass(c, E, X, k, mine, c->nloc, alpha, st, second);
+    }
+    DME_NCCL(ncclAllGather(mine, c->stage, (size_t)c->nloc * k, ncclDouble, c->comm, st));
+    for (int gr = 0; gr < c->world; ++gr) {
+      const int64_t r0 = std::min<int64_t>(c->n, (int64_t)gr * c->nloc);
+      const int64_t rows = std::min<int64_t>(c->nloc, c->n - r0);
+      if (rows > 0)
+        copy_cols(out + r0, ldo, c->stage + (size_t)gr * c->nloc * k, c->nloc, rows, k, 1.0, st);
+    }
+    return;
+  }
   if (c->world == 1) {
     GemmNTArgs g;
     g.A = E; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
@@ -423,7 +507,10 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
   a = SmallArgs();
   if (do_compress) {
     const int64_t kk = t3 ? k + c->m : k;
-    if (t3) copy_cols(Zc + k * c->ldn, c->ldn, c->Bcol, c->ldn, c->n, c->m, 1.0, c->st);
+    if (t3) {
+      ProfScope pc(c, 4);
+      copy_cols(Zc + k * c->ldn, c->ldn, c->Bcol, c->ldn, c->n, c->m, 1.0, c->st);
+    }
     ProfScope ps(c, PROF_GRAM);
     GemmNTArgs g;
     g.A = Zc; g.lda = c->ldn; g.B = Zc; g.ldb = c->ldn;
@@ -825,6 +912,9 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     Ecur = En;
   }
   DME_CUDA(cudaMemcpyAsync(c->E_half, Ecur, (size_t)n * ld * 8, cudaMemcpyDeviceToDevice, st));
+  if (c->oz)  // digit slices of the local rows of E_{h/2}
+    oz_slice_rows(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->ozld,
+                  c->rows_loc * c->ozld, c->exEh, c->ozpm, st);
   c->qh = q_cur;
   // L_I(h) = compress([L_I(h/2), E_{h/2} L_I(h/2)]),  E_h = E_{h/2}^2
   copy_cols(c->Zc12f, ld, c->Zc12h, ld, n, c->qh, 1.0, st);
@@ -832,6 +922,11 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   ladder_double(c, c->Zc12f, qf, c->E_half);
   c->qf = qf;
   matmul_sq(c, c->E_half, c->E_half, c->E_full);
+  if (c->oz) {
+    oz_slice_rows(c->E_full + c->row0 * ld, ld, c->rows_loc, n, c->ozEf, c->ozld,
+                  c->rows_loc * c->ozld, c->exEf, c->ozpm, st);
+    c->oz_ready = true;
+  }
   // look-ahead operand: E_h L_I(h) stays in the leading columns of LA
   epass(c, c->E_full, c->Zc12f, c->qf, c->LA, ld, 1.0);
   c->stats.q_half = c->qh;
@@ -919,6 +1014,8 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     P.base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(o->workspace) + 255) & ~uintptr_t(255));
     plan_buffers(c, P);
     c->gs2.max_grid = std::max(1, num_sms() - EIG_SPLIT_CTAS);  // SMs left to the eigen kernels
+    c->ozs.max_grid = std::min(256, num_sms());
+    c->ozs2.max_grid = std::max(1, num_sms() - EIG_SPLIT_CTAS);
     if (c->world > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, o->nccl_uid, sizeof(uid));
@@ -1033,6 +1130,11 @@ dme_status dme_split_step(dme_ctx* c, dme_scheme scheme, dme_composition comp, i
     DME_REQUIRE(nsteps >= 0, DME_ERR_INVALID, "nsteps must be >= 0");
     auto seq = step_sequence(scheme, comp, c->h);
     check_capable(c, seq);
+    if (c->profile && getenv("DME_TIMELINE")) {
+      if (!c->tl_base) DME_CUDA(cudaEventCreate(&c->tl_base));
+      DME_CUDA(cudaEventRecord(c->tl_base, c->st));
+      fprintf(stderr, "[dme timeline] split_step start\n");
+    }
     // FSAL: under Strang, the trailing A(h/2) of a step and the leading A(h/2) of the next are one
     // A(h) when A is a semigroup flow computed exactly (T1: E_{h/2}^2 = E_h; T12: the ladder rule
     // gives I(h) = I(h/2) + E_{h/2} I(h/2) E_{h/2}^T exactly), so nsteps steps run as
@@ -1190,7 +1292,7 @@ dme_status dme_debug_matmul(int64_t M, int64_t N, int64_t K, const double* A, co
                             double* C) {
   return guarded(nullptr, [&] {
     DME_REQUIRE(M > 0 && N > 0 && K > 0 && A && B && C, DME_ERR_INVALID, "bad matmul args");
-    const int64_t ldk = (K + 1) / 2 * 2;
+    const int64_t ldk = (K + 15) / 16 * 16;
     double *dA, *dBT, *dC, *part;
     int* cnt;
     GemmScratch gs;
@@ -1217,6 +1319,53 @@ dme_status dme_debug_matmul(int64_t M, int64_t N, int64_t K, const double* A, co
     DME_CUDA(cudaDeviceSynchronize());
     DME_CUDA(cudaMemcpy(C, dC, M * N * 8, cudaMemcpyDeviceToHost));
     cudaFree(dA); cudaFree(dBT); cudaFree(dC); cudaFree(part); cudaFree(cnt);
+  });
+}
+
+dme_status dme_debug_matmul_ozaki(int64_t M, int64_t N, int64_t K, const double* A, const double* B,
+                                  double* C) {
+  return guarded(nullptr, [&] {
+    DME_REQUIRE(M > 0 && N > 0 && K > 0 && A && B && C, DME_ERR_INVALID, "bad matmul args");
+    DME_REQUIRE(N <= OZ_NMAX && K <= OZ_KMAX, DME_ERR_DIM, "ozaki matmul: N <= 64, K <= 32768");
+    const int64_t ldd = (K + 15) / 16 * 16, ldq = oz_ldk(K);
+    double *dA, *dBT, *dC, *part;
+    int8_t *qa, *qb;
+    int *ea, *eb, *cnt;
+    double* pm;
+    OzScratch ws;
+    ws.max_tiles = ceil_div(M, 128);
+    ws.max_grid = std::min(256, num_sms());
+    DME_CUDA(cudaMalloc(&dA, M * ldd * 8));
+    DME_CUDA(cudaMalloc(&dBT, OZ_NMAX * ldd * 8));
+    DME_CUDA(cudaMalloc(&dC, M * N * 8));
+    DME_CUDA(cudaMalloc(&qa, (size_t)OZ_S * M * ldq));
+    DME_CUDA(cudaMalloc(&qb, (size_t)OZ_S * OZ_NMAX * ldq));
+    DME_CUDA(cudaMalloc(&ea, M * sizeof(int)));
+    DME_CUDA(cudaMalloc(&eb, OZ_NMAX * sizeof(int)));
+    DME_CUDA(cudaMalloc(&part, OzScratch::partial_doubles(ws.max_tiles, ws.max_grid) * 8));
+    DME_CUDA(cudaMalloc(&cnt, ws.max_tiles * sizeof(int)));
+    DME_CUDA(cudaMalloc(&pm, oz_slice_scratch_doubles(std::max<int64_t>(M, N), K) * 8));
+    DME_CUDA(cudaMemset(cnt, 0, ws.max_tiles * sizeof(int)));
+    DME_CUDA(cudaMemset(qb, 0, (size_t)OZ_S * OZ_NMAX * ldq));
+    ws.partial = part;
+    ws.counters = cnt;
+    DME_CUDA(cudaMemcpy2D(dA, ldd * 8, A, K * 8, K * 8, M, cudaMemcpyHostToDevice));
+    std::vector<double> bt((size_t)N * K);
+    for (int64_t i = 0; i < K; ++i)
+      for (int64_t j = 0; j < N; ++j) bt[j * K + i] = B[i * N + j];
+    DME_CUDA(cudaMemcpy2D(dBT, ldd * 8, bt.data(), K * 8, K * 8, N, cudaMemcpyHostToDevice));
+    oz_slice_rows(dA, ldd, M, K, qa, ldq, M * ldq, ea, pm, 0);
+    oz_slice_rows(dBT, ldd, N, K, qb, ldq, OZ_NMAX * ldq, eb, pm, 0);
+    OzGemmArgs g;
+    g.A = qa; g.eA = ea; g.lda = ldq; g.a_slice_stride = M * ldq;
+    g.B = qb; g.eB = eb; g.ldb = ldq; g.b_slice_stride = OZ_NMAX * ldq;
+    g.M = M; g.N = N; g.K = K;
+    g.out = dC; g.out_rs = N; g.out_cs = 1;
+    oz_gemm(g, ws, 0);
+    DME_CUDA(cudaDeviceSynchronize());
+    DME_CUDA(cudaMemcpy(C, dC, M * N * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dA); cudaFree(dBT); cudaFree(dC); cudaFree(part); cudaFree(cnt);
+    cudaFree(qa); cudaFree(qb); cudaFree(ea); cudaFree(eb); cudaFree(pm);
   });
 }
 

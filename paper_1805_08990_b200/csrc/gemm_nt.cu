@@ -429,6 +429,20 @@ CUtensorMap make_tmap_3d(const double* base, uint64_t d0, uint64_t d1, uint64_t 
   return m;
 }
 
+CUtensorMap make_tmap_3d_u8(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
+                            uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1_bytes, s2_bytes};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides,
+                           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled(3d u8) failed: " + std::to_string(r));
+  return m;
+}
+
 namespace {
 std::atomic<int64_t> g_launches{0};
 }

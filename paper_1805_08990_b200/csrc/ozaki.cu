@@ -1,0 +1,437 @@
+// E·Y on the int8 tensor cores by exact digit slicing (see ozaki.h).
+//
+// Kernel layout (one persistent CTA per SM, 224 threads):
+//   warp 0      TMA producer of E: per 128-deep K chunk OZ_S boxes of 128 rows x 128 bytes of E
+//               digits (A ring, one slice per stage);
+//   warp 6      TMA producer of Y: per K chunk one 3D box with all OZ_S digit slices of the Y
+//               columns (B ring, 2 stages), running ahead independently of the A ring;
+//   warp 1      TMEM owner (512 columns) and MMA issuer (one thread): for E slice a the B operand
+//               is Y slices b = 0 .. OZ_S-1-a stacked along N, written at TMEM column a*NP, so the
+//               accumulator block c holds sum_{a+b=c} D_a Y_b (c = 0 .. OZ_S-1, NP columns each);
+//   warps 2..5  epilogue: TMEM -> registers, sum_c 2^{-7(c+2)} acc_c in FP64, scale by
+//               2^{e_i + f_j}, store (or write a partial and let the last CTA of the tile reduce
+//               the partials in CTA order: deterministic).
+#include "common.cuh"
+#include "ozaki.h"
+
+#include <algorithm>
+
+namespace dme {
+namespace {
+
+template <int NP>
+struct OzCfg {
+  static constexpr int S = OZ_S;
+  static constexpr int BST = S * NP * 128;  // B stage: all slices, NP rows x 128 bytes each
+  static constexpr int AST = 128 * 128;     // A stage: one slice, 128 rows x 128 bytes
+  static constexpr int NB = 2;
+  static constexpr int NA = (212 * 1024 - NB * BST) / AST;
+  static constexpr int NBAR = 2 * NA + 2 * NB + 2;
+  static constexpr int SMEM = NB * BST + NA * AST + 1024 + NBAR * 8 + 16;
+  static_assert(NA >= 4, "A ring too shallow");
+};
+
+// ------------------------------------------------------------------ tcgen05 wrappers
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  // K-major operand, 128-byte swizzle: rows of 128 B, 8-row groups 1024 B apart (SBO), LBO unused,
+  // descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// low / high halves of the descriptor: lo = start address >> 4 | LBO (1) << 16, hi = SBO (1024 B)
+// | version 1 | SWIZZLE_128B; operands only move the start address, so lo += bytes >> 4
+__device__ __forceinline__ uint32_t desc_lo(uint32_t saddr) { return ((saddr >> 4) & 0x3FFFu) | (1u << 16); }
+__device__ __forceinline__ uint64_t mk_desc(uint32_t lo) {
+  return (uint64_t)lo | ((uint64_t)((1024 >> 4) | (1u << 14) | (2u << 29)) << 32);
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(p));
+  return p != 0;
+}
+__device__ __forceinline__ uint32_t idesc_i8(int N) {
+  // D s32 (bits 4-5 = 2), A s8 (bits 7-9 = 1), B s8 (bits 10-12 = 1), K-major both,
+  // N >> 3 at bits 17-22, M >> 4 = 8 (M = 128) at bits 24-28
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t addr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+      " [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// int32 (as raw bits) -> double, exactly, without the quarter-rate I2F.F64
+__device__ __forceinline__ double i2d_exact(uint32_t v) {
+  return __hiloint2double(0x43300000, (int)(v ^ 0x80000000u)) - 4503601774854144.0;  // 2^52 + 2^31
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+      " [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// x * 2^s exactly for |s| <= 2000 (two normal-range power-of-two factors)
+__device__ __forceinline__ double scale2(double x, int s) {
+  s = s < -2000 ? -2000 : (s > 2000 ? 2000 : s);  // beyond: under/overflow either way
+  const int s1 = s / 2, s2 = s - s1;
+  return x * __longlong_as_double((long long)(1023 + s1) << 52) *
+         __longlong_as_double((long long)(1023 + s2) << 52);
+}
+
+// Stream-K: CTA b owns the units [b U / G, (b+1) U / G) of the (tile, K chunk) sequence
+__device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
+  int64_t b = (u * G) / U;
+  while (b + 1 < G && ((b + 1) * U) / G <= u) ++b;
+  while (b > 0 && (b * U) / G > u) --b;
+  return (int)b;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(224, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const int* __restrict__ eA, const int* __restrict__ eB, double* __restrict__ out,
+                   int64_t out_rs, int64_t out_cs, int M, int N, int nkc, int tiles, double alpha,
+                   double* __restrict__ partial, int* __restrict__ counters) {
+  using C = OzCfg<NP>;
+  constexpr int S = C::S;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* Bs = base;
+  uint8_t* As = base + C::NB * C::BST;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(As + C::NA * C::AST);
+  uint64_t* full_a = bars;
+  uint64_t* empty_a = bars + C::NA;
+  uint64_t* full_b = bars + 2 * C::NA;
+  uint64_t* empty_b = full_b + C::NB;
+  uint64_t* tfull = empty_b + C::NB;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int64_t U = (int64_t)tiles * nkc;
+  const int64_t u0 = (int64_t)blockIdx.x * U / G, u1 = (int64_t)(blockIdx.x + 1) * U / G;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, 1); }
+    for (int i = 0; i < C::NB; ++i) { mbar_init(full_b + i, 1); mbar_init(empty_b + i, 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);  // one arrive per epilogue warp
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 || warp == 6) {
+    if (lane == 0) {  // ---------------------------------------- TMA producers: A (warp 0), B (warp 6)
+      const bool isA = warp == 0;
+      if (isA) prefetch_tmap(&tmA); else prefetch_tmap(&tmB);
+      int as = 0, bs = 0;
+      uint32_t pa = 0, pb = 0;
+      for (int64_t u = u0; u < u1;) {
+        const int tile = (int)(u / nkc);
+        const int kc0 = (int)(u % nkc);
+        const int kc1 = (int)(kc0 + (u1 - u) < nkc ? kc0 + (u1 - u) : nkc);
+        for (int kc = kc0; kc < kc1; ++kc) {
+          if (!isA) {
+            mbar_wait(empty_b + bs, pb ^ 1);
+            mbar_arrive_expect_tx(full_b + bs, C::BST);
+            tma_load_3d(Bs + bs * C::BST, &tmB, full_b + bs, kc * 128, 0, 0);
+            if (++bs == C::NB) { bs = 0; pb ^= 1; }
+            continue;
+          }
+          for (int a = 0; a < S; ++a) {
+            mbar_wait(empty_a + as, pa ^ 1);
+            mbar_arrive_expect_tx(full_a + as, C::AST);
+            tma_load_3d(As + as * C::AST, &tmA, full_a + as, kc * 128, tile * 128, a);
+            if (++as == C::NA) { as = 0; pa ^= 1; }
+          }
+        }
+        u += kc1 - kc0;
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (whole warp waits,
+    // one elected lane issues; descriptors are base + compile-time offsets)
+    int as = 0, bs = 0, seg = 0;
+    uint32_t pa = 0, pb = 0;
+    const uint32_t lo_a0 = desc_lo(smem_u32(As)), lo_b0 = desc_lo(smem_u32(Bs));
+    for (int64_t u = u0; u < u1; ++seg) {
+      const int kc0 = (int)(u % nkc);
+      const int kc1 = (int)(kc0 + (u1 - u) < nkc ? kc0 + (u1 - u) : nkc);
+      if (seg > 0) mbar_wait(tempty, (seg - 1) & 1);  // epilogue has drained the accumulators
+      tc_fence_after();
+      for (int kc = kc0; kc < kc1; ++kc) {
+        mbar_wait(full_b + bs, pb);
+        tc_fence_after();
+        const uint32_t lo_b = lo_b0 + (uint32_t)(bs * (C::BST >> 4));
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          mbar_wait(full_a + as, pa);
+          tc_fence_after();
+          const uint32_t lo_a = lo_a0 + (uint32_t)(as * (C::AST >> 4));
+          if (elect_one()) {
+            const int rows = (S - a) * NP;                        // Y slices 0 .. S-1-a
+            const int n0 = rows <= 256 ? rows : ((rows / 2 + 15) / 16) * 16;  // balanced split
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {                      // 4 x K=32 per 128-byte chunk
+              const uint32_t acc = (kc > kc0 || a > 0 || ks > 0) ? 1u : 0u;
+              const uint64_t ad = mk_desc(lo_a + ks * 2);
+              mma_i8(tmem + (uint32_t)(a * NP), ad, mk_desc(lo_b + ks * 2), idesc_i8(n0), acc);
+              if (rows > n0)
+                mma_i8(tmem + (uint32_t)(a * NP + n0), ad, mk_desc(lo_b + ks * 2 + n0 * 8),
+                       idesc_i8(rows - n0), acc);
+            }
+            umma_commit(empty_a + as);  // A slot free once these MMAs have read it
+          }
+          __syncwarp();
+          if (++as == C::NA) { as = 0; pa ^= 1; }
+        }
+        if (elect_one()) umma_commit(empty_b + bs);
+        __syncwarp();
+        if (++bs == C::NB) { bs = 0; pb ^= 1; }
+      }
+      if (elect_one()) umma_commit(tfull);
+      __syncwarp();
+      u += kc1 - kc0;
+    }
+  } else if (warp <= 5) {  // ------------------------------------------------ epilogue (warps 2..5)
+    const int qd = warp & 3;            // TMEM sub-partition of this warp
+    const int rl = 32 * qd + lane;      // row within the tile
+    const int et = threadIdx.x - 64;    // 0..127
+    int seg = 0;
+    for (int64_t u = u0; u < u1; ++seg) {
+      const int tile = (int)(u / nkc);
+      const int kc0 = (int)(u % nkc);
+      const int kc1 = (int)(kc0 + (u1 - u) < nkc ? kc0 + (u1 - u) : nkc);
+      mbar_wait(tfull, seg & 1);
+      tc_fence_after();
+      // drain TMEM: per accumulator block c (smallest scale first) NP/16 loads, one wait
+      double acc[NP];
+#pragma unroll
+      for (int j = 0; j < NP; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int c = S - 1; c >= 0; --c) {
+        uint32_t v[NP];
+#pragma unroll
+        for (int j0 = 0; j0 < NP; j0 += 16)
+          tmem_ld16_nowait(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(c * NP + j0), v + j0);
+        tmem_wait_ld();
+        const double sc = __longlong_as_double((long long)(1023 - 7 * (c + 2)) << 52);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) acc[j] = fma(i2d_exact(v[j]), sc, acc[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+
+      const int row = tile * 128 + rl;
+      const int ea = row < M ? eA[row] : 0;
+      const bool whole = kc0 == 0 && kc1 == nkc;
+      if (whole) {
+        if (row < M) {
+#pragma unroll
+          for (int j = 0; j < NP; ++j)
+            if (j < N) out[(int64_t)row * out_rs + (int64_t)j * out_cs] = alpha * scale2(acc[j], ea + eB[j]);
+        }
+      } else {
+        double* slot = partial + (size_t)(tile + blockIdx.x) * OZ_NMAX * 128;
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+          __stcg(slot + j * 128 + rl, (j < N && row < M) ? alpha * scale2(acc[j], ea + eB[j]) : 0.0);
+        __threadfence();
+        named_bar_sync(1, 128);
+        const int b0 = cta_of((int64_t)tile * nkc, U, G);
+        const int b1 = cta_of((int64_t)tile * nkc + nkc - 1, U, G);
+        if (et == 0) {
+          const int old = atomicAdd(counters + tile, 1);
+          *flag = (old == b1 - b0) ? 1 : 0;
+        }
+        named_bar_sync(1, 128);
+        if (*flag) {  // last CTA of the tile: sum the partials in CTA order (deterministic)
+          __threadfence();
+          if (row < M) {
+            constexpr int JC = NP < 32 ? NP : 32;
+#pragma unroll
+            for (int j0 = 0; j0 < NP; j0 += JC) {
+              double sum[JC];
+#pragma unroll
+              for (int t = 0; t < JC; ++t) sum[t] = 0.0;
+              for (int b = b0; b <= b1; ++b) {
+                const double* src = partial + (size_t)(tile + b) * OZ_NMAX * 128 + rl;
+                double v[JC];
+#pragma unroll
+                for (int t = 0; t < JC; ++t) v[t] = __ldcg(src + (j0 + t) * 128);
+#pragma unroll
+                for (int t = 0; t < JC; ++t) sum[t] += v[t];
+              }
+#pragma unroll
+              for (int t = 0; t < JC; ++t)
+                if (j0 + t < N) out[(int64_t)row * out_rs + (int64_t)(j0 + t) * out_cs] = sum[t];
+            }
+          }
+          if (et == 0) counters[tile] = 0;
+        }
+        named_bar_sync(1, 128);
+      }
+      u += kc1 - kc0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ digit slicing
+constexpr int SL_T = 256, SL_CH = SL_T * 4 * 2;  // threads, columns per CTA chunk
+
+__global__ void __launch_bounds__(SL_T) oz_rowmax_kernel(const double* __restrict__ X, int64_t ld,
+                                                         int64_t cols, double* __restrict__ pm) {
+  __shared__ double red[SL_T / 32];
+  const int64_t row = blockIdx.y, c0 = (int64_t)blockIdx.x * SL_CH;
+  const double* x = X + row * ld;
+  double m = 0.0;
+#pragma unroll
+  for (int t = 0; t < SL_CH / SL_T; ++t) {
+    const int64_t c = c0 + t * SL_T + threadIdx.x;
+    if (c < cols) m = fmax(m, fabs(x[c]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < SL_T / 32; ++w) m = fmax(m, red[w]);
+    pm[row * gridDim.x + blockIdx.x] = m;
+  }
+}
+
+__global__ void __launch_bounds__(SL_T) oz_slice_kernel(const double* __restrict__ X, int64_t ld,
+                                                        int64_t cols, const double* __restrict__ pm,
+                                                        int8_t* __restrict__ q, int64_t ldk,
+                                                        int64_t sstride, int* __restrict__ ex) {
+  const int64_t row = blockIdx.y;
+  double mx = 0.0;
+  for (unsigned i = 0; i < gridDim.x; ++i) mx = fmax(mx, pm[row * gridDim.x + i]);
+  const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;  // max |x| 2^-e in [1/4, 1/2)
+  if (blockIdx.x == 0 && threadIdx.x == 0) ex[row] = e;
+  const double* x = X + row * ld;
+  const int64_t c4end = (cols + 3) / 4 * 4;
+#pragma unroll
+  for (int it = 0; it < SL_CH / (SL_T * 4); ++it) {
+    const int64_t c4 = (int64_t)blockIdx.x * SL_CH + ((int64_t)it * SL_T + threadIdx.x) * 4;
+    if (c4 >= c4end) break;
+    uint32_t w[OZ_S];
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) w[s] = 0u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      double v = c4 + t < cols ? scale2(x[c4 + t], -e) : 0.0;
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) {
+        v *= 128.0;                 // exact
+        const double d = rint(v);   // |d| <= 64
+        v -= d;                     // exact, |v| <= 1/2
+        w[s] |= (uint32_t)(uint8_t)(int8_t)(int)d << (8 * t);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s)
+      *reinterpret_cast<uint32_t*>(q + s * sstride + row * ldk + c4) = w[s];
+  }
+}
+
+template <int NP>
+void launch_oz(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
+  using C = OzCfg<NP>;
+  const int nkc = (int)ceil_div(a.K, 128), tiles = (int)ceil_div(a.M, 128);
+  const int64_t U = (int64_t)tiles * nkc;
+  const int G = (int)std::min<int64_t>(ws.max_grid, U);
+  if (tiles > ws.max_tiles) throw std::runtime_error("oz_gemm: scratch too small");
+  const CUtensorMap tmA = make_tmap_3d_u8(a.A, a.K, a.M, OZ_S, a.lda, a.a_slice_stride, 128, 128, 1);
+  const CUtensorMap tmB = make_tmap_3d_u8(a.B, a.K, NP, OZ_S, a.ldb, a.b_slice_stride, 128, NP, OZ_S);
+  static bool attr = false;
+  if (!attr) {
+    DME_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  oz_gemm_kernel<NP><<<G, 224, C::SMEM, st>>>(tmA, tmB, a.eA, a.eB, a.out, a.out_rs, a.out_cs,
+                                              (int)a.M, (int)a.N, nkc, tiles, a.alpha, ws.partial,
+                                              ws.counters);
+  DME_KCHECK();
+}
+
+}  // namespace
+
+int64_t oz_slice_scratch_doubles(int64_t rows, int64_t cols) { return rows * ceil_div(cols, SL_CH); }
+
+void oz_slice_rows(const double* X, int64_t ld, int64_t rows, int64_t cols, int8_t* q, int64_t ldk,
+                   int64_t slice_stride, int* ex, double* scratch, cudaStream_t st) {
+  if (rows <= 0) return;
+  const dim3 grid((unsigned)std::max<int64_t>(1, ceil_div(cols, SL_CH)), (unsigned)rows);
+  oz_rowmax_kernel<<<grid, SL_T, 0, st>>>(X, ld, cols, scratch);
+  DME_KCHECK();
+  oz_slice_kernel<<<grid, SL_T, 0, st>>>(X, ld, cols, scratch, q, ldk, slice_stride, ex);
+  DME_KCHECK();
+}
+
+void oz_gemm(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
+  if (a.M <= 0 || a.N <= 0) return;
+  if (a.N > OZ_NMAX || a.K > OZ_KMAX || a.K <= 0)
+    throw std::runtime_error("oz_gemm: N > 64 or K out of range");
+  const int np = (int)((a.N + 15) / 16 * 16);
+  switch (np) {
+    case 16: launch_oz<16>(a, ws, st); break;
+    case 32: launch_oz<32>(a, ws, st); break;
+    case 48: launch_oz<48>(a, ws, st); break;
+    default: launch_oz<64>(a, ws, st); break;
+  }
+}
+
+}  // namespace dme
