@@ -29,6 +29,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "split steps/sec & time-to-T, n=10000 DRE FP64"
 UNIT = "steps/s"
+OZ_PAIRS = 36           # digit-slice pairs a + b <= 7 of the int8 E pass (ozaki.h, OZ_S = 8)
 FP64_PEAK_TFLOPS = 36.6   # measured DMMA microbenchmark on this pool's B200 (profiles/r01_peaks_fp64.json)
 H, NT, RANK_CAP = 0.005, 100, 64
 
@@ -216,28 +217,82 @@ def run_ours(args):
     # ------------------------------------------------------------ roofline of the dominant kernel
     ep_s, ep_f, ep_b, npass = (st["prof_epass_seconds"], st["prof_epass_flops"],
                                st["prof_epass_bytes"], st["prof_passes"])
-    achieved_tf = ep_f / ep_s / 1e12 if ep_s > 0 else None
-    achieved_gbs = ep_b / ep_s / 1e9 if ep_s > 0 else None
     peaks = _peaks()
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_peak = peaks.get("hbm_gbs", 6538.6)
+    achieved_tf = ep_f / ep_s / 1e12 if ep_s > 0 else None     # FP64-equivalent 2 n^2 k
+    achieved_gbs = ep_b / ep_s / 1e9 if ep_s > 0 else None     # 8 n^2 bytes of E per pass
     tr = _traffic()
-    roofline = {"bound": "tensor", "kernel": "gemm_nt (E_{h/2} L, FP64 DMMA)",
-                "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": (achieved_tf / FP64_PEAK_TFLOPS) if achieved_tf else None,
-                "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_peaks_fp64.json); "
-                               "MEASURED_PEAKS.json has no FP64 entry",
-                "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm_peak,
-                             "frac": (achieved_gbs / hbm_peak) if achieved_gbs else None},
-                "algorithmic_per_launch": {"flops": ep_f / max(npass, 1), "bytes": ep_b / max(npass, 1)},
-                "share_of_step": ep_s / (ms_prof * 1e-3) if ms_prof > 0 else None,
-                "gram_share": st["prof_gram_seconds"] / (ms_prof * 1e-3),
-                "small_eig_share": st["prof_small_seconds"] / (ms_prof * 1e-3),
-                "apply_share": st["prof_apply_seconds"] / (ms_prof * 1e-3),
-                "shares_note": "per-class kernel time / wall of a separate profiled run of the same "
-                               "K steps (E pass and eigen solve overlap on two streams)",
-                "profiled_ms_per_step": ms_prof / args.steps,
-                "passes_timed": npass}
+    shares = {"share_of_step": ep_s / (ms_prof * 1e-3) if ms_prof > 0 else None,
+              "gram_share": st["prof_gram_seconds"] / (ms_prof * 1e-3),
+              "small_eig_share": st["prof_small_seconds"] / (ms_prof * 1e-3),
+              "apply_share": st["prof_apply_seconds"] / (ms_prof * 1e-3),
+              "shares_note": "per-class kernel time / wall of a separate profiled run of the same "
+                             "K steps (E pass and eigen solve overlap on two streams)",
+              "profiled_ms_per_step": ms_prof / args.steps, "passes_timed": npass}
+    if st["ozaki_passes"] > 0:
+        # int8 digit-slicing pass: OZ_PAIRS int8 GEMMs of the E digit slices with the Y slices.
+        # Binding roof = max(tensor time, HBM time); both reported.
+        i8_peak = 2.0 * peaks.get("bf16_tflops", 1668.9)          # nominal int8:bf16 = 2
+        achieved_tops = OZ_PAIRS * ep_f / ep_s / 1e12 if ep_s > 0 else None
+        t_tensor = OZ_PAIRS * ep_f / (i8_peak * 1e12)
+        t_hbm = ep_b / (hbm_peak * 1e9)
+        if t_tensor >= t_hbm:
+            bound, ach, peak, unit = "tensor", achieved_tops, i8_peak, "TOP/s (int8)"
+        else:
+            bound, ach, peak, unit = "hbm", achieved_gbs, hbm_peak, "GB/s"
+        roofline = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit,
+                    "frac": (ach / peak) if ach else None,
+                    "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                    "kernel": "oz_gemm (E_h L on int8 tensor cores, tcgen05.mma kind::i8, "
+                              "8 digit slices per operand, 36 slice pairs, FP64 assembly)",
+                    "peak_source": "int8: 2 x MEASURED_PEAKS.bf16_tflops (nominal int8:bf16 = 2); "
+                                   "hbm: MEASURED_PEAKS.hbm_gbs",
+                    "tensor_view": {"achieved_tops": achieved_tops, "peak_tops": i8_peak,
+                                    "frac": achieved_tops / i8_peak if achieved_tops else None},
+                    "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm_peak,
+                                 "frac": (achieved_gbs / hbm_peak) if achieved_gbs else None},
+                    "fp64_equivalent_tflops": achieved_tf,
+                    "algorithmic_per_launch": {"int8_ops": OZ_PAIRS * ep_f / max(npass, 1),
+                                               "fp64_equiv_flops": ep_f / max(npass, 1),
+                                               "bytes": ep_b / max(npass, 1)},
+                    **shares}
+    else:
+        roofline = {"bound": "tensor", "kernel": "gemm_nt (E_h L, FP64 DMMA)",
+                    "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": (achieved_tf / FP64_PEAK_TFLOPS) if achieved_tf else None,
+                    "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                    "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_peaks_fp64.json); "
+                                   "MEASURED_PEAKS.json has no FP64 entry",
+                    "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm_peak,
+                                 "frac": (achieved_gbs / hbm_peak) if achieved_gbs else None},
+                    "algorithmic_per_launch": {"flops": ep_f / max(npass, 1),
+                                               "bytes": ep_b / max(npass, 1)},
+                    **shares}
+
+    # ------------------------------------------------------------ native-FP64 (DMMA) variant
+    variant = None
+    if not args.no_variant:
+        s3 = dme.Solver(**dme.problem_kwargs(prob), **kw, e_pass="dmma")
+        s3.split_step("strang", "F12F3", args.warmup)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(s3.stream)
+        s3.split_step("strang", "F12F3", args.steps)
+        v1.record(s3.stream)
+        torch.cuda.synchronize()
+        ms3 = v0.elapsed_time(v1)
+        if world > 1:
+            t = torch.tensor([ms3], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms3 = float(t.item())
+        variant = {"e_pass": "dmma (native FP64 mma.sync m8n8k4)", "value": args.steps / (ms3 * 1e-3),
+                   "unit": UNIT, "ms_per_step": ms3 / args.steps,
+                   "ozaki_passes": s3.stats()["ozaki_passes"]}
+        s3.close()
+        del s3
+        torch.cuda.empty_cache()
 
     # ------------------------------------------------------------ end to end through the public API
     e2e = None
@@ -280,6 +335,11 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
+                "dtype_detail": ("FP64 everywhere except the E pass, which runs on int8 tensor cores "
+                                 "as an exact digit-sliced FP64 product (8 x 7-bit digits per operand, "
+                                 "int32 exact accumulation, FP64 assembly; per-entry error <= "
+                                 "2^-54 max_l|E_il| sum_l|L_lj|, DESIGN.md 5b)"
+                                 if st["ozaki_passes"] > 0 else "FP64 (DMMA + DFMA)"),
                 "config": {"workload": "config5: DRE 2D heat n=10000 (n_x=100), Strang F12F3, "
                                        "rank cap 64, tol 1e-16, h=0.005 (T=0.5, N_t=100)",
                            "n": prob.n, "rank_after_timed_steps": rank_now,
@@ -289,7 +349,8 @@ def run_ours(args):
                 "time_to_T_what": "init from HBM-resident A (wall, synchronised) + 100 x ms_per_step",
                 "init_s": init_wall, "init_lib_s": init_dev,
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk.summary()}
+                "gpu_launches": launches, "clocks": clk.summary(),
+                "fp64_dmma_variant": variant}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -305,6 +366,7 @@ def main():
     ap.add_argument("--nx", type=int, default=100, help="(debug) grid size; default = config 5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variant", action="store_true", help="skip the native-FP64 E-pass run")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -158,7 +158,7 @@ class Solver:
     def __init__(self, A, C=None, L0=None, D0=None, B=None, R=None, S=None, *, h, trunc_tol=1e-16,
                  rank_cap=0, quad_nodes=14, quad_subpanels=1, device=None, stream=None,
                  world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None, fsal=True,
-                 e_pass="auto"):
+                 e_pass="auto", poison_workspace=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1805_08990_b200.Solver needs a CUDA device (no CPU fallback)")
@@ -200,6 +200,8 @@ class Solver:
         _check(_lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(opt), ctypes.byref(nbytes)),
                "dme_workspace_size")
         self.workspace = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=dev)
+        if poison_workspace:  # test hook: the library must not rely on zeroed caller memory
+            self.workspace.fill_(0xFF)
         opt.workspace = self.workspace.data_ptr()
         opt.workspace_bytes = self.workspace.numel()
         self._opt = opt

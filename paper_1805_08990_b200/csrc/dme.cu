@@ -777,6 +777,10 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   cudaStream_t st = c->st;
   DME_CUDA(cudaMemsetAsync(c->gs.counters, 0, sizeof(int) * c->gs.max_tiles, st));
   DME_CUDA(cudaMemsetAsync(c->gs2.counters, 0, sizeof(int) * c->gs2.max_tiles, st));
+  // the Stream-K fixup counters of the int8 E pass (the workspace is uninitialised caller memory)
+  if (c->oz)
+    for (OzScratch* o : {&c->ozs, &c->ozs2})
+      DME_CUDA(cudaMemsetAsync(o->counters, 0, sizeof(int) * o->max_tiles, st));
   // ---------------------------------------------------------------- upload (H2D boundary)
   // A and S: host memory (pageable or pinned) or, with options.big_inputs_on_device, device memory
   const cudaMemcpyKind kbig = c->opt.big_inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;

@@ -127,3 +127,20 @@ def test_device_resident_inputs(dme):
     La, Da = a.get_factor()
     Lb, Db = b.get_factor()
     assert np.array_equal(La, Lb)
+
+
+@pytest.mark.parametrize("e_pass", ["auto", "dmma"])
+def test_poisoned_workspace(dme, e_pass):
+    """The workspace is caller memory with arbitrary contents (0xFF bytes here): every counter and
+    scratch the kernels rely on is initialised by the library (regression: the int8 E pass's Stream-K
+    fixup counters were once left uninitialised)."""
+    prob = make_config(5, nx=30)
+    out = []
+    for poison in (False, True):
+        s = dme.Solver(**dme.problem_kwargs(prob), h=0.005, rank_cap=64, e_pass=e_pass,
+                       poison_workspace=poison)
+        s.split_step("strang", "F12F3", 4)
+        out.append(s.get_factor())
+        s.close()
+    (L1, D1), (L2, D2) = out
+    assert L1.shape == L2.shape and np.array_equal(L1, L2) and np.array_equal(D1, D2)
