@@ -45,6 +45,17 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
   return cnt;
 }
 
+// 1/x to ~1 ulp without the IEEE division sequence: MUFU reciprocal seed + two Newton steps
+// (callers guarantee a normal, finite, nonzero x)
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double t = fma(-x, r, 1.0);
+  r = fma(r, t, r);
+  t = fma(-x, r, 1.0);
+  return fma(r, t, r);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

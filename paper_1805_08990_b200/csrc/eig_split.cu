@@ -51,8 +51,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
     const int i = e_ % k, j = e_ / k;
     A[i * ld + j] = 0.5 * (a.G[i + (size_t)j * a.ldg] + a.G[j + (size_t)i * a.ldg]);
   }
+  const long long t0 = clock64();
   __syncthreads();
   tridiagonalise<FK>(A, k, ld, d, e, tau, vec, pv, pv2);
+  const long long t1 = clock64();
   if (tid == 0) {
     normalise_tridiagonal(k, d, e, e2, &s_scale, &s_lo, &s_hi);
     s_lo_t = s_lo;
@@ -88,6 +90,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
     h[2] = s_hi;
     h[3] = tmax;
     h[4] = (double)r;
+    if (a.stats) {  // phase cycles (tools/eig_split_probe.py)
+      a.stats[8] = (double)(t1 - t0);
+      a.stats[9] = (double)(clock64() - t1);
+    }
   }
   for (int i = tid; i < k; i += ENT) {
     es.d()[i] = d[i];
@@ -110,6 +116,8 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = a.k, ld = k | 1;
   const EsLayout es{a.Es, SMALL_K_MAX};
+  long long t_ph[5];
+  t_ph[0] = clock64();
   const double* h = es.hdr();
   const int r = (int)h[4];
   const int nr = r < k ? r + 1 : r;
@@ -128,9 +136,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   __syncthreads();
 
   // ------------------------------------------------------------ multisection on this slice
+  t_ph[1] = clock64();
   {
     int P = ENT / nb;
-    P = P < 1 ? 1 : (P > 64 ? 64 : P);
+    P = P < 1 ? 1 : (P > 16 ? 16 : P);  // more probes: more busy warps, no fewer cycles (measured)
     const int grp = tid / P, t = tid % P;
     const bool act = grp < nb;
     const int jj = k - 1 - (c0 + grp);  // ascending index
@@ -168,21 +177,23 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   }
 
   // ------------------------------------------------------------ twisted-factorisation vectors
+  t_ph[2] = clock64();
   const int cv1 = c1 < r ? c1 : r;  // vectors only for kept eigenvalues
   const int nv = cv1 - c0;
   if (tid < 2 * nv) {
     const unsigned msk = __activemask();
     const int c = c0 + (tid >> 1), side = tid & 1;
     const double lm = lam_s[tid >> 1];
-    double* Dp = es.dp() + (size_t)c * SMALL_K_MAX;
-    double* Dm = es.dm() + (size_t)c * SMALL_K_MAX;
+    // FK <= 96: the twisted-factorisation arrays live in shared memory behind the reflectors
+    double* Dp = FK <= 96 ? R + k * ld + (tid >> 1) * FK : es.dp() + (size_t)c * SMALL_K_MAX;
+    double* Dm = FK <= 96 ? R + k * ld + (MAXE + (tid >> 1)) * FK : es.dm() + (size_t)c * SMALL_K_MAX;
     const double pivmin = 1e-290;
     if (side == 0) {
       double x = d[0] - lm;
       if (fabs(x) < pivmin) x = -pivmin;
       Dp[0] = x;
       for (int i = 1; i < k; ++i) {
-        x = (d[i] - lm) - e2[i - 1] / x;
+        x = (d[i] - lm) - e2[i - 1] * frcp(x);
         if (fabs(x) < pivmin) x = -pivmin;
         Dp[i] = x;
       }
@@ -191,7 +202,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
       if (fabs(x) < pivmin) x = -pivmin;
       Dm[k - 1] = x;
       for (int i = k - 2; i >= 0; --i) {
-        x = (d[i] - lm) - e2[i] / x;
+        x = (d[i] - lm) - e2[i] * frcp(x);
         if (fabs(x) < pivmin) x = -pivmin;
         Dm[i] = x;
       }
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
     if (ob < best || (ob == best && ot < tw)) { best = ob; tw = ot; }
     double nrm2 = 0.0;
     if (side == 0) {
-      for (int i = 0; i < tw; ++i) Dp[i] = -e[i] / Dp[i];
+      for (int i = 0; i < tw; ++i) Dp[i] = -e[i] * frcp(Dp[i]);
       double zi = 1.0;
       for (int i = tw - 1; i >= 0; --i) {
         zi *= Dp[i];
@@ -218,7 +229,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
         Dp[i] = zi;
       }
     } else {
-      for (int i = tw + 1; i < k; ++i) Dm[i] = -e[i - 1] / Dm[i];
+      for (int i = tw + 1; i < k; ++i) Dm[i] = -e[i - 1] * frcp(Dm[i]);
       double zi = 1.0;
       for (int i = tw + 1; i < k; ++i) {
         zi *= Dm[i];
@@ -238,9 +249,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   __syncthreads();
 
   // ------------------------------------------------------------ W = Q Z, one warp per column
+  t_ph[3] = clock64();
   for (int cc = warp; cc < nv; cc += NW) {
     const int c = c0 + cc;
-    const double* zsrc = es.dp() + (size_t)c * SMALL_K_MAX;
+    const double* zsrc = FK <= 96 ? R + k * ld + cc * FK : es.dp() + (size_t)c * SMALL_K_MAX;
     double z[RCH];
 #pragma unroll
     for (int u = 0; u < RCH; ++u) {
@@ -269,6 +281,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
       if (i < k) a.Tm[i + (size_t)c * a.ldt] = z[u] * f;
     }
   }
+  __syncthreads();
+  t_ph[4] = clock64();
+  if (blockIdx.x == 0 && tid == 0 && a.stats)  // phase cycles (tools/eig_split_probe.py)
+    for (int q = 0; q < 4; ++q) a.stats[10 + q] = (double)(t_ph[q + 1] - t_ph[q]);
 }
 
 template <int FK>
@@ -365,7 +381,8 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
   if (smem < floor_b) smem = floor_b;
   static bool attr = false;
   if (!attr) {
-    const int mx = (int)(need_max > floor_b ? need_max : floor_b);
+    int mx = (int)(need_max > floor_b ? need_max : floor_b);
+    if (FK <= 96) mx += (int)(sizeof(double) * 2 * ((FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1) * FK);
     DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_vec_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_fin_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -373,7 +390,9 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
   }
   eig_tri_kernel<FK><<<1, ENT, smem, st>>>(a);
   DME_KCHECK();
-  eig_vec_kernel<FK><<<EIG_SPLIT_CTAS, ENT, smem, st>>>(a);
+  constexpr int MAXE = (FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1;
+  const size_t vsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * MAXE * FK) : smem;
+  eig_vec_kernel<FK><<<EIG_SPLIT_CTAS, ENT, vsmem > smem ? vsmem : smem, st>>>(a);
   DME_KCHECK();
   eig_fin_kernel<FK><<<1, ENT, smem, st>>>(a);
   DME_KCHECK();
