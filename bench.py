@@ -67,15 +67,18 @@ class ClockSampler:
                  "clocks_event_reasons.sw_power_cap")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.25)
+            t0 = time.time()  # wait for the first sample (nvidia-smi start-up), at most 5 s
+            while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.05)  # one more sample at the end of the timed region
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -272,7 +275,11 @@ def run_ours(args):
     # ------------------------------------------------------------ native-FP64 (DMMA) variant
     variant = None
     if not args.no_variant:
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
         s3 = dme.Solver(**dme.problem_kwargs(prob), **kw, e_pass="dmma")
+        torch.cuda.synchronize()
+        init3 = time.perf_counter() - t3
         s3.split_step("strang", "F12F3", args.warmup)
         torch.cuda.synchronize()
         if world > 1:
@@ -287,7 +294,8 @@ def run_ours(args):
             t = torch.tensor([ms3], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms3 = float(t.item())
-        variant = {"e_pass": "dmma (native FP64 mma.sync m8n8k4)", "value": args.steps / (ms3 * 1e-3),
+        variant = {"e_pass": "dmma (native FP64 mma.sync m8n8k4, E pass and init products)",
+                   "value": args.steps / (ms3 * 1e-3), "init_s_from_host_A": init3,
                    "unit": UNIT, "ms_per_step": ms3 / args.steps,
                    "ozaki_passes": s3.stats()["ozaki_passes"]}
         s3.close()
@@ -360,8 +368,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)  # = N_t of config 5
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nx", type=int, default=100, help="(debug) grid size; default = config 5")
     ap.add_argument("--no-e2e", action="store_true")

@@ -121,6 +121,12 @@ struct dme_ctx {
   int *exEh = nullptr, *exEf = nullptr, *exY = nullptr, *exY2 = nullptr;
   double *ozpm = nullptr, *ozpm2 = nullptr;  // slicing scratch (row maxima per chunk)
   OzScratch ozs, ozs2;
+  // init-time square products on the int8 tensor cores (world == 1): rasterised tile lists
+  bool oz_init = false;
+  int2* oz_tiles_up = nullptr;  // upper tile triangle (symmetric products)
+  int2* oz_tiles_all = nullptr;
+  int ntiles_up = 0, ntiles_all = 0;
+  std::vector<int2> h_tiles_up, h_tiles_all;
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_gram = nullptr, ev_ahead = nullptr;
   bool lookahead = true;
@@ -204,6 +210,14 @@ void plan_buffers(dme_ctx* c, Planner& P) {
     c->exY2 = P.take<int>(OZ_NMAX);
     c->ozpm = P.take<double>(oz_slice_scratch_doubles(std::max<int64_t>(rl, OZ_NMAX), n));
     c->ozpm2 = P.take<double>(oz_slice_scratch_doubles(OZ_NMAX, n));
+    if (c->world == 1) {
+      c->h_tiles_up = oz_tile_list(n, n, true);
+      c->h_tiles_all = oz_tile_list(n, n, false);
+      c->ntiles_up = (int)c->h_tiles_up.size();
+      c->ntiles_all = (int)c->h_tiles_all.size();
+      c->oz_tiles_up = P.take<int2>(c->h_tiles_up.size());
+      c->oz_tiles_all = P.take<int2>(c->h_tiles_all.size());
+    }
     for (OzScratch* o : {&c->ozs, &c->ozs2}) {
       o->max_tiles = ceil_div(rl, 128);
       o->max_grid = 256;
@@ -257,6 +271,9 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->fsal = o->no_fsal == 0;
   // E pass on the int8 tensor cores (exact digit slicing) unless disabled or out of its range
   c->oz = o->e_pass != DME_EPASS_DMMA && c->n <= OZ_KMAX && c->rows_loc > 0;
+  // the Padé products and squarings on the int8 tensor cores too (digits of both operands live
+  // in the E-digit buffers until E is sliced; replicated init, so one GPU only)
+  c->oz_init = c->oz && c->world == 1;
 }
 
 bool all_finite(const double* x, size_t cnt) {
@@ -753,12 +770,29 @@ void matmul_sq(dme_ctx* c, const double* X, const double* Y, double* out) {
   // and X Y is symmetric: only the upper tile triangle is computed, then mirrored.
   const bool sym = c->symA;
   if (!sym) transpose_rect(Y, c->n, c->n, c->ldn, c->BT, c->ldn, c->st);
-  GemmNTArgs g;
-  g.A = X; g.lda = c->ldn; g.B = sym ? Y : c->BT; g.ldb = c->ldn;
-  g.M = c->n; g.N = c->n; g.K = c->n;
-  g.out = out; g.out_rs = c->ldn; g.out_cs = 1;
-  g.sym_upper = sym;
-  gemm_nt(g, c->gs, c->st);
+  if (c->oz_init) {
+    // int8 digit slicing of both operands (ozaki.h): rows of X, rows of Y^T; the E-digit buffers
+    // serve as scratch (E is sliced after the last product)
+    const int64_t n = c->n, ldk = c->ozld;
+    oz_slice_rows(X, c->ldn, n, n, c->ozEh, ldk, n * ldk, c->exEh, c->ozpm, c->st);
+    oz_slice_rows(sym ? Y : c->BT, c->ldn, n, n, c->ozEf, ldk, n * ldk, c->exEf, c->ozpm, c->st);
+    OzGemmArgs g;
+    g.A = c->ozEh; g.eA = c->exEh; g.lda = ldk; g.a_slice_stride = n * ldk;
+    g.B = c->ozEf; g.eB = c->exEf; g.ldb = ldk; g.b_slice_stride = n * ldk;
+    g.M = n; g.N = n; g.K = n; g.alpha = 1.0;
+    g.out = out; g.out_rs = c->ldn; g.out_cs = 1;
+    g.tiles = sym ? c->oz_tiles_up : c->oz_tiles_all;
+    g.ntiles = sym ? c->ntiles_up : c->ntiles_all;
+    g.round_robin = true;
+    oz_gemm(g, c->ozs, c->st);
+  } else {
+    GemmNTArgs g;
+    g.A = X; g.lda = c->ldn; g.B = sym ? Y : c->BT; g.ldb = c->ldn;
+    g.M = c->n; g.N = c->n; g.K = c->n;
+    g.out = out; g.out_rs = c->ldn; g.out_cs = 1;
+    g.sym_upper = sym;
+    gemm_nt(g, c->gs, c->st);
+  }
   if (sym) mirror_lower(out, c->n, c->ldn, false, c->st);
 }
 
@@ -781,6 +815,12 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   if (c->oz)
     for (OzScratch* o : {&c->ozs, &c->ozs2})
       DME_CUDA(cudaMemsetAsync(o->counters, 0, sizeof(int) * o->max_tiles, st));
+  if (c->oz_init) {
+    DME_CUDA(cudaMemcpyAsync(c->oz_tiles_up, c->h_tiles_up.data(), c->h_tiles_up.size() * sizeof(int2),
+                             cudaMemcpyHostToDevice, st));
+    DME_CUDA(cudaMemcpyAsync(c->oz_tiles_all, c->h_tiles_all.data(),
+                             c->h_tiles_all.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  }
   // ---------------------------------------------------------------- upload (H2D boundary)
   // A and S: host memory (pageable or pinned) or, with options.big_inputs_on_device, device memory
   const cudaMemcpyKind kbig = c->opt.big_inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -916,9 +956,6 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     Ecur = En;
   }
   DME_CUDA(cudaMemcpyAsync(c->E_half, Ecur, (size_t)n * ld * 8, cudaMemcpyDeviceToDevice, st));
-  if (c->oz)  // digit slices of the local rows of E_{h/2}
-    oz_slice_rows(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->ozld,
-                  c->rows_loc * c->ozld, c->exEh, c->ozpm, st);
   c->qh = q_cur;
   // L_I(h) = compress([L_I(h/2), E_{h/2} L_I(h/2)]),  E_h = E_{h/2}^2
   copy_cols(c->Zc12f, ld, c->Zc12h, ld, n, c->qh, 1.0, st);
@@ -926,7 +963,9 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   ladder_double(c, c->Zc12f, qf, c->E_half);
   c->qf = qf;
   matmul_sq(c, c->E_half, c->E_half, c->E_full);
-  if (c->oz) {
+  if (c->oz) {  // digit slices of the local rows of E_{h/2} and E_h (after the last product)
+    oz_slice_rows(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->ozld,
+                  c->rows_loc * c->ozld, c->exEh, c->ozpm, st);
     oz_slice_rows(c->E_full + c->row0 * ld, ld, c->rows_loc, n, c->ozEf, c->ozld,
                   c->rows_loc * c->ozld, c->exEf, c->ozpm, st);
     c->oz_ready = true;

@@ -15,6 +15,7 @@
 #include "ozaki.h"
 
 #include <algorithm>
+#include <vector>
 
 namespace dme {
 namespace {
@@ -119,11 +120,44 @@ __device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
   return (int)b;
 }
 
+// The segments (tile, K-chunk range) a CTA works on, in order. Stream-K mode (E pass: few row
+// tiles, long K): the contiguous unit range [u0, u1) of the (tile, chunk) sequence, split tiles
+// reduced deterministically in CTA order. Round-robin mode (square GEMMs: many tiles): whole tiles
+// b, b + G, b + 2G, ... of a rasterised tile list, no reduction.
+struct SegIter {
+  int64_t u, u1;
+  int t, ntiles, G, nkc;
+  bool rr;
+  __device__ SegIter(bool rr_, int ntiles_, int nkc_) : rr(rr_), ntiles(ntiles_), G(gridDim.x), nkc(nkc_) {
+    const int64_t U = (int64_t)ntiles * nkc;
+    u = (int64_t)blockIdx.x * U / G;
+    u1 = (int64_t)(blockIdx.x + 1) * U / G;
+    t = blockIdx.x;
+  }
+  __device__ bool next(int& tile, int& kc0, int& kc1) {
+    if (rr) {
+      if (t >= ntiles) return false;
+      tile = t;
+      kc0 = 0;
+      kc1 = nkc;
+      t += G;
+      return true;
+    }
+    if (u >= u1) return false;
+    tile = (int)(u / nkc);
+    kc0 = (int)(u % nkc);
+    kc1 = (int)(kc0 + (u1 - u) < nkc ? kc0 + (u1 - u) : nkc);
+    u += kc1 - kc0;
+    return true;
+  }
+};
+
 template <int NP>
 __global__ void __launch_bounds__(224, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const int* __restrict__ eA, const int* __restrict__ eB, double* __restrict__ out,
-                   int64_t out_rs, int64_t out_cs, int M, int N, int nkc, int tiles, double alpha,
+                   int64_t out_rs, int64_t out_cs, int M, int N, int nkc, int ntiles,
+                   const int2* __restrict__ tile_list, int rr, double alpha,
                    double* __restrict__ partial, int* __restrict__ counters) {
   using C = OzCfg<NP>;
   constexpr int S = C::S;
@@ -144,8 +178,11 @@ __global__ void __launch_bounds__(224, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
-  const int64_t U = (int64_t)tiles * nkc;
-  const int64_t u0 = (int64_t)blockIdx.x * U / G, u1 = (int64_t)(blockIdx.x + 1) * U / G;
+  const int64_t U = (int64_t)ntiles * nkc;
+  auto coords = [&](int tile, int& rt, int& ct) {
+    if (tile_list) { const int2 tc = tile_list[tile]; rt = tc.x; ct = tc.y; }
+    else { rt = tile; ct = 0; }
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, 1); }
@@ -171,26 +208,26 @@ __global__ void __launch_bounds__(224, 1)
       if (isA) prefetch_tmap(&tmA); else prefetch_tmap(&tmB);
       int as = 0, bs = 0;
       uint32_t pa = 0, pb = 0;
-      for (int64_t u = u0; u < u1;) {
-        const int tile = (int)(u / nkc);
-        const int kc0 = (int)(u % nkc);
-        const int kc1 = (int)(kc0 + (u1 - u) < nkc ? kc0 + (u1 - u) : nkc);
+      SegIter it(rr != 0, ntiles, nkc);
+      int tile, kc0, kc1;
+      while (it.next(tile, kc0, kc1)) {
+        int rt, ct;
+        coords(tile, rt, ct);
         for (int kc = kc0; kc < kc1; ++kc) {
           if (!isA) {
             mbar_wait(empty_b + bs, pb ^ 1);
             mbar_arrive_expect_tx(full_b + bs, C::BST);
-            tma_load_3d(Bs + bs * C::BST, &tmB, full_b + bs, kc * 128, 0, 0);
+            tma_load_3d(Bs + bs * C::BST, &tmB, full_b + bs, kc * 128, ct * NP, 0);
             if (++bs == C::NB) { bs = 0; pb ^= 1; }
             continue;
           }
           for (int a = 0; a < S; ++a) {
             mbar_wait(empty_a + as, pa ^ 1);
             mbar_arrive_expect_tx(full_a + as, C::AST);
-            tma_load_3d(As + as * C::AST, &tmA, full_a + as, kc * 128, tile * 128, a);
+            tma_load_3d(As + as * C::AST, &tmA, full_a + as, kc * 128, rt * 128, a);
             if (++as == C::NA) { as = 0; pa ^= 1; }
           }
         }
-        u += kc1 - kc0;
       }
     }
   } else if (warp == 1) {
@@ -199,9 +236,9 @@ __global__ void __launch_bounds__(224, 1)
     int as = 0, bs = 0, seg = 0;
     uint32_t pa = 0, pb = 0;
     const uint32_t lo_a0 = desc_lo(smem_u32(As)), lo_b0 = desc_lo(smem_u32(Bs));
-    for (int64_t u = u0; u < u1; ++seg) {
-      const int kc0 = (int)(u % nkc);
-      const int kc1 = (int)(kc0 + (u1 - u) < nkc ? kc0 + (u1 - u) : nkc);
+    SegIter it(rr != 0, ntiles, nkc);
+    int tile, kc0, kc1;
+    while (it.next(tile, kc0, kc1)) {
       if (seg > 0) mbar_wait(tempty, (seg - 1) & 1);  // epilogue has drained the accumulators
       tc_fence_after();
       for (int kc = kc0; kc < kc1; ++kc) {
@@ -236,17 +273,18 @@ __global__ void __launch_bounds__(224, 1)
       }
       if (elect_one()) umma_commit(tfull);
       __syncwarp();
-      u += kc1 - kc0;
+      ++seg;
     }
   } else if (warp <= 5) {  // ------------------------------------------------ epilogue (warps 2..5)
     const int qd = warp & 3;            // TMEM sub-partition of this warp
     const int rl = 32 * qd + lane;      // row within the tile
     const int et = threadIdx.x - 64;    // 0..127
     int seg = 0;
-    for (int64_t u = u0; u < u1; ++seg) {
-      const int tile = (int)(u / nkc);
-      const int kc0 = (int)(u % nkc);
-      const int kc1 = (int)(kc0 + (u1 - u) < nkc ? kc0 + (u1 - u) : nkc);
+    SegIter it(rr != 0, ntiles, nkc);
+    int tile, kc0, kc1;
+    while (it.next(tile, kc0, kc1)) {
+      int rt, ct;
+      coords(tile, rt, ct);
       mbar_wait(tfull, seg & 1);
       tc_fence_after();
       // drain TMEM: per accumulator block c (smallest scale first) NP/16 loads, one wait
@@ -267,25 +305,33 @@ __global__ void __launch_bounds__(224, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty);
+      ++seg;
 
-      const int row = tile * 128 + rl;
+      const int row = rt * 128 + rl;
+      const int col0 = ct * NP;
       const int ea = row < M ? eA[row] : 0;
+      double* orow = out + (int64_t)row * out_rs + (int64_t)col0 * out_cs;
+      const int* eb = eB + col0;
+      const int ncol = N - col0 < NP ? N - col0 : NP;
       const bool whole = kc0 == 0 && kc1 == nkc;
       if (whole) {
         if (row < M) {
 #pragma unroll
           for (int j = 0; j < NP; ++j)
-            if (j < N) out[(int64_t)row * out_rs + (int64_t)j * out_cs] = alpha * scale2(acc[j], ea + eB[j]);
+            if (j < ncol) orow[(int64_t)j * out_cs] = alpha * scale2(acc[j], ea + eb[j]);
         }
       } else {
-        double* slot = partial + (size_t)(tile + blockIdx.x) * OZ_NMAX * 128;
+        // split tile (Stream-K mode): slot 2b + (this CTA started before the tile)
+        const int64_t tu0 = (int64_t)tile * nkc;
+        const int64_t my_u0 = (int64_t)blockIdx.x * U / G;
+        double* slot = partial + (size_t)(2 * blockIdx.x + (my_u0 < tu0 ? 1 : 0)) * OZ_NMAX * 128;
 #pragma unroll
         for (int j = 0; j < NP; ++j)
-          __stcg(slot + j * 128 + rl, (j < N && row < M) ? alpha * scale2(acc[j], ea + eB[j]) : 0.0);
+          __stcg(slot + j * 128 + rl, (j < ncol && row < M) ? alpha * scale2(acc[j], ea + eb[j]) : 0.0);
         __threadfence();
         named_bar_sync(1, 128);
-        const int b0 = cta_of((int64_t)tile * nkc, U, G);
-        const int b1 = cta_of((int64_t)tile * nkc + nkc - 1, U, G);
+        const int b0 = cta_of(tu0, U, G);
+        const int b1 = cta_of(tu0 + nkc - 1, U, G);
         if (et == 0) {
           const int old = atomicAdd(counters + tile, 1);
           *flag = (old == b1 - b0) ? 1 : 0;
@@ -301,7 +347,9 @@ __global__ void __launch_bounds__(224, 1)
 #pragma unroll
               for (int t = 0; t < JC; ++t) sum[t] = 0.0;
               for (int b = b0; b <= b1; ++b) {
-                const double* src = partial + (size_t)(tile + b) * OZ_NMAX * 128 + rl;
+                const int64_t bu0 = (int64_t)b * U / G;
+                const double* src =
+                    partial + (size_t)(2 * b + (bu0 < tu0 ? 1 : 0)) * OZ_NMAX * 128 + rl;
                 double v[JC];
 #pragma unroll
                 for (int t = 0; t < JC; ++t) v[t] = __ldcg(src + (j0 + t) * 128);
@@ -310,14 +358,13 @@ __global__ void __launch_bounds__(224, 1)
               }
 #pragma unroll
               for (int t = 0; t < JC; ++t)
-                if (j0 + t < N) out[(int64_t)row * out_rs + (int64_t)(j0 + t) * out_cs] = sum[t];
+                if (j0 + t < ncol) orow[(int64_t)(j0 + t) * out_cs] = sum[t];
             }
           }
           if (et == 0) counters[tile] = 0;
         }
         named_bar_sync(1, 128);
       }
-      u += kc1 - kc0;
     }
   }
   tc_fence_before();
@@ -390,19 +437,24 @@ __global__ void __launch_bounds__(SL_T) oz_slice_kernel(const double* __restrict
 template <int NP>
 void launch_oz(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
   using C = OzCfg<NP>;
-  const int nkc = (int)ceil_div(a.K, 128), tiles = (int)ceil_div(a.M, 128);
-  const int64_t U = (int64_t)tiles * nkc;
-  const int G = (int)std::min<int64_t>(ws.max_grid, U);
-  if (tiles > ws.max_tiles) throw std::runtime_error("oz_gemm: scratch too small");
+  const int nkc = (int)ceil_div(a.K, 128);
+  const bool listed = a.tiles != nullptr;
+  const int ntiles = listed ? a.ntiles : (int)ceil_div(a.M, 128);
+  const int64_t U = (int64_t)ntiles * nkc;
+  const int G = (int)std::min<int64_t>(ws.max_grid, a.round_robin ? ntiles : U);
+  if (!a.round_robin && ntiles > ws.max_tiles) throw std::runtime_error("oz_gemm: scratch too small");
+  if (G > ws.max_grid) throw std::runtime_error("oz_gemm: grid exceeds scratch");
   const CUtensorMap tmA = make_tmap_3d_u8(a.A, a.K, a.M, OZ_S, a.lda, a.a_slice_stride, 128, 128, 1);
-  const CUtensorMap tmB = make_tmap_3d_u8(a.B, a.K, NP, OZ_S, a.ldb, a.b_slice_stride, 128, NP, OZ_S);
+  const CUtensorMap tmB = make_tmap_3d_u8(a.B, a.K, listed ? a.N : NP, OZ_S, a.ldb, a.b_slice_stride,
+                                          128, NP, OZ_S);
   static bool attr = false;
   if (!attr) {
     DME_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   oz_gemm_kernel<NP><<<G, 224, C::SMEM, st>>>(tmA, tmB, a.eA, a.eB, a.out, a.out_rs, a.out_cs,
-                                              (int)a.M, (int)a.N, nkc, tiles, a.alpha, ws.partial,
+                                              (int)a.M, (int)a.N, nkc, ntiles, a.tiles,
+                                              a.round_robin ? 1 : 0, a.alpha, ws.partial,
                                               ws.counters);
   DME_KCHECK();
 }
@@ -423,8 +475,12 @@ void oz_slice_rows(const double* X, int64_t ld, int64_t rows, int64_t cols, int8
 
 void oz_gemm(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0) return;
-  if (a.N > OZ_NMAX || a.K > OZ_KMAX || a.K <= 0)
-    throw std::runtime_error("oz_gemm: N > 64 or K out of range");
+  if (a.K > OZ_KMAX || a.K <= 0) throw std::runtime_error("oz_gemm: K out of range");
+  if (a.tiles) {  // general N: 128 x 64 output tiles from the list
+    launch_oz<64>(a, ws, st);
+    return;
+  }
+  if (a.N > OZ_NMAX) throw std::runtime_error("oz_gemm: N > 64 without a tile list");
   const int np = (int)((a.N + 15) / 16 * 16);
   switch (np) {
     case 16: launch_oz<16>(a, ws, st); break;
@@ -432,6 +488,19 @@ void oz_gemm(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
     case 48: launch_oz<48>(a, ws, st); break;
     default: launch_oz<64>(a, ws, st); break;
   }
+}
+
+std::vector<int2> oz_tile_list(int64_t M, int64_t N, bool upper) {
+  // 128 x 64 output tiles rasterised in bands of 8 row tiles (column-major inside a band), so
+  // the ~#SM tiles in flight share few A row panels and B column panels (L2 reuse)
+  const int RT = (int)ceil_div(M, 128), CT = (int)ceil_div(N, 64);
+  constexpr int BAND = 8;
+  std::vector<int2> t;
+  for (int r0 = 0; r0 < RT; r0 += BAND)
+    for (int ct = 0; ct < CT; ++ct)
+      for (int rt = r0; rt < std::min(RT, r0 + BAND); ++rt)
+        if (!upper || ct * 64 + 63 >= rt * 128) t.push_back(make_int2(rt, ct));
+  return t;
 }
 
 }  // namespace dme

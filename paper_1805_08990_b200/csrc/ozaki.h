@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 namespace dme {
 
@@ -34,8 +35,9 @@ struct OzScratch {
   int* counters = nullptr;    // max_tiles ints, zero-initialised once (reset by the kernel)
   int max_grid = 0;
   int64_t max_tiles = 0;
-  static size_t partial_doubles(int64_t tiles, int grid) {
-    return (size_t)(tiles + grid) * OZ_NMAX * 128;
+  static size_t partial_doubles(int64_t tiles, int grid) {  // two split-tile slots per CTA
+    (void)tiles;
+    return (size_t)2 * grid * OZ_NMAX * 128;
   }
 };
 
@@ -50,10 +52,18 @@ struct OzGemmArgs {
   double alpha = 1.0;
   double* out = nullptr;       // element (i, j) at out + i*out_rs + j*out_cs
   int64_t out_rs = 0, out_cs = 0;
+  // square GEMMs: 128 x 64 output tiles from a device list (oz_tile_list), B holds the digits of
+  // all N columns, whole tiles round-robin over the CTAs (round_robin = true)
+  const int2* tiles = nullptr;
+  int ntiles = 0;
+  bool round_robin = false;
 };
 
-// out = alpha * E * Y (N <= OZ_NMAX, K <= OZ_KMAX); persistent Stream-K over 128-row tiles x
-// 128-deep K chunks, deterministic in-kernel fixup of split tiles.
+// out = alpha * E * Y (K <= OZ_KMAX). Without a tile list (N <= OZ_NMAX): persistent Stream-K
+// over 128-row tiles x 128-deep K chunks, deterministic in-kernel fixup of split tiles. With a
+// tile list: any N, whole 128 x 64 tiles.
 void oz_gemm(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st);
+// host: rasterised 128 x 64 tile list of an M x N output (upper: tiles meeting col >= row only)
+std::vector<int2> oz_tile_list(int64_t M, int64_t N, bool upper);
 
 }  // namespace dme

@@ -42,9 +42,10 @@ def test_fullsize_expm_sampled(solver):
     for which, t in ((0, H / 2), (1, H)):
         E = solver.debug_get_exp(which)
         ref = exact.heat_expm_entries(NX, t, rows, cols)
-        scale = np.abs(np.diag(E)).max()
+        # normwise FP64 accuracy: ||E||_inf = 1 (heat semigroup); the int8 digit-sliced init
+        # products measure 4.8e-16 here, the FP64 DMMA products 1e-16
         err = np.abs(E[rows, cols] - ref).max()
-        assert err <= 1e-13 * scale, (which, err, scale)
+        assert err <= 2e-15 * np.abs(E).sum(axis=1).max(), (which, err)
         # symmetry of the symmetric-A path
         assert np.array_equal(E[rows, cols], E[cols, rows])
 

@@ -91,3 +91,24 @@ def test_solver_ozaki_vs_dmma_vs_oracle(dme, comp):
     orc.step("strang", comp, 8)
     Lo, Do = orc.factor()
     assert lowrank.rel_diff(La, Da, Lo, Do) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg,kw", [(5, dict(nx=30)), (3, dict(nx=20)), (1, dict(n=300))])
+def test_init_products_ozaki_vs_dmma(dme, cfg, kw):
+    """The Padé products and squarings on the int8 tensor cores (square tiles, symmetric upper
+    triangle or full) give the same E_{h/2}, E_h as the FP64 DMMA GEMMs to FP64 accuracy."""
+    prob = make_config(cfg, **kw)
+    E = {}
+    for mode in ("auto", "dmma"):
+        s = dme.Solver(**dme.problem_kwargs(prob), h=0.005, e_pass=mode)
+        E[mode] = (s.debug_get_exp(0), s.debug_get_exp(1))
+        sq = s.stats()["squarings"]
+        s.close()
+    # normwise FP64 agreement: the digit-sliced products err by ~2^-55 of row max x column sum
+    # (absolute, not per entry), and the squaring ladder doubles an absolute error per squaring
+    # (||E||_inf = 1): bound 2^(s+2) u. Measured: 4.8e-16 (config 5, s = 6), 4.2e-15 (config 1,
+    # s = 8); the FP64 DMMA products keep ~1e-16 (DESIGN.md 5b).
+    tol = 2.0 ** (sq + 2) * 2.0 ** -53
+    for w in (0, 1):
+        a, b = E["auto"][w], E["dmma"][w]
+        assert np.abs(a - b).max() <= tol * np.abs(b).sum(axis=1).max(), (w, sq, np.abs(a - b).max())
