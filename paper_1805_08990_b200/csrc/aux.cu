@@ -1,5 +1,7 @@
 // Element-wise / reduction / tall-times-small kernels of the DME path.
 #include "aux.h"
+
+#include <algorithm>
 #include "common.cuh"
 #include "gemm_nt.h"
 
@@ -285,6 +287,110 @@ void rowmajor_to_colmajor(double* dst, int64_t ldd, const double* src, int64_t l
                           int64_t cols, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return;
   rowmajor_to_colmajor_kernel<<<grid_for(rows * cols), 256, 0, st>>>(dst, ldd, src, lds, rows, cols);
+  DME_KCHECK();
+}
+
+// CTA b owns the columns j of its slice of [0, r): it stages Gh[:, LA] (rows x kp) and Tm in
+// shared memory, forms F[:, j] = Gh[:, LA] Tm[:, j] for all q + m + kp rows, then writes G12 /
+// G21, H2 and G22[i, j] = G22[j, i] (i <= j) for its j; CTA 0 also copies G11 and H1. Launched on
+// CONG_CTAS CTAs: it must fit beside the look-ahead E pass (#SM - 8 persistent CTAs).
+constexpr int CONG_CTAS = 8;
+__global__ void __launch_bounds__(512) gram_congruence_kernel(const double* __restrict__ Gh,
+                                                              int64_t ldh, int q, int m, int kp,
+                                                              const double* __restrict__ Tm,
+                                                              int64_t ldt, int r, double* G,
+                                                              int64_t ldg) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int rows = q + m + kp, la = q + m, k = q + r;
+  const int j0 = (int)((int64_t)blockIdx.x * r / gridDim.x);
+  const int j1 = (int)((int64_t)(blockIdx.x + 1) * r / gridDim.x);
+  const int nj = j1 - j0;
+  if (blockIdx.x == 0) {
+    for (int e = tid; e < q * q; e += nt) {
+      const int i = e % q, jj = e / q;
+      G[i + (size_t)jj * ldg] = Gh[i + (size_t)jj * ldh];
+    }
+    for (int e = tid; e < q * m; e += nt) {
+      const int i = e % q, mu = e / q;
+      G[i + (size_t)(k + mu) * ldg] = Gh[i + (size_t)(q + mu) * ldh];
+    }
+  }
+  if (nj <= 0) return;
+  double* Gs = sm;                        // rows x kp, column-major (ld rows)
+  double* T = Gs + (size_t)rows * kp;     // kp x r, column-major (ld kp)
+  double* F = T + (size_t)kp * r;         // rows x nj, column-major (ld rows)
+  for (int e = tid; e < rows * kp; e += nt) {
+    const int i = e % rows, l = e / rows;
+    Gs[e] = Gh[i + (size_t)(la + l) * ldh];
+  }
+  for (int e = tid; e < kp * r; e += nt) T[e] = Tm[(e % kp) + (size_t)(e / kp) * ldt];
+  __syncthreads();
+  for (int e = tid; e < rows * nj; e += nt) {
+    const int i = e % rows, jj = e / rows;
+    const double* t = T + (size_t)(j0 + jj) * kp;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int l = 0;
+    for (; l + 3 < kp; l += 4) {
+      s0 = fma(Gs[i + (size_t)l * rows], t[l], s0);
+      s1 = fma(Gs[i + (size_t)(l + 1) * rows], t[l + 1], s1);
+      s2 = fma(Gs[i + (size_t)(l + 2) * rows], t[l + 2], s2);
+      s3 = fma(Gs[i + (size_t)(l + 3) * rows], t[l + 3], s3);
+    }
+    for (; l < kp; ++l) s0 = fma(Gs[i + (size_t)l * rows], t[l], s0);
+    F[i + (size_t)jj * rows] = (s0 + s1) + (s2 + s3);
+  }
+  __syncthreads();
+  for (int e = tid; e < q * nj; e += nt) {  // G12 / G21
+    const int i = e % q, jj = e / q;
+    const double v = F[i + (size_t)jj * rows];
+    G[i + (size_t)(q + j0 + jj) * ldg] = v;
+    G[(q + j0 + jj) + (size_t)i * ldg] = v;
+  }
+  for (int e = tid; e < m * nj; e += nt) {  // H2
+    const int mu = e % m, jj = e / m;
+    G[(q + j0 + jj) + (size_t)(k + mu) * ldg] = F[(q + mu) + (size_t)jj * rows];
+  }
+  for (int e = tid; e < r * nj; e += nt) {  // G22[i, j] for i <= j, mirrored
+    const int i = e % r, jj = e / r, j = j0 + jj;
+    if (i > j) continue;
+    const double* t = T + (size_t)i * kp;
+    const double* f = F + la + (size_t)jj * rows;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int l = 0;
+    for (; l + 3 < kp; l += 4) {
+      s0 = fma(t[l], f[l], s0);
+      s1 = fma(t[l + 1], f[l + 1], s1);
+      s2 = fma(t[l + 2], f[l + 2], s2);
+      s3 = fma(t[l + 3], f[l + 3], s3);
+    }
+    for (; l < kp; ++l) s0 = fma(t[l], f[l], s0);
+    const double v = (s0 + s1) + (s2 + s3);
+    G[(q + i) + (size_t)(q + j) * ldg] = v;
+    G[(q + j) + (size_t)(q + i) * ldg] = v;
+  }
+}
+
+size_t gram_congruence_smem(int q, int m, int kp, int r) {
+  const int rows = q + m + kp;
+  const int ctas = std::max(1, std::min(CONG_CTAS, r));
+  const int njmax = (r + ctas - 1) / ctas;
+  return sizeof(double) * ((size_t)rows * kp + (size_t)kp * r + (size_t)rows * njmax);
+}
+
+void gram_congruence(const double* Gh, int64_t ldh, int q, int m, int kp, const double* Tm,
+                     int64_t ldt, int r, double* G, int64_t ldg, cudaStream_t st) {
+  if (q + r <= 0) return;
+  const int ctas = std::max(1, std::min(CONG_CTAS, r));
+  const size_t smem = gram_congruence_smem(q, m, kp, r);
+  static bool attr = false;
+  if (!attr) {
+    DME_CUDA(cudaFuncSetAttribute(gram_congruence_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  220 * 1024));
+    attr = true;
+  }
+  if (smem > 220 * 1024) throw std::runtime_error("gram_congruence: too large");
+  gram_congruence_kernel<<<ctas, 512, smem, st>>>(Gh, ldh, q, m, kp, Tm, ldt, r, G, ldg);
   DME_KCHECK();
 }
 

@@ -1,5 +1,6 @@
 #pragma once
 #include <cuda_runtime.h>
+#include <cstddef>
 #include <cstdint>
 
 namespace dme {
@@ -29,5 +30,14 @@ void rowmajor_to_colmajor(double* dst, int64_t ldd, const double* src, int64_t l
 // C = A * B, A: M x K column-major, B: K x N column-major (small K, N), C: column-major
 void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                 int64_t M, int64_t N, int64_t K, cudaStream_t st);
+
+// Gram matrix of Zc' = [L_I | LA Tm] (and H = Zc'^T B) from the Gram Gh of GB = [L_I | B | LA]
+// (q, m, kp columns; ld ldh) and Tm (kp x r, ld ldt), without touching the n-row factors:
+//   G = [[Gh_II, Gh_I,LA Tm], [Tm^T Gh_LA,I, Tm^T Gh_LA,LA Tm]]  (k = q + r, column-major, ld ldg)
+//   H = [Gh_I,B; Tm^T Gh_LA,B]  stored at G + k * ldg  (k x m)
+// One CTA; kp, r <= 224, q + m + kp <= 224.
+size_t gram_congruence_smem(int q, int m, int kp, int r);  // <= 220 KB required
+void gram_congruence(const double* Gh, int64_t ldh, int q, int m, int kp, const double* Tm,
+                     int64_t ldt, int r, double* G, int64_t ldg, cudaStream_t st);
 
 }  // namespace dme

@@ -111,6 +111,9 @@ struct dme_ctx {
   double *G = nullptr, *H = nullptr, *Tm = nullptr, *Vg = nullptr, *Es = nullptr, *LRinv = nullptr, *sstats = nullptr;
   double *norm_dev = nullptr, *red_scratch = nullptr, *stage = nullptr;
   double *LA = nullptr;  // look-ahead operand [E_h L_I(h) | E_h Y]  (ldn x KMAX)
+  // Gram-congruence pipeline (run_f12f3_body): GB = [L_I(h) | B | E_h L_I(h) | E_h Y] (ldn x KMAX),
+  // its Gram Ghat (KMAX^2), double-buffered eigen-compression output Tm / Tm2
+  double *GB = nullptr, *Ghat = nullptr, *Tm2 = nullptr;
   int* r_dev = nullptr;
   GemmScratch gs, gs2;   // scratch of the main stream and of the look-ahead stream
   // int8 digit slices for the Ozaki E pass (ozaki.h): rows of E_{h/2} / E_h (local shard, sliced
@@ -128,7 +131,8 @@ struct dme_ctx {
   int ntiles_up = 0, ntiles_all = 0;
   std::vector<int2> h_tiles_up, h_tiles_all;
   cudaStream_t st2 = nullptr;
-  cudaEvent_t ev_gram = nullptr, ev_ahead = nullptr;
+  cudaEvent_t ev_gram = nullptr, ev_ahead = nullptr, ev_ghat = nullptr, ev_cong = nullptr,
+              ev_y = nullptr;
   bool lookahead = true;
   // init-only device buffers
   double *Aup = nullptr, *X0 = nullptr, *BT = nullptr, *X2 = nullptr, *X4 = nullptr, *X6 = nullptr;
@@ -157,6 +161,8 @@ struct dme_ctx {
     if (st2) cudaStreamDestroy(st2);
     if (ev_gram) cudaEventDestroy(ev_gram);
     if (ev_ahead) cudaEventDestroy(ev_ahead);
+    for (cudaEvent_t e : {ev_ghat, ev_cong, ev_y})
+      if (e) cudaEventDestroy(e);
     if (tl_base) cudaEventDestroy(tl_base);
   }
 };
@@ -196,6 +202,9 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   c->gs2.partial = P.take<double>(GemmScratch::partial_doubles(c->gs2.max_grid));
   c->gs2.counters = P.take<int>((size_t)c->gs2.max_tiles);
   c->LA = P.take<double>(fk);
+  c->GB = P.take<double>(fk);
+  c->Ghat = P.take<double>((size_t)KMAX * KMAX);
+  c->Tm2 = P.take<double>((size_t)KMAX * KMAX);
   if (c->oz) {
     c->ozld = oz_ldk(n);
     const int64_t rl = std::max<int64_t>(c->rows_loc, 1);
@@ -517,12 +526,16 @@ void epass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out,
 // factor, so G_ext = [Zc, B]^T [Zc, B] yields G and H = Zc^T B in one pass) and the small kernel.
 // Zc must have KMAX columns of capacity.
 void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bool do_compress,
-                     SmallArgs& a, bool& fast, cudaEvent_t after_gram = nullptr) {
+                     SmallArgs& a, bool& fast, cudaEvent_t after_gram = nullptr,
+                     double* Tm_out = nullptr, bool gram_ready = false) {
   DME_REQUIRE(k <= KMAX && (!t3 || k + c->m <= KMAX), DME_ERR_DIM,
               "factor width exceeds the small-system limit (224)");
   c->stats.compressions += do_compress ? 1 : 0;
   a = SmallArgs();
-  if (do_compress) {
+  if (gram_ready) {  // G (and H = G + k KMAX) assembled by the caller (gram_congruence)
+    DME_REQUIRE(do_compress && t3, DME_ERR_CONFIG, "assembled Gram path needs compress + T3");
+    a.H = c->G + k * KMAX;
+  } else if (do_compress) {
     const int64_t kk = t3 ? k + c->m : k;
     if (t3) {
       ProfScope pc(c, 4);
@@ -557,7 +570,7 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
   a.ldh = KMAX;
   a.LRinv = c->LRinv;
   a.tau = tau3;
-  a.Tm = c->Tm; a.ldt = KMAX;
+  a.Tm = Tm_out ? Tm_out : c->Tm; a.ldt = KMAX;
   a.V = c->Vg; a.ldv = KMAX;
   a.Es = c->Es;
   a.r_out = c->r_dev;
@@ -719,41 +732,94 @@ void run_sequence(dme_ctx* c, const std::vector<Op>& seq) {
   }
 }
 
-// Merged Strang F12F3 body [T12(h) with T3(h) fused] x nb, pipelined: the compression of step t
-// (Gram on all SMs, then the one-CTA eigen kernel) overlaps the look-ahead E pass of step t+1 on the
-// other SMs, using E_h Z_{t+1} = E_h (Zc_t Tm_t) = [E_h L_I(h) | E_h Y_t] Tm_t  (Y_t = E_h Z_t is
-// the factor part of Zc_t; E_h L_I(h) is precomputed at init). Exact reassociation of the same
-// products; only the last body step materialises the state Z.
+// Pipelined body of the merged Strang F12F3 steps: nb x [T12(h) T3(h)] (compression + fused T3).
+// Step t: Zc_t = [L_I(h) | Y_t], G_t = Zc_t^T Zc_t, eigen-compression -> Tm_t (k_t x r_t),
+// Z_t = Zc_t Tm_t, Y_{t+1} = E_h Z_t = [E_h L_I(h) | E_h Y_t] Tm_t = LA_t Tm_t.
+// The Gram of the next step is a congruence of a Gram that does not depend on Tm_t:
+//   GB_t = [L_I(h) | B | LA_t],  Ghat_t = GB_t^T GB_t,
+//   G_{t+1} = [[Ghat_II, Ghat_I,LA Tm_t], [Tm_t^T Ghat_LA,I, Tm_t^T Ghat_LA,LA Tm_t]], H likewise,
+// so the critical path is eigen-compression_t -> congruence (one small kernel) ->
+// eigen-compression_{t+1}, while the second stream runs Y_{t+1} = LA_t Tm_t (tall-small), the E pass
+// E_h Y_{t+1} and Ghat_{t+1} (n-row work) underneath. Exact reassociation of the same products
+// (rounding differs only); only the last step materialises the state Z.
 void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
   if (nb <= 0) return;
-  const int64_t ld = c->ldn, q = c->qf, n = c->n;
+  const int64_t ld = c->ldn, q = c->qf, n = c->n, m = c->m;
   double* Zc = c->Zc12f;
-  epass(c, c->E_full, c->Z, c->r, Zc + q * ld, ld, 1.0);
+  double* Tmb[2] = {c->Tm, c->Tm2};
+  epass(c, c->E_full, c->Z, c->r, Zc + q * ld, ld, 1.0);  // Y_0 = E_h Z
+  const int rc = (int)std::min<int64_t>(c->rank_cap, n);  // bound on every rank of the body
+  const bool pipe = c->lookahead && nb > 1 && 2 * q + m + rc <= KMAX &&
+                    gram_congruence_smem((int)q, (int)m, (int)(q + rc), rc) <= 220 * 1024;
+  int64_t r_prev = c->r;  // columns of Y_t
+  SmallArgs a;
+  bool fast = false;
+  // step 0: direct Gram of Zc_0 (main stream), eigen-compression 0
+  compress_launch(c, Zc, q + r_prev, true, h, true, a, fast, c->ev_gram, Tmb[0]);
+  if (pipe) {  // second stream: E_h Y_0 into GB, Ghat_0
+    DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_gram, 0));
+    epass_on(c, c->E_full, Zc + q * ld, r_prev, c->GB + (2 * q + m) * ld, ld, 1.0, c->st2, c->gs2);
+    GemmNTArgs g;
+    g.A = c->GB; g.lda = ld; g.B = c->GB; g.ldb = ld;
+    g.M = g.N = 2 * q + m + r_prev; g.K = n;
+    g.out = c->Ghat; g.out_rs = 1; g.out_cs = KMAX;
+    gemm_nt(g, c->gs2, c->st2);
+    DME_CUDA(cudaEventRecord(c->ev_ghat, c->st2));
+  }
+  int64_t rn = compress_finish(c, a, fast, true);
   for (int64_t it = 0; it < nb; ++it) {
-    const int64_t k = q + c->r;
-    const bool ahead = c->lookahead && it + 1 < nb;
-    SmallArgs a;
-    bool fast = false;
-    if (ahead) {
-      // the look-ahead pass starts once the Gram has been read (the eigen kernel needs 1 SM,
-      // the pass is launched on #SM - 1 persistent CTAs)
-      compress_launch(c, Zc, k, true, h, true, a, fast, c->ev_gram);
-      DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_gram, 0));
-      epass_on(c, c->E_full, Zc + q * ld, c->r, c->LA + q * ld, ld, 1.0, c->st2, c->gs2);
-      DME_CUDA(cudaEventRecord(c->ev_ahead, c->st2));
-    } else {
-      compress_launch(c, Zc, k, true, h, true, a, fast);
-    }
-    const int64_t rn = compress_finish(c, a, fast, true);
-    if (ahead) {
-      DME_CUDA(cudaStreamWaitEvent(c->st, c->ev_ahead, 0));
+    double* Tm_cur = Tmb[it & 1];
+    const int64_t kp = q + r_prev;  // columns of Zc_t = columns of LA_t
+    const bool last = it + 1 == nb;
+    if (!last && pipe) {
+      // critical path: congruence -> eigen-compression t+1
+      DME_CUDA(cudaStreamWaitEvent(c->st, c->ev_ghat, 0));
+      {
+        ProfScope ps(c, PROF_GRAM);
+        gram_congruence(c->Ghat, KMAX, (int)q, (int)m, (int)kp, Tm_cur, KMAX, (int)rn, c->G, KMAX,
+                        c->st);
+      }
+      DME_CUDA(cudaEventRecord(c->ev_cong, c->st));
+      SmallArgs an;
+      bool fastn = false;
+      compress_launch(c, Zc, q + rn, true, h, true, an, fastn, nullptr, Tmb[(it + 1) & 1], true);
+      // underneath: Y_{t+1} = LA_t Tm_t, E_h Y_{t+1}, Ghat_{t+1}
+      if (rn > 0) {
+        ProfScope ps(c, PROF_APPLY, 0, 0, c->st2);
+        tall_small(c->GB + (q + m) * ld, ld, Tm_cur, KMAX, Zc + q * ld, ld, n, rn, kp, c->st2);
+      }
+      if (it + 2 < nb) {  // Ghat_{t+1} is needed only if step t+2 exists
+        epass_on(c, c->E_full, Zc + q * ld, rn, c->GB + (2 * q + m) * ld, ld, 1.0, c->st2, c->gs2);
+        DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_cong, 0));
+        GemmNTArgs g;
+        g.A = c->GB; g.lda = ld; g.B = c->GB; g.ldb = ld;
+        g.M = g.N = 2 * q + m + rn; g.K = n;
+        g.out = c->Ghat; g.out_rs = 1; g.out_cs = KMAX;
+        gemm_nt(g, c->gs2, c->st2);
+        DME_CUDA(cudaEventRecord(c->ev_ghat, c->st2));
+      }
+      r_prev = rn;
+      rn = compress_finish(c, an, fastn, true);
+    } else if (!last) {  // no pipeline: Y_{t+1} = E_h (Zc_t Tm_t), direct Gram
       if (rn > 0) {
         ProfScope ps(c, PROF_APPLY);
-        tall_small(c->LA, ld, c->Tm, KMAX, Zc + q * ld, ld, n, rn, k, c->st);
+        tall_small(Zc, ld, Tm_cur, KMAX, c->Ztmp, ld, n, rn, kp, c->st);
       }
-    } else if (rn > 0) {
-      ProfScope ps(c, PROF_APPLY);
-      tall_small(Zc, ld, c->Tm, KMAX, c->Ztmp, ld, n, rn, k, c->st);
+      epass(c, c->E_full, c->Ztmp, rn, Zc + q * ld, ld, 1.0);
+      r_prev = rn;
+      SmallArgs an;
+      bool fastn = false;
+      compress_launch(c, Zc, q + rn, true, h, true, an, fastn, nullptr, Tmb[(it + 1) & 1]);
+      rn = compress_finish(c, an, fastn, true);
+    } else {  // last step: materialise Z = Zc_t Tm_t (Y_t was written on the second stream)
+      if (pipe) {
+        DME_CUDA(cudaEventRecord(c->ev_y, c->st2));
+        DME_CUDA(cudaStreamWaitEvent(c->st, c->ev_y, 0));
+      }
+      if (rn > 0) {
+        ProfScope ps(c, PROF_APPLY);
+        tall_small(Zc, ld, Tm_cur, KMAX, c->Ztmp, ld, n, rn, kp, c->st);
+      }
       swapZ(c);
     }
     c->r = rn;
@@ -763,7 +829,6 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
   }
 }
 
-// ------------------------------------------------------------------ init: expm + quadrature
 void matmul_sq(dme_ctx* c, const double* X, const double* Y, double* out) {
   // out = X * Y  (n x n row-major): B operand rows = columns of Y = rows of Y^T.
   // Symmetric A: every factor here is a polynomial in the symmetric X0 (or E = r(X0)), so Y^T = Y
@@ -972,6 +1037,12 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   }
   // look-ahead operand: E_h L_I(h) stays in the leading columns of LA
   epass(c, c->E_full, c->Zc12f, c->qf, c->LA, ld, 1.0);
+  // fixed columns of the congruence pipeline's GB = [L_I(h) | B | E_h L_I(h) | (E_h Y)]
+  if (c->m > 0 && 2 * c->qf + c->m <= KMAX) {
+    copy_cols(c->GB, ld, c->Zc12f, ld, n, c->qf, 1.0, st);
+    copy_cols(c->GB + c->qf * ld, ld, c->Bcol, ld, n, c->m, 1.0, st);
+    copy_cols(c->GB + (c->qf + c->m) * ld, ld, c->LA, ld, n, c->qf, 1.0, st);
+  }
   c->stats.q_half = c->qh;
   c->stats.q_full = c->qf;
 
@@ -1049,6 +1120,8 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     DME_CUDA(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, lo_pri));
     DME_CUDA(cudaEventCreateWithFlags(&c->ev_gram, cudaEventDisableTiming));
     DME_CUDA(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming));
+    for (cudaEvent_t* e : {&c->ev_ghat, &c->ev_cong, &c->ev_y})
+      DME_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     Planner sizing;
     plan_buffers(c, sizing);
     DME_REQUIRE(o->workspace && o->workspace_bytes >= sizing.off + 256, DME_ERR_CAPACITY,
