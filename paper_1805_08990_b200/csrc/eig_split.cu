@@ -302,47 +302,68 @@ __global__ void __launch_bounds__(ENT, 1) eig_fin_kernel(SmallArgs a) {
   const double scale = h[0], tmax = h[3];
   const int r = (int)h[4];
   const int nr = r < k ? r + 1 : r;
+  const long long f0 = clock64();
   for (int i = tid; i < nr; i += ENT) {
     lam[i] = es.lam()[i];
     slam[i] = sqrt(fabs(lam[i]));
   }
   __syncthreads();
-  for (int e_ = tid; e_ < k * r; e_ += ENT) {
-    const int i = e_ % k, c = e_ / k;
-    const double f = a.sqrt_scale ? sqrt(fmax(lam[c] * scale, 0.0)) : 1.0;
-    A[c * ld + i] = f > 0.0 ? a.Tm[i + (size_t)c * a.ldt] / f : 0.0;
+  if (a.sqrt_scale) {
+    for (int e_ = tid; e_ < k * r; e_ += ENT) {
+      const int i = e_ % k, c = e_ / k;
+      const double f = sqrt(fmax(lam[c] * scale, 0.0));
+      A[c * ld + i] = f > 0.0 ? a.Tm[i + (size_t)c * a.ldt] / f : 0.0;
+    }
+  } else {  // W = Tm as written by VEC
+    for (int e_ = tid; e_ < k * r; e_ += ENT) {
+      const int i = e_ % k, c = e_ / k;
+      A[c * ld + i] = a.Tm[i + (size_t)c * a.ldt];
+    }
   }
   __syncthreads();
-  constexpr int TB = 4;
+  const long long f1 = clock64();
+  // weighted orthogonality |W^T W - I| (4 x 4 blocks of the upper triangle; the k-long dots are
+  // split over KS lanes of a warp and combined by shuffles, so ~all 512 threads work)
+  constexpr int TB = 4, KS = 4;
   const int nbk = (r + TB - 1) / TB;
   double mx = 0.0;
-  for (int blk = tid; blk < nbk * nbk; blk += ENT) {
-    const int bi = blk % nbk, bj = blk / nbk;
-    if (bi > bj) continue;
+  const int nblk = nbk * (nbk + 1) / 2;
+  for (int base = warp * (32 / KS); base < nblk; base += NW * (32 / KS)) {
+    const int blk = base + lane / KS, ks = lane % KS;
+    int bi = 0, bj = 0;
+    if (blk < nblk) {  // blk -> (bi <= bj): row-major enumeration of the upper triangle
+      int rem = blk;
+      while (rem >= nbk - bi) { rem -= nbk - bi; ++bi; }
+      bj = bi + rem;
+    }
     double acc[TB][TB];
 #pragma unroll
     for (int x = 0; x < TB; ++x)
 #pragma unroll
       for (int y = 0; y < TB; ++y) acc[x][y] = 0.0;
-    for (int i = 0; i < k; ++i) {
-      double wa[TB], wb[TB];
+    if (blk < nblk) {
+      for (int i = ks; i < k; i += KS) {
+        double wa[TB], wb[TB];
 #pragma unroll
-      for (int x = 0; x < TB; ++x) {
-        const int c1 = bi * TB + x, c2 = bj * TB + x;
-        wa[x] = c1 < r ? A[c1 * ld + i] : 0.0;
-        wb[x] = c2 < r ? A[c2 * ld + i] : 0.0;
+        for (int x = 0; x < TB; ++x) {
+          const int c1 = bi * TB + x, c2 = bj * TB + x;
+          wa[x] = c1 < r ? A[c1 * ld + i] : 0.0;
+          wb[x] = c2 < r ? A[c2 * ld + i] : 0.0;
+        }
+#pragma unroll
+        for (int x = 0; x < TB; ++x)
+#pragma unroll
+          for (int y = 0; y < TB; ++y) acc[x][y] = fma(wa[x], wb[y], acc[x][y]);
       }
-#pragma unroll
-      for (int x = 0; x < TB; ++x)
-#pragma unroll
-        for (int y = 0; y < TB; ++y) acc[x][y] = fma(wa[x], wb[y], acc[x][y]);
     }
 #pragma unroll
     for (int x = 0; x < TB; ++x)
 #pragma unroll
       for (int y = 0; y < TB; ++y) {
+#pragma unroll
+        for (int o = 1; o < KS; o <<= 1) acc[x][y] += __shfl_xor_sync(0xffffffffu, acc[x][y], o);
         const int c1 = bi * TB + x, c2 = bj * TB + y;
-        if (c1 < r && c2 < r && c1 <= c2) {
+        if (blk < nblk && ks == 0 && c1 < r && c2 < r && c1 <= c2) {
           const double w = (c1 == c2) ? 1.0 : slam[c1] * slam[c2] / fmax(fabs(lam[0]), 1e-300);
           mx = fmax(mx, fabs(acc[x][y] - (c1 == c2 ? 1.0 : 0.0)) * w);
         }
@@ -369,8 +390,85 @@ __global__ void __launch_bounds__(ENT, 1) eig_fin_kernel(SmallArgs a) {
     if (tid == 0) *a.r_out = -1;  // caller falls back to the Jacobi kernel
     return;
   }
-  if (a.t3 && r > 0) smallk::t3_fuse(a, k, r, A, Gam, Phi);
-  if (tid == 0) *a.r_out = r;
+  const long long f2 = clock64();
+  if (a.t3 && r > 0) {
+    if constexpr (FK <= 96) {
+      // Riccati flow T3 on the compression output from shared memory (the generic t3_fuse reads
+      // Tm and H from global memory in k-long dependent loops): Tm = W (f = 1 unless
+      // sqrt_scale), K^{-1/2} = I + F g(F^T F) F^T, F = sqrt(tau) Tm^T H L_R^{-T}  (small.cu)
+      const int m = a.m;
+      double* Hs = A + (size_t)r * ld;        // k x m
+      double* Fs = Hs + (size_t)k * m;        // r x m
+      double* Us = Fs + (size_t)r * m;        // k x m
+      for (int e = tid; e < k * m; e += ENT) Hs[e] = a.H[(e % k) + (size_t)(e / k) * a.ldh];
+      for (int i = tid; i < r; i += ENT)
+        slam[i] = a.sqrt_scale ? sqrt(fmax(lam[i] * scale, 0.0)) : 1.0;
+      __syncthreads();
+      for (int e = tid; e < r * m; e += ENT) {  // Us[c, mu] <- (Tm^T H)[c, mu] (temporary)
+        const int c = e % r, mu = e / r;
+        const double* w = A + (size_t)c * ld;
+        const double* hh = Hs + (size_t)mu * k;
+        double s0 = 0.0, s1 = 0.0;
+        int i = 0;
+        for (; i + 1 < k; i += 2) { s0 = fma(w[i], hh[i], s0); s1 = fma(w[i + 1], hh[i + 1], s1); }
+        if (i < k) s0 = fma(w[i], hh[i], s0);
+        Us[c + (size_t)mu * r] = (s0 + s1) * slam[c];
+      }
+      __syncthreads();
+      for (int e = tid; e < r * m; e += ENT) {  // F = sqrt(tau) W Linv^T
+        const int c = e % r, mu = e / r;
+        double acc = 0.0;
+        for (int nu = 0; nu < m; ++nu) acc += Us[c + (size_t)nu * r] * a.LRinv[mu * m + nu];
+        Fs[c + (size_t)mu * r] = sqrt(a.tau) * acc;
+      }
+      __syncthreads();
+      if (tid < m * m) {  // Phi = F^T F
+        const int mu = tid / m, nu = tid % m;
+        double acc = 0.0;
+        for (int c = 0; c < r; ++c) acc += Fs[c + (size_t)mu * r] * Fs[c + (size_t)nu * r];
+        Phi[mu * m + nu] = acc;
+      }
+      __syncthreads();
+      if (tid == 0) {  // Gamma = g(Phi)
+        if (m == 1) {
+          const double sg = sqrt(1.0 + fmax(Phi[0], 0.0));
+          Gam[0] = -1.0 / (sg * (1.0 + sg));
+        } else {
+          smallk::tiny_sym_fun_g(Phi, Gam, m);
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < k * m; e += ENT) {  // U = Tm F Gamma  (k x m)
+        const int i = e % k, mu = e / k;
+        double u[SMALL_M_MAX];
+        for (int nu = 0; nu < m; ++nu) u[nu] = 0.0;
+        for (int c = 0; c < r; ++c) {
+          const double t = A[(size_t)c * ld + i] * slam[c];
+          for (int nu = 0; nu < m; ++nu) u[nu] = fma(t, Fs[c + (size_t)nu * r], u[nu]);
+        }
+        double acc = 0.0;
+        for (int nu = 0; nu < m; ++nu) acc += u[nu] * Gam[nu * m + mu];
+        Us[i + (size_t)mu * k] = acc;
+      }
+      __syncthreads();
+      for (int e = tid; e < k * r; e += ENT) {  // Tm += U F^T
+        const int i = e % k, c = e / k;
+        double acc = A[(size_t)c * ld + i] * slam[c];
+        for (int mu = 0; mu < m; ++mu) acc = fma(Us[i + (size_t)mu * k], Fs[c + (size_t)mu * r], acc);
+        a.Tm[i + (size_t)c * a.ldt] = acc;
+      }
+    } else {
+      smallk::t3_fuse(a, k, r, A, Gam, Phi);
+    }
+  }
+  if (tid == 0) {
+    *a.r_out = r;
+    if (a.stats) {  // phase cycles (tools/eig_split_probe.py)
+      a.stats[14] = (double)(f1 - f0);
+      a.stats[15] = (double)(f2 - f1);
+      a.stats[5] = (double)(clock64() - f2);
+    }
+  }
 }
 
 template <int FK>
@@ -394,7 +492,10 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
   const size_t vsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * MAXE * FK) : smem;
   eig_vec_kernel<FK><<<EIG_SPLIT_CTAS, ENT, vsmem > smem ? vsmem : smem, st>>>(a);
   DME_KCHECK();
-  eig_fin_kernel<FK><<<1, ENT, smem, st>>>(a);
+  const size_t fsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * (size_t)a.k * SMALL_M_MAX +
+                                                  (size_t)a.k * SMALL_M_MAX)
+                                 : smem;
+  eig_fin_kernel<FK><<<1, ENT, fsmem > smem ? fsmem : smem, st>>>(a);
   DME_KCHECK();
 }
 
