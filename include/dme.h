@@ -85,6 +85,14 @@ typedef struct {
   int64_t r0;         /* columns of L0 (0 => P0 = 0)                                        */
   const double* L0;   /* n x r0                                                             */
   const double* D0;   /* r0 x r0 symmetric positive semidefinite (NULL => identity)         */
+  const double* M;    /* n x n mass matrix or NULL (Example 4): the equation is
+                         M^T P' M = A^T P M + M^T P A + C^T C [- M^T P B R^-1 B^T P M]
+                         [+ M^T S P S^T M is NOT supported with M]; init cancels M once
+                         (P:L357-359): A <- A M^-1, C <- C M^-1 (dense LU without pivoting,
+                         P:L362 "compute and store a dense LU factorization"; M must admit
+                         it, e.g. SPD mass matrices; DME_ERR_NUMERIC on a tiny pivot).
+                         Same memory space as A (host, or device with big_inputs_on_device).
+                         Callers that zero-initialise the struct get M = NULL.              */
 } dme_problem;
 
 typedef struct {

@@ -25,6 +25,18 @@ COMPOSITIONS = {
 }
 
 
+def mass_transform(M, A, C):
+    """Example 4: cancelling M^T and M in
+        M^T P' M = A^T P M + M^T P A + Q - M^T P B R^-1 B^T P M
+    gives  P' = M^-T A^T P + P A M^-1 + M^-T Q M^-1 - P B R^-1 B^T P,  i.e. the standard DRE
+    with A replaced by A M^-1 (the displayed equation; the text's "M^-1 A" is the same
+    matrix when A and M are symmetric -- reading G23) and Q = C^T C by (C M^-1)^T (C M^-1).
+    B and R are unchanged. Returns (A M^-1, C M^-1)."""
+    At = np.linalg.solve(M.T, A.T).T            # A M^-1
+    Ct = None if C is None else np.linalg.solve(M.T, C.T).T   # C M^-1
+    return At, Ct
+
+
 def step_sequence(scheme, composition, h):
     """[(flow, tau), ...] in application order for one step."""
     fl = COMPOSITIONS[composition]
@@ -53,13 +65,17 @@ class OracleSolver:
         self.p = prob
         self.h = h
         self.o = opts
-        self.op = flows.Operator(prob.A, method, prob.heat_nx, prob.heat_dim, dense_apply)
+        A, C = prob.A, prob.C
+        if getattr(prob, "M", None) is not None:
+            A, C = mass_transform(prob.M, A, C)
+        self.A = A
+        self.op = flows.Operator(A, method, prob.heat_nx, prob.heat_dim, dense_apply)
         n = prob.n
-        if prob.C is not None and prob.C.shape[0] > 0:
-            self.LQ, self.DQ = prob.C.T.copy(), np.eye(prob.C.shape[0])   # Q = C^T C (G11)
+        if C is not None and C.shape[0] > 0:
+            self.LQ, self.DQ = C.T.copy(), np.eye(C.shape[0])   # Q = C^T C (G11)
         else:
             self.LQ, self.DQ = np.zeros((n, 0)), np.zeros((0, 0))
-        self.delta = quadrature.panel_width(prob.A, h, opts.quad_subpanels)
+        self.delta = quadrature.panel_width(A, h, opts.quad_subpanels)
         self._LI = {}
         # P0 is compressed when loaded (reading G10)
         L0 = prob.L0 if prob.L0 is not None else np.zeros((n, 0))

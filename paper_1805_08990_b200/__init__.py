@@ -37,7 +37,7 @@ _dp = ctypes.POINTER(ctypes.c_double)
 class _Problem(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("A", _dp), ("p", ctypes.c_int64), ("C", _dp),
                 ("m", ctypes.c_int64), ("B", _dp), ("R", _dp), ("S", _dp),
-                ("r0", ctypes.c_int64), ("L0", _dp), ("D0", _dp)]
+                ("r0", ctypes.c_int64), ("L0", _dp), ("D0", _dp), ("M", _dp)]
 
 
 class _Options(ctypes.Structure):
@@ -155,7 +155,8 @@ E_PASS = {"auto": 0, "dmma": 1}
 class Solver:
     """One problem on one GPU (or one rank of a row-sharded multi-GPU run)."""
 
-    def __init__(self, A, C=None, L0=None, D0=None, B=None, R=None, S=None, *, h, trunc_tol=1e-16,
+    def __init__(self, A, C=None, L0=None, D0=None, B=None, R=None, S=None, M=None, *, h,
+                 trunc_tol=1e-16,
                  rank_cap=0, quad_nodes=14, quad_subpanels=1, device=None, stream=None,
                  world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None, fsal=True,
                  e_pass="auto", poison_workspace=False):
@@ -173,19 +174,22 @@ class Solver:
             if S is not None and not (isinstance(S, torch.Tensor) and S.is_cuda and
                                       S.dtype == torch.float64 and S.is_contiguous()):
                 raise ValueError("with a device A, S must be a contiguous float64 CUDA tensor")
+            if M is not None and not (isinstance(M, torch.Tensor) and M.is_cuda and
+                                      M.dtype == torch.float64 and M.is_contiguous()):
+                raise ValueError("with a device A, M must be a contiguous float64 CUDA tensor")
             dptr = lambda t: None if t is None else ctypes.cast(t.data_ptr(), _dp)
-            self._keep = [A, _f64(C), _f64(B), _f64(R), S, _f64(L0), _f64(D0)]
-            A_, C_, B_, R_, S_, L0_, D0_ = self._keep
-            pA, pS = dptr(A_), dptr(S_)
+            self._keep = [A, _f64(C), _f64(B), _f64(R), S, _f64(L0), _f64(D0), M]
+            A_, C_, B_, R_, S_, L0_, D0_, M_ = self._keep
+            pA, pS, pM = dptr(A_), dptr(S_), dptr(M_)
         else:
-            self._keep = [_f64(A), _f64(C), _f64(B), _f64(R), _f64(S), _f64(L0), _f64(D0)]
-            A_, C_, B_, R_, S_, L0_, D0_ = self._keep
-            pA, pS = _ptr(A_), _ptr(S_)
+            self._keep = [_f64(A), _f64(C), _f64(B), _f64(R), _f64(S), _f64(L0), _f64(D0), _f64(M)]
+            A_, C_, B_, R_, S_, L0_, D0_, M_ = self._keep
+            pA, pS, pM = _ptr(A_), _ptr(S_), _ptr(M_)
         n = A_.shape[0]
         self.n = n
         pr = _Problem(n=n, A=pA, p=0 if C_ is None else C_.shape[0], C=_ptr(C_),
                       m=0 if B_ is None else B_.shape[1], B=_ptr(B_), R=_ptr(R_), S=pS,
-                      r0=0 if L0_ is None else L0_.shape[1], L0=_ptr(L0_), D0=_ptr(D0_))
+                      r0=0 if L0_ is None else L0_.shape[1], L0=_ptr(L0_), D0=_ptr(D0_), M=pM)
         self._pr = pr
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
         uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid is not None else None
@@ -293,4 +297,4 @@ def problem_kwargs(prob) -> dict:
     """workloads.Problem -> Solver keyword arguments (data only)."""
     return dict(A=prob.A, C=prob.C, L0=prob.L0 if prob.L0 is not None and prob.L0.shape[1] else None,
                 D0=prob.D0 if prob.L0 is not None and prob.L0.shape[1] else None, B=prob.B,
-                R=prob.R, S=prob.S)
+                R=prob.R, S=prob.S, M=getattr(prob, "M", None))

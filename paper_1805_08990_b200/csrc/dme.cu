@@ -314,6 +314,8 @@ void validate(const dme_problem* pr, const dme_options* o, bool dre) {
   // input finiteness (host scan; inputs are host arrays)
   const size_t nn = (size_t)pr->n * pr->n;
   (void)nn;  // A and S (n x n) are checked on the device after the upload (init_all)
+  DME_REQUIRE(!(pr->M && pr->S), DME_ERR_CONFIG,
+              "a mass matrix M together with the bilinear term S is not supported");
   if (pr->p) DME_REQUIRE(all_finite(pr->C, (size_t)pr->p * pr->n), DME_ERR_INVALID, "C non-finite");
   if (pr->r0) DME_REQUIRE(all_finite(pr->L0, (size_t)pr->n * pr->r0), DME_ERR_INVALID, "L0 non-finite");
   if (pr->m) {
@@ -892,6 +894,28 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, kbig, st));
   if (c->has_S)
     DME_CUDA(cudaMemcpy2DAsync(c->S, ld * 8, pr->S, n * 8, n * 8, n, kbig, st));
+  // mass matrix (Example 4): A <- A M^-1, C <- C M^-1 by a dense LU of M
+  const bool mass = pr->M != nullptr;
+  if (mass) {
+    int mflags[2] = {0, 0};
+    DME_CUDA(cudaMemcpy2DAsync(c->X4, ld * 8, pr->M, n * 8, n * 8, n, kbig, st));
+    DME_CUDA(cudaMemsetAsync(c->r_dev, 0, 2 * sizeof(int), st));
+    check_square(c->X4, n, ld, c->r_dev, st);
+    DME_CUDA(cudaMemcpyAsync(mflags, c->r_dev, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    sync(c);
+    DME_REQUIRE(mflags[0] == 0, DME_ERR_INVALID, "M has non-finite entries");
+    lu_nopiv_solve_right(c->X4, c->Aup, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 2);
+    double mp = 0;
+    DME_CUDA(cudaMemcpyAsync(&mp, c->norm_dev + 2, 8, cudaMemcpyDeviceToHost, st));
+    sync(c);
+    DME_REQUIRE(std::isfinite(mp) && mp > 0.0, DME_ERR_NUMERIC, "LU of M hit a zero pivot");
+    if (c->p > 0) {  // rows of [C; 0] (n x n) times M^-1
+      DME_CUDA(cudaMemcpy2DAsync(c->X4, ld * 8, pr->M, n * 8, n * 8, n, kbig, st));
+      DME_CUDA(cudaMemsetAsync(c->X6, 0, (size_t)n * ld * 8, st));
+      DME_CUDA(cudaMemcpy2DAsync(c->X6, ld * 8, pr->C, n * 8, n * 8, c->p, cudaMemcpyHostToDevice, st));
+      lu_nopiv_solve_right(c->X4, c->X6, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 2);
+    }
+  }
   // device-side validation of the big inputs: finiteness, and the exact symmetry of A that
   // enables the symmetric Padé products
   {
@@ -905,8 +929,12 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     DME_REQUIRE(flags_host[2] == 0, DME_ERR_INVALID, "S has non-finite entries");
     c->symA = flags_host[1] == 0;
   }
-  if (c->p > 0)  // C (p x n row-major): row i of C = column i of L_Q = C^T
-    DME_CUDA(cudaMemcpy2DAsync(c->LQ, ld * 8, pr->C, n * 8, n * 8, c->p, cudaMemcpyHostToDevice, st));
+  if (c->p > 0) {  // C (p x n row-major): row i of C = column i of L_Q = C^T
+    if (mass)
+      DME_CUDA(cudaMemcpy2DAsync(c->LQ, ld * 8, c->X6, ld * 8, n * 8, c->p, cudaMemcpyDeviceToDevice, st));
+    else
+      DME_CUDA(cudaMemcpy2DAsync(c->LQ, ld * 8, pr->C, n * 8, n * 8, c->p, cudaMemcpyHostToDevice, st));
+  }
   if (c->m > 0) {
     DME_CUDA(cudaMemcpyAsync(c->Wa, pr->B, n * c->m * 8, cudaMemcpyHostToDevice, st));
     rowmajor_to_colmajor(c->Bcol, ld, c->Wa, c->m, n, c->m, st);

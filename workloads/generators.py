@@ -42,6 +42,7 @@ class Problem:
     heat_nx: Optional[int] = None
     heat_dim: Optional[int] = None
     meta: dict = field(default_factory=dict)
+    M: Optional[np.ndarray] = None   # mass matrix of  M^T P' M = A^T P M + M^T P A + ...
 
     @property
     def n(self) -> int:
@@ -116,6 +117,55 @@ def stochastic_heat_matrices(nx: int):
     return A, B, S, C
 
 
+def fem2d_matrices(nx: int, conv: float = 0.0):
+    """Steel-cooling STRUCTURE (Example 4; the Oberwolfach data itself is not available):
+    P1 finite elements on the unit square, uniform grid of spacing 1/nx, every square split into two
+    triangles by its (0,0)-(1,1) diagonal; homogeneous Dirichlet on x = 0 and y = 0, Neumann on
+    x = 1 and y = 1 (unknowns: nodes (i, j), i, j = 1..nx, index (i-1) nx + (j-1)).
+    Returns (M, A, B, C): M consistent mass, A = -(stiffness) - conv * (x-derivative transport,
+    element-wise, nonsymmetric when conv != 0), B = boundary mass of the Neumann edge x = 1 (boundary
+    control, m = 1), C = 2 x n temperature differences between node pairs ("an operator that
+    measures temperature differences between different points")."""
+    n = nx * nx
+    hh = 1.0 / nx
+    M = np.zeros((n, n))
+    A = np.zeros((n, n))
+
+    def idx(i, j):
+        return (i - 1) * nx + (j - 1) if i >= 1 and j >= 1 else -1
+
+    Ke = 0.5 * np.array([[2.0, -1.0, -1.0], [-1.0, 1.0, 0.0], [-1.0, 0.0, 1.0]])  # right angle first
+    Me = hh * hh / 24.0 * np.array([[2.0, 1.0, 1.0], [1.0, 2.0, 1.0], [1.0, 1.0, 2.0]])
+    for i in range(nx):
+        for j in range(nx):
+            # lower triangle: right angle at (i+1, j), legs to (i, j) and (i+1, j+1)
+            # upper triangle: right angle at (i, j+1), legs to (i+1, j+1) and (i, j)
+            for tri, xs in (([(i + 1, j), (i, j), (i + 1, j + 1)], None),
+                            ([(i, j + 1), (i + 1, j + 1), (i, j)], None)):
+                g = [idx(a, b) for a, b in tri]
+                # transport c d/dx: element matrix int phi_a d(phi_b)/dx = (area/3) d(phi_b)/dx
+                xb = np.array([a for a, _ in tri], dtype=float) * hh
+                yb = np.array([b for _, b in tri], dtype=float) * hh
+                det = (xb[1] - xb[0]) * (yb[2] - yb[0]) - (xb[2] - xb[0]) * (yb[1] - yb[0])
+                dphidx = np.array([yb[1] - yb[2], yb[2] - yb[0], yb[0] - yb[1]]) / det
+                Ce = np.outer(np.full(3, abs(det) / 6.0), dphidx)
+                for a in range(3):
+                    if g[a] < 0:
+                        continue
+                    for b in range(3):
+                        if g[b] < 0:
+                            continue
+                        M[g[a], g[b]] += Me[a, b]
+                        A[g[a], g[b]] -= Ke[a, b] + conv * Ce[a, b]
+    B = np.zeros((n, 1))
+    for j in range(1, nx + 1):           # Neumann edge x = 1 (i = nx): boundary mass, lumped
+        B[idx(nx, j), 0] = hh if j < nx else hh / 2
+    C = np.zeros((2, n))
+    C[0, idx(nx // 2, nx // 2)], C[0, idx(nx, nx)] = 1.0, -1.0
+    C[1, idx(max(1, nx // 4), nx)], C[1, idx(nx, max(1, nx // 4))] = 1.0, -1.0
+    return M, A, B, C
+
+
 def _rng(config: int, role: int) -> np.random.Generator:
     return np.random.Generator(np.random.PCG64(1000 * config + role))
 
@@ -139,17 +189,24 @@ CONFIGS = {
     5: dict(desc="DRE 2D heat n=10000 FP64, rank cap 64, Strang F12F3", kind="heat2d", nx=100,
             p=2, r0=5, m=1, T=0.5, nsteps=100, scheme="strang", composition="F12F3",
             rank_cap=64),
+    # SURVEY §8(f3), beyond BASELINE.json's five: Example 4's mass-matrix DRE structure
+    # on a synthetic P1 FEM pair, R^-1 = I, P0 = 0
+    6: dict(desc="mass-matrix DRE (steel-cooling structure), P1 FEM n=nx^2, Strang F12F3",
+            kind="fem2d", nx=40, p=2, r0=0, m=1, T=0.5, nsteps=100, scheme="strang",
+            composition="F12F3"),
 }
 
 
 def make_config(config: int, nx: Optional[int] = None, n: Optional[int] = None,
-                rinv: float = 1.0, dle: bool = False) -> Problem:
+                rinv: float = 1.0, dle: bool = False, conv: Optional[float] = None) -> Problem:
     """Build the problem of BASELINE.json config `config` (optionally at a smaller size).
 
     `nx`/`n` override the size (same recipe, e.g. the n=25 verification problems of P:L370).
     `rinv` sets R = (1/rinv) I (P:L384 uses R^-1 in {1, 1e-3}). `dle=True` drops B.
     """
     c = dict(CONFIGS[config])
+    if conv is not None:
+        c["conv"] = conv
     kind = c["kind"]
     heat_nx = heat_dim = None
     S = None
@@ -167,10 +224,13 @@ def make_config(config: int, nx: Optional[int] = None, n: Optional[int] = None,
     elif kind == "stochastic":
         nxx = nx or c["nx"]
         A, Bs, S, Cs = stochastic_heat_matrices(nxx)
+    elif kind == "fem2d":
+        nxx = nx or c["nx"]
+        Mm, A, Bs, Cs = fem2d_matrices(nxx, conv=c.get("conv", 0.0))
     else:
         raise ValueError(kind)
     N = A.shape[0]
-    if kind == "stochastic":
+    if kind in ("stochastic", "fem2d"):
         C = Cs
         B = None if dle else Bs
     else:
@@ -182,4 +242,4 @@ def make_config(config: int, nx: Optional[int] = None, n: Optional[int] = None,
     R = None if B is None else np.eye(B.shape[1]) / rinv
     return Problem(A=np.ascontiguousarray(A), C=C, L0=L0, D0=D0, B=B, R=R, S=S, T=c["T"],
                    name=f"config{config}", heat_nx=heat_nx, heat_dim=heat_dim,
-                   meta=dict(c, config=config))
+                   meta=dict(c, config=config), M=Mm if kind == "fem2d" else None)
