@@ -120,7 +120,7 @@ def cpu_baseline(prob, steps: int):
     orc.step("strang", "F12F3", steps)
     t2 = time.perf_counter()
     return {"value": steps / (t2 - t1), "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{steps} Strang F12F3 steps of config 5 (n={prob.n}) after a warm-up step; "
+            "sample": f"{steps} Strang F12F3 steps of {prob.name} (n={prob.n}) after a warm-up step; "
                       f"oracle setup {t1 - t0:.1f}s untimed; NumPy/OpenBLAS threads = all cores"}
 
 
@@ -129,13 +129,13 @@ def run_reference(args):
     if rank != 0:
         return
     from workloads import make_config
-    prob = make_config(5)
+    prob = make_config(args.config, nx=args.nx)
     cb = cpu_baseline(prob, max(1, args.steps))
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config5: DRE 2D heat n=10000, Strang F12F3, rank cap 64, h=0.005"},
+            "config": {"workload": f"config{args.config}: n={prob.n}, Strang F12F3, rank cap 64, h=0.005"},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -154,7 +154,7 @@ def run_ours(args):
     import paper_1805_08990_b200 as dme
     from workloads import make_config
 
-    prob = make_config(5, nx=args.nx)
+    prob = make_config(args.config, nx=args.nx)
     uid = None
     if world > 1:
         buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
@@ -169,6 +169,8 @@ def run_ours(args):
     # (validation, Padé expm, quadrature ladder, P0 compression) is timed as part of time-to-T.
     A_dev = torch.from_numpy(prob.A).cuda()
     kw_dev = dict(dme.problem_kwargs(prob), A=A_dev)
+    if prob.M is not None:  # the mass matrix lives with A (device-resident too)
+        kw_dev["M"] = torch.from_numpy(prob.M).cuda()
     torch.cuda.synchronize()
     t_init0 = time.perf_counter()
     s = dme.Solver(**kw_dev, **kw)
@@ -272,6 +274,35 @@ def run_ours(args):
                                                "bytes": ep_b / max(npass, 1)},
                     **shares}
 
+    # ------------------------------------------------------------ end to end through the public API
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        # host inputs in pinned memory (the caller's buffers), H2D inside the timed region
+        A_pin = torch.empty(prob.A.shape, dtype=torch.float64, pin_memory=True)
+        A_pin.copy_(torch.from_numpy(prob.A))
+        kw_host = dict(dme.problem_kwargs(prob), A=A_pin.numpy())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2 = dme.Solver(**kw_host, **kw)                            # H2D of A, C, B, R, L0
+        s2.split_step("strang", "F12F3", NT)
+        L, D = s2.get_factor()                                      # D2H of the factor
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        h2d = sum(a.nbytes for a in (prob.A, prob.C, prob.B, prob.R, prob.L0, prob.D0) if a is not None)
+        e2e = {"value": NT / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d / NT,
+               "d2h_bytes_per_step": (L.nbytes + D.nbytes) / NT, "time_to_T_s": t_e2e,
+               "what": "N_t=100 steps/(wall time of dme_dre_init from host arrays + 100 steps + "
+                       "dme_get_factor to host): time-to-T end to end"}
+        s2.close()
+        del s2
+
     # ------------------------------------------------------------ native-FP64 (DMMA) variant
     variant = None
     if not args.no_variant:
@@ -302,35 +333,6 @@ def run_ours(args):
         del s3
         torch.cuda.empty_cache()
 
-    # ------------------------------------------------------------ end to end through the public API
-    e2e = None
-    if not args.no_e2e:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        # host inputs in pinned memory (the caller's buffers), H2D inside the timed region
-        A_pin = torch.empty(prob.A.shape, dtype=torch.float64, pin_memory=True)
-        A_pin.copy_(torch.from_numpy(prob.A))
-        kw_host = dict(dme.problem_kwargs(prob), A=A_pin.numpy())
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        s2 = dme.Solver(**kw_host, **kw)                            # H2D of A, C, B, R, L0
-        s2.split_step("strang", "F12F3", NT)
-        L, D = s2.get_factor()                                      # D2H of the factor
-        torch.cuda.synchronize()
-        t_e2e = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
-        h2d = sum(a.nbytes for a in (prob.A, prob.C, prob.B, prob.R, prob.L0, prob.D0) if a is not None)
-        e2e = {"value": NT / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d / NT,
-               "d2h_bytes_per_step": (L.nbytes + D.nbytes) / NT, "time_to_T_s": t_e2e,
-               "what": "N_t=100 steps/(wall time of dme_dre_init from host arrays + 100 steps + "
-                       "dme_get_factor to host): time-to-T end to end"}
-        s2.close()
-        del s2
-
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -348,8 +350,11 @@ def run_ours(args):
                                  "int32 exact accumulation, FP64 assembly; per-entry error <= "
                                  "2^-54 max_l|E_il| sum_l|L_lj|, DESIGN.md 5b)"
                                  if st["ozaki_passes"] > 0 else "FP64 (DMMA + DFMA)"),
-                "config": {"workload": "config5: DRE 2D heat n=10000 (n_x=100), Strang F12F3, "
-                                       "rank cap 64, tol 1e-16, h=0.005 (T=0.5, N_t=100)",
+                "config": {"workload": (f"config{args.config}: " + (
+                               "DRE 2D heat n=10000 (n_x=100), Strang F12F3, rank cap 64, tol 1e-16, "
+                               "h=0.005 (T=0.5, N_t=100)" if args.config == 5 else
+                               f"mass-matrix DRE (Example 4 structure, P1 FEM n={prob.n}), Strang "
+                               "F12F3, rank cap 64, tol 1e-16, h=0.005 (T=0.5, N_t=100)")),
                            "n": prob.n, "rank_after_timed_steps": rank_now,
                            "l2": "inputs larger than L2 (E_{h/2} = 800 MB streamed per pass)",
                            "parallelism": f"rows of E sharded over {world} GPU(s)"},
@@ -371,11 +376,15 @@ def main():
     ap.add_argument("--steps", type=int, default=100)  # = N_t of config 5
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--nx", type=int, default=100, help="(debug) grid size; default = config 5")
+    ap.add_argument("--config", type=int, default=5, choices=[5, 6],
+                    help="5 (default, BASELINE.json's headline) or 6 (mass-matrix DRE, SURVEY f3)")
+    ap.add_argument("--nx", type=int, default=None, help="grid size (default: 100 for 5, 70 for 6)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variant", action="store_true", help="skip the native-FP64 E-pass run")
     args = ap.parse_args()
+    if args.nx is None:
+        args.nx = 100 if args.config == 5 else 70
     if args.impl == "reference":
         run_reference(args)
     else:
