@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   extern __shared__ double R[];  // reflectors, k x ld
   __shared__ double d[FK], e[FK], e2[FK], tau[FK];
   __shared__ double lo_s[MAXE], hi_s[MAXE], lam_s[MAXE];
+  __shared__ double cpair[(FK / 4 + 1) * 6];  // per block of 4 reflectors: v_p^T v_q
   __shared__ int cnt_s[ENT];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = a.k, ld = k | 1;
@@ -249,7 +250,26 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   __syncthreads();
 
   // ------------------------------------------------------------ W = Q Z, one warp per column
+  // Reflectors are applied four at a time (H_j0 H_j1 H_j2 H_j3 with j0 = j3 + 3 applied first):
+  // the four dots v_jm^T z share one warp reduction and the coupling v_p^T v_q of the block
+  // (precomputed below) turns them into the four coefficients by a 4-term recurrence:
+  //   s_m = tau_jm (a_m - sum_{m' < m} (v_jm^T v_jm') s_m')
   t_ph[3] = clock64();
+  const int nb4 = (k - 2 + 3) / 4;  // reflectors 0 .. k-3
+  for (int e = tid; e < nb4 * 6; e += ENT) {
+    const int b = e / 6, pr = e % 6;
+    const int jt = k - 3 - 4 * b;
+    // pr -> (ma, mb): (0,1) (0,2) (1,2) (0,3) (1,3) (2,3)
+    const int mb = pr < 1 ? 1 : (pr < 3 ? 2 : 3), ma = pr - mb * (mb - 1) / 2;
+    const int q = jt - ma, p = jt - mb;  // p < q: v_p^T v_q
+    double sum = 0.0;
+    if (p >= 0) {
+      sum = R[p * ld + q + 1];  // v_q[q+1] = 1
+      for (int i = q + 2; i < k; ++i) sum = fma(R[p * ld + i], R[q * ld + i], sum);
+    }
+    cpair[e] = sum;
+  }
+  __syncthreads();
   for (int cc = warp; cc < nv; cc += NW) {
     const int c = c0 + cc;
     const double* zsrc = FK <= 96 ? R + k * ld + cc * FK : es.dp() + (size_t)c * SMALL_K_MAX;
@@ -259,20 +279,35 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
       const int i = lane + 32 * u;
       z[u] = i < k ? zsrc[i] : 0.0;
     }
-    for (int j = k - 3; j >= 0; --j) {
-      const double tj = tau[j];
-      if (tj == 0.0) continue;
-      double vr[RCH];
-      double sv = 0.0;
+    for (int b = 0; b < nb4; ++b) {
+      const int jt = k - 3 - 4 * b;
+      double vr[4][RCH], am[4];
 #pragma unroll
-      for (int u = 0; u < RCH; ++u) {
-        const int i = lane + 32 * u;
-        vr[u] = (i == j + 1) ? 1.0 : ((i > j + 1 && i < k) ? R[j * ld + i] : 0.0);
-        sv = fma(vr[u], z[u], sv);
+      for (int mm = 0; mm < 4; ++mm) {
+        const int j = jt - mm;
+        double sv = 0.0;
+#pragma unroll
+        for (int u = 0; u < RCH; ++u) {
+          const int i = lane + 32 * u;
+          vr[mm][u] = j < 0 ? 0.0 : ((i == j + 1) ? 1.0 : ((i > j + 1 && i < k) ? R[j * ld + i] : 0.0));
+          sv = fma(vr[mm][u], z[u], sv);
+        }
+        am[mm] = sv;
       }
-      sv = warp_sum(sv) * tj;
 #pragma unroll
-      for (int u = 0; u < RCH; ++u) z[u] = fma(-sv, vr[u], z[u]);
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) am[mm] += __shfl_xor_sync(0xffffffffu, am[mm], o);
+      const double* cp = cpair + b * 6;
+      const double t0 = tau[jt], t1 = jt >= 1 ? tau[jt - 1] : 0.0;
+      const double t2 = jt >= 2 ? tau[jt - 2] : 0.0, t3 = jt >= 3 ? tau[jt - 3] : 0.0;
+      const double s0 = t0 * am[0];
+      const double s1 = t1 * fma(-cp[0], s0, am[1]);
+      const double s2 = t2 * fma(-cp[2], s1, fma(-cp[1], s0, am[2]));
+      const double s3 = t3 * fma(-cp[5], s2, fma(-cp[4], s1, fma(-cp[3], s0, am[3])));
+#pragma unroll
+      for (int u = 0; u < RCH; ++u)
+        z[u] = fma(-s3, vr[3][u], fma(-s2, vr[2][u], fma(-s1, vr[1][u], fma(-s0, vr[0][u], z[u]))));
     }
     const double f = a.sqrt_scale ? sqrt(fmax(lam_s[cc] * scale, 0.0)) : 1.0;
 #pragma unroll
