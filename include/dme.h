@@ -119,8 +119,8 @@ typedef struct {
                              slicing (Ozaki scheme, 8 x 7-bit digits per operand, int32 exact
                              accumulation, FP64 assembly; error per entry <= ~2^-54
                              max_l|E_il| sum_l|L_lj|) when n <= 32768 and the
-                             pass has <= 64 columns, else FP64 DMMA; on one GPU the Padé
-                             products and squarings of the init use the same int8 kernel
+                             pass has <= 64 columns, else FP64 DMMA; the Padé products and
+                             squarings of the (replicated) init use the same int8 kernel
                              (square tiles); DME_EPASS_DMMA: every E pass and every init
                              product in native FP64 DMMA (mma.sync m8n8k4 f64)                  */
 } dme_options;

@@ -124,7 +124,7 @@ struct dme_ctx {
   int *exEh = nullptr, *exEf = nullptr, *exY = nullptr, *exY2 = nullptr;
   double *ozpm = nullptr, *ozpm2 = nullptr;  // slicing scratch (row maxima per chunk)
   OzScratch ozs, ozs2;
-  // init-time square products on the int8 tensor cores (world == 1): rasterised tile lists
+  // init-time square products on the int8 tensor cores: rasterised tile lists
   bool oz_init = false;
   int2* oz_tiles_up = nullptr;  // upper tile triangle (symmetric products)
   int2* oz_tiles_all = nullptr;
@@ -208,18 +208,21 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   if (c->oz) {
     c->ozld = oz_ldk(n);
     const int64_t rl = std::max<int64_t>(c->rows_loc, 1);
-    const size_t es = (size_t)OZ_S * rl * c->ozld, ys = (size_t)OZ_S * OZ_NMAX * c->ozld;
+    // E-digit buffers: the local rows of E for the passes, and during the (replicated) init the
+    // digits of both n x n operands of each product: n rows
+    const int64_t rb = c->oz_init ? std::max<int64_t>(rl, n) : rl;
+    const size_t es = (size_t)OZ_S * rb * c->ozld, ys = (size_t)OZ_S * OZ_NMAX * c->ozld;
     c->ozEh = P.take<int8_t>(es);
     c->ozEf = P.take<int8_t>(es);
     c->ozY = P.take<int8_t>(ys);
     c->ozY2 = P.take<int8_t>(ys);
-    c->exEh = P.take<int>(rl);
-    c->exEf = P.take<int>(rl);
+    c->exEh = P.take<int>(rb);
+    c->exEf = P.take<int>(rb);
     c->exY = P.take<int>(OZ_NMAX);
     c->exY2 = P.take<int>(OZ_NMAX);
-    c->ozpm = P.take<double>(oz_slice_scratch_doubles(std::max<int64_t>(rl, OZ_NMAX), n));
+    c->ozpm = P.take<double>(oz_slice_scratch_doubles(std::max<int64_t>(rb, OZ_NMAX), n));
     c->ozpm2 = P.take<double>(oz_slice_scratch_doubles(OZ_NMAX, n));
-    if (c->world == 1) {
+    if (c->oz_init) {
       c->h_tiles_up = oz_tile_list(n, n, true);
       c->h_tiles_all = oz_tile_list(n, n, false);
       c->ntiles_up = (int)c->h_tiles_up.size();
@@ -281,8 +284,8 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   // E pass on the int8 tensor cores (exact digit slicing) unless disabled or out of its range
   c->oz = o->e_pass != DME_EPASS_DMMA && c->n <= OZ_KMAX && c->rows_loc > 0;
   // the Padé products and squarings on the int8 tensor cores too (digits of both operands live
-  // in the E-digit buffers until E is sliced; replicated init, so one GPU only)
-  c->oz_init = c->oz && c->world == 1;
+  // in the E-digit buffers until E is sliced; the init is replicated on every rank, local work)
+  c->oz_init = c->oz;
 }
 
 bool all_finite(const double* x, size_t cnt) {
