@@ -2,6 +2,7 @@
 // See include/dme.h for the contract and DESIGN.md for the design and the paper readings.
 #include <nccl.h>
 
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -131,6 +132,9 @@ struct dme_ctx {
   int ntiles_up = 0, ntiles_all = 0;
   std::vector<int2> h_tiles_up, h_tiles_all;
   cudaStream_t st2 = nullptr;
+  HostMap* hmap = nullptr;       // pinned, host-mapped rank record (small.h)
+  HostMap* hmap_dev = nullptr;   // its device alias
+  int map_seq = 0;
   cudaEvent_t ev_gram = nullptr, ev_ahead = nullptr, ev_ghat = nullptr, ev_cong = nullptr,
               ev_y = nullptr;
   bool lookahead = true;
@@ -159,6 +163,7 @@ struct dme_ctx {
     for (auto e : pool) cudaEventDestroy(e);
     if (comm) ncclCommDestroy(comm);
     if (st2) cudaStreamDestroy(st2);
+    if (hmap) cudaFreeHost(hmap);
     if (ev_gram) cudaEventDestroy(ev_gram);
     if (ev_ahead) cudaEventDestroy(ev_ahead);
     for (cudaEvent_t e : {ev_ghat, ev_cong, ev_y})
@@ -580,6 +585,10 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
   a.Es = c->Es;
   a.r_out = c->r_dev;
   a.stats = c->sstats;
+  if (c->hmap_dev) {
+    a.map = c->hmap_dev;
+    a.map_seq = ++c->map_seq;
+  }
   fast = do_compress && k <= FAST_K_MAX && !c->force_jacobi;
   ProfScope ps(c, PROF_SMALL);
   if (fast && k >= EIG_SPLIT_MIN) eig_split(a, c->st);
@@ -587,22 +596,49 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
   else compress_t3(a, c->st);
 }
 
+// Wait until the small kernel launched with sequence number `seq` has published its rank in the
+// host-mapped record (spinning on pinned memory: no D2H copy, no stream synchronisation on the
+// step's critical path); the stream is polled now and then so a failed launch surfaces as an error.
+void wait_published(dme_ctx* c, int seq) {
+  volatile HostMap* m = c->hmap;
+  for (int64_t spins = 1; m->seq != seq; ++spins) {
+    if ((spins & 1023) == 0) {
+      const cudaError_t q = cudaStreamQuery(c->st);
+      if (q == cudaSuccess) {
+        if (m->seq == seq) break;
+        throw DmeError(DME_ERR_CUDA, "small kernel finished without publishing its rank");
+      }
+      if (q != cudaErrorNotReady) DME_CUDA(q);
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+
 // Wait for the small kernel (main stream only), fall back to Jacobi if the fast path refused.
 int64_t compress_finish(dme_ctx* c, const SmallArgs& a, bool fast, bool do_compress) {
   int r_host = 0;
   double st_host[5] = {0, 0, 0, 0, 0};
-  DME_CUDA(cudaMemcpyAsync(&r_host, c->r_dev, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  DME_CUDA(cudaMemcpyAsync(st_host, c->sstats, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  sync(c);
+  auto fetch = [&](const SmallArgs& x) {
+    if (x.map) {
+      wait_published(c, x.map_seq);
+      r_host = c->hmap->r;
+      for (int i = 0; i < 5; ++i) st_host[i] = c->hmap->stats[i];
+    } else {
+      DME_CUDA(cudaMemcpyAsync(&r_host, c->r_dev, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+      DME_CUDA(cudaMemcpyAsync(st_host, c->sstats, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+    }
+  };
+  fetch(a);
   if (fast && r_host < 0) {  // near-degenerate cluster: orthogonality check failed -> Jacobi
     c->stats.eig_fallbacks++;
+    SmallArgs b = a;
+    if (b.map) b.map_seq = ++c->map_seq;
     {
       ProfScope ps(c, PROF_SMALL);
-      compress_t3(a, c->st);
+      compress_t3(b, c->st);
     }
-    DME_CUDA(cudaMemcpyAsync(&r_host, c->r_dev, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-    DME_CUDA(cudaMemcpyAsync(st_host, c->sstats, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    sync(c);
+    fetch(b);
   }
   if (do_compress) c->stats.last_drop = st_host[2];
   return r_host;
@@ -1149,6 +1185,11 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     int lo_pri = 0, hi_pri = 0;
     DME_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
     DME_CUDA(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, lo_pri));
+    // (pinned host memory for the rank record: the library's only host allocation besides the
+    // ctx; device memory stays the caller's workspace)
+    DME_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->hmap), sizeof(HostMap), cudaHostAllocMapped));
+    std::memset(c->hmap, 0, sizeof(HostMap));
+    DME_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hmap_dev), c->hmap, 0));
     DME_CUDA(cudaEventCreateWithFlags(&c->ev_gram, cudaEventDisableTiming));
     DME_CUDA(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming));
     for (cudaEvent_t* e : {&c->ev_ghat, &c->ev_cong, &c->ev_y})

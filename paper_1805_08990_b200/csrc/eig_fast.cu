@@ -377,14 +377,14 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   if (tid == 0 && a.stats)
     for (int i = 0; i < 6; ++i) a.stats[8 + i] = (double)(t_ph[i + 1] - t_ph[i]);
   if (s_bad) {
-    if (tid == 0) *a.r_out = -1;  // caller falls back to the Jacobi kernel
+    if (tid == 0) publish_rank(a, -1);  // caller falls back to the Jacobi kernel
     return;
   }
   if (a.t3 && r > 0) {
     __syncthreads();
     smallk::t3_fuse(a, k, r, A, Gam, Phi);
   }
-  if (tid == 0) *a.r_out = r;
+  if (tid == 0) publish_rank(a, r);
 }
 
 template <int FK>

@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fin_kernel(SmallArgs a) {
   }
   __syncthreads();
   if (s_bad) {
-    if (tid == 0) *a.r_out = -1;  // caller falls back to the Jacobi kernel
+    if (tid == 0) publish_rank(a, -1);  // caller falls back to the Jacobi kernel
     return;
   }
   const long long f2 = clock64();
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fin_kernel(SmallArgs a) {
     }
   }
   if (tid == 0) {
-    *a.r_out = r;
+    publish_rank(a, r);
     if (a.stats) {  // phase cycles (tools/eig_split_probe.py)
       a.stats[14] = (double)(f1 - f0);
       a.stats[15] = (double)(f2 - f1);

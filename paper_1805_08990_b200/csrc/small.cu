@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(NT, 1) compress_t3_kernel(SmallArgs a) {
   }
 
   if (a.t3 && r > 0) t3_fuse(a, k, r, S, Gam, Phi);
-  if (tid == 0) *a.r_out = r;
+  if (tid == 0) publish_rank(a, r);
 }
 
 }  // namespace

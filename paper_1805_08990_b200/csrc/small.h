@@ -11,6 +11,14 @@ constexpr int EIG_SPLIT_MIN = 48;         // k from which the eigen-compression 
 constexpr int EIG_SPLIT_CTAS = 8;         // CTAs of the VEC kernel (the look-ahead E pass leaves them)            // columns of B handled by the fused Riccati flow
 constexpr int SMALL_SMEM_MAX = SMALL_K_MAX * (SMALL_K_MAX + 1) / 2 * 8;
 
+// Host-mapped (pinned, zero-copy) record through which the small kernels publish the new rank:
+// the host spins on `seq` instead of a D2H copy + stream synchronisation per compression.
+struct HostMap {
+  int seq;
+  int r;
+  double stats[5];
+};
+
 struct SmallArgs {
   int k = 0;                 // columns of the concatenated factor Zc
   int compress = 1;          // 1: eigen-compression of G (Z_new = Zc W_kept)
@@ -34,6 +42,8 @@ struct SmallArgs {
   double* Es = nullptr;      // split path: global scratch (eig_split_scratch_doubles())
   int zsmem = 1;             // fast path: back-transformation columns in shared memory when they fit
   double orth_tol = 1e-12;   // fast path: max weighted |W^T W - I| before falling back to Jacobi
+  HostMap* map = nullptr;    // device alias of the host-mapped record (nullptr: r_out only)
+  int map_seq = 0;           // sequence number this launch publishes
 };
 
 void compress_t3(const SmallArgs& a, cudaStream_t st);  // Jacobi (any k <= SMALL_K_MAX)

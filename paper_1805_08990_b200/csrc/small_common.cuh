@@ -3,6 +3,21 @@
 #include "small.h"
 
 namespace dme {
+
+// Thread 0 of the last block of a compression: the new rank to r_out and, when the host-mapped
+// record is set, stats + rank, a system-scope fence, then the sequence number the host waits for.
+__device__ inline void publish_rank(const SmallArgs& a, int r) {
+  *a.r_out = r;
+  if (a.map) {
+    volatile HostMap* m = a.map;
+    if (a.stats)
+      for (int i = 0; i < 5; ++i) m->stats[i] = a.stats[i];
+    m->r = r;
+    __threadfence_system();
+    m->seq = a.map_seq;
+  }
+}
+
 namespace smallk {
 
 constexpr int NT = 1024;
