@@ -458,6 +458,8 @@ void drain_profile(dme_ctx* c) {
 // out (rows x k) = alpha * E[rows] * X on the int8 tensor cores; E = E_{h/2} or E_h (sliced)
 void oz_pass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t out_cs,
              double alpha, cudaStream_t st, bool second) {
+  // profiled as the E-pass kernel: the int8 product alone (the digit slicing of X, ~n k bytes, is
+  // its own pair of small kernels before it)
   int8_t* yq = second ? c->ozY2 : c->ozY;
   int* ye = second ? c->exY2 : c->exY;
   oz_slice_rows(X, c->ldn, k, c->n, yq, c->ozld, (int64_t)OZ_NMAX * c->ozld, ye,
@@ -469,7 +471,10 @@ void oz_pass(dme_ctx* c, const double* E, const double* X, int64_t k, double* ou
   g.B = yq; g.eB = ye; g.ldb = c->ozld; g.b_slice_stride = (int64_t)OZ_NMAX * c->ozld;
   g.M = c->rows_loc; g.N = k; g.K = c->n; g.alpha = alpha;
   g.out = out; g.out_rs = 1; g.out_cs = out_cs;
-  oz_gemm(g, second ? c->ozs2 : c->ozs, st);
+  {
+    ProfScope ps(c, PROF_EPASS, 2.0 * g.M * c->n * k, 1.0 * OZ_S * g.M * c->n, st);
+    oz_gemm(g, second ? c->ozs2 : c->ozs, st);
+  }
   c->stats.ozaki_passes++;
 }
 
@@ -480,16 +485,12 @@ void epass_on(dme_ctx* c, const double* E, const double* X, int64_t k, double* o
   const bool second = &gs == &c->gs2;
   const bool use_oz = c->oz && c->oz_ready && k <= OZ_NMAX && (E == c->E_half || E == c->E_full);
   if (use_oz && c->world == 1) {
-    ProfScope ps(c, PROF_EPASS, 2.0 * c->n * c->n * k, 1.0 * OZ_S * c->n * c->n, st);
     oz_pass(c, E, X, k, out, ldo, alpha, st, second);
     return;
   }
   if (use_oz) {
     double* mine = c->stage + (size_t)c->rank * c->nloc * k;
-    {
-      ProfScope ps(c, PROF_EPASS, 2.0 * c->rows_loc * c->n * k, 1.0 * OZ_S * c->rows_loc * c->n, st);
-      oz_pass(c, E, X, k, mine, c->nloc, alpha, st, second);
-    }
+    oz_pass(c, E, X, k, mine, c->nloc, alpha, st, second);
     DME_NCCL(ncclAllGather(mine, c->stage, (size_t)c->nloc * k, ncclDouble, c->comm, st));
     for (int gr = 0; gr < c->world; ++gr) {
       const int64_t r0 = std::min<int64_t>(c->n, (int64_t)gr * c->nloc);
