@@ -216,7 +216,10 @@ void plan_buffers(dme_ctx* c, Planner& P) {
     // E-digit buffers: the local rows of E for the passes, and during the (replicated) init the
     // digits of both n x n operands of each product: n rows
     const int64_t rb = c->oz_init ? std::max<int64_t>(rl, n) : rl;
-    const size_t es = (size_t)OZ_S * rb * c->ozld, ys = (size_t)OZ_S * OZ_NMAX * c->ozld;
+    // (the E passes read the tiled, pre-swizzled image of oz_slice_rows_tiled; the init products
+    // the row layout)
+    const size_t es = std::max<size_t>((size_t)OZ_S * rb * c->ozld, (size_t)oz_tiled_bytes(rl, n));
+    const size_t ys = (size_t)OZ_S * OZ_NMAX * c->ozld;
     c->ozEh = P.take<int8_t>(es);
     c->ozEf = P.take<int8_t>(es);
     c->ozY = P.take<int8_t>(ys);
@@ -471,6 +474,7 @@ void oz_pass(dme_ctx* c, const double* E, const double* X, int64_t k, double* ou
   g.B = yq; g.eB = ye; g.ldb = c->ozld; g.b_slice_stride = (int64_t)OZ_NMAX * c->ozld;
   g.M = c->rows_loc; g.N = k; g.K = c->n; g.alpha = alpha;
   g.out = out; g.out_rs = 1; g.out_cs = out_cs;
+  g.A_tiled = g.A;  // E digits in the tiled image (oz_slice_rows_tiled at the end of init)
   {
     ProfScope ps(c, PROF_EPASS, 2.0 * g.M * c->n * k, 1.0 * OZ_S * g.M * c->n, st);
     oz_gemm(g, second ? c->ozs2 : c->ozs, st);
@@ -1097,10 +1101,8 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   c->qf = qf;
   matmul_sq(c, c->E_half, c->E_half, c->E_full);
   if (c->oz) {  // digit slices of the local rows of E_{h/2} and E_h (after the last product)
-    oz_slice_rows(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->ozld,
-                  c->rows_loc * c->ozld, c->exEh, c->ozpm, st);
-    oz_slice_rows(c->E_full + c->row0 * ld, ld, c->rows_loc, n, c->ozEf, c->ozld,
-                  c->rows_loc * c->ozld, c->exEf, c->ozpm, st);
+    oz_slice_rows_tiled(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->exEh, c->ozpm, st);
+    oz_slice_rows_tiled(c->E_full + c->row0 * ld, ld, c->rows_loc, n, c->ozEf, c->exEf, c->ozpm, st);
     c->oz_ready = true;
   }
   // look-ahead operand: E_h L_I(h) stays in the leading columns of LA
@@ -1527,7 +1529,7 @@ dme_status dme_debug_matmul_ozaki(int64_t M, int64_t N, int64_t K, const double*
     DME_CUDA(cudaMalloc(&dA, M * ldd * 8));
     DME_CUDA(cudaMalloc(&dBT, OZ_NMAX * ldd * 8));
     DME_CUDA(cudaMalloc(&dC, M * N * 8));
-    DME_CUDA(cudaMalloc(&qa, (size_t)OZ_S * M * ldq));
+    DME_CUDA(cudaMalloc(&qa, std::max<size_t>((size_t)OZ_S * M * ldq, (size_t)oz_tiled_bytes(M, K))));
     DME_CUDA(cudaMalloc(&qb, (size_t)OZ_S * OZ_NMAX * ldq));
     DME_CUDA(cudaMalloc(&ea, M * sizeof(int)));
     DME_CUDA(cudaMalloc(&eb, OZ_NMAX * sizeof(int)));
@@ -1543,10 +1545,11 @@ dme_status dme_debug_matmul_ozaki(int64_t M, int64_t N, int64_t K, const double*
     for (int64_t i = 0; i < K; ++i)
       for (int64_t j = 0; j < N; ++j) bt[j * K + i] = B[i * N + j];
     DME_CUDA(cudaMemcpy2D(dBT, ldd * 8, bt.data(), K * 8, K * 8, N, cudaMemcpyHostToDevice));
-    oz_slice_rows(dA, ldd, M, K, qa, ldq, M * ldq, ea, pm, 0);
+    // A in the tiled image, as the E pass reads E
+    oz_slice_rows_tiled(dA, ldd, M, K, qa, ea, pm, 0);
     oz_slice_rows(dBT, ldd, N, K, qb, ldq, OZ_NMAX * ldq, eb, pm, 0);
     OzGemmArgs g;
-    g.A = qa; g.eA = ea; g.lda = ldq; g.a_slice_stride = M * ldq;
+    g.A = qa; g.A_tiled = qa; g.eA = ea; g.lda = ldq; g.a_slice_stride = M * ldq;
     g.B = qb; g.eB = eb; g.ldb = ldq; g.b_slice_stride = OZ_NMAX * ldq;
     g.M = M; g.N = N; g.K = K;
     g.out = dC; g.out_rs = N; g.out_cs = 1;

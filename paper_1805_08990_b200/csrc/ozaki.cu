@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(224, 1)
                    const int* __restrict__ eA, const int* __restrict__ eB, double* __restrict__ out,
                    int64_t out_rs, int64_t out_cs, int M, int N, int nkc, int ntiles,
                    const int2* __restrict__ tile_list, int rr, double alpha,
-                   double* __restrict__ partial, int* __restrict__ counters) {
+                   double* __restrict__ partial, int* __restrict__ counters,
+                   const int8_t* __restrict__ a_tiled) {
   using C = OzCfg<NP>;
   constexpr int S = C::S;
   extern __shared__ uint8_t smem_raw[];
@@ -224,7 +225,12 @@ __global__ void __launch_bounds__(224, 1)
           for (int a = 0; a < S; ++a) {
             mbar_wait(empty_a + as, pa ^ 1);
             mbar_arrive_expect_tx(full_a + as, C::AST);
-            tma_load_3d(As + as * C::AST, &tmA, full_a + as, kc * 128, rt * 128, a);
+            if (a_tiled)  // pre-swizzled tile image: one contiguous 16 KB bulk copy
+              bulk_load(As + as * C::AST,
+                        a_tiled + (((size_t)rt * nkc + kc) * S + a) * (size_t)C::AST, C::AST,
+                        full_a + as);
+            else
+              tma_load_3d(As + as * C::AST, &tmA, full_a + as, kc * 128, rt * 128, a);
             if (++as == C::NA) { as = 0; pa ^= 1; }
           }
         }
@@ -434,6 +440,49 @@ __global__ void __launch_bounds__(SL_T) oz_slice_kernel(const double* __restrict
   }
 }
 
+// Digit slicing into the tiled, pre-swizzled image the E-pass kernel streams with plain bulk
+// copies: block (row tile t, K chunk c, slice s) = 128 rows x 128 bytes at
+// ((t * nkc + c) * OZ_S + s) * 16384, row i at i * 128, 16-byte chunk j at (j ^ (i & 7)) * 16
+// (SWIZZLE_128B). Padding rows / columns must be zero (the caller clears the buffer once).
+__global__ void __launch_bounds__(SL_T) oz_slice_tiled_kernel(const double* __restrict__ X, int64_t ld,
+                                                              int64_t cols, const double* __restrict__ pm,
+                                                              int8_t* __restrict__ q, int nkc,
+                                                              int* __restrict__ ex) {
+  const int64_t row = blockIdx.y;
+  double mx = 0.0;
+  for (unsigned i = 0; i < gridDim.x; ++i) mx = fmax(mx, pm[row * gridDim.x + i]);
+  const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ex[row] = e;
+  const double* x = X + row * ld;
+  const int64_t c4end = (cols + 3) / 4 * 4;
+  const int64_t t = row >> 7;
+  const int il = (int)(row & 127);
+#pragma unroll
+  for (int it = 0; it < SL_CH / (SL_T * 4); ++it) {
+    const int64_t c4 = (int64_t)blockIdx.x * SL_CH + ((int64_t)it * SL_T + threadIdx.x) * 4;
+    if (c4 >= c4end) break;
+    uint32_t w[OZ_S];
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) w[s] = 0u;
+#pragma unroll
+    for (int tt = 0; tt < 4; ++tt) {
+      double v = c4 + tt < cols ? scale2(x[c4 + tt], -e) : 0.0;
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) {
+        v *= 128.0;
+        const double d = rint(v);
+        v -= d;
+        w[s] |= (uint32_t)(uint8_t)(int8_t)(int)d << (8 * tt);
+      }
+    }
+    const int64_t ck = c4 >> 7;
+    const int lb = (int)(c4 & 127);
+    const int64_t off = ((t * nkc + ck) * OZ_S) * 16384 + il * 128 + ((((lb >> 4) ^ (il & 7)) << 4) | (lb & 15));
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(q + off + (int64_t)s * 16384) = w[s];
+  }
+}
+
 template <int NP>
 void launch_oz(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
   using C = OzCfg<NP>;
@@ -444,7 +493,9 @@ void launch_oz(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
   const int G = (int)std::min<int64_t>(ws.max_grid, a.round_robin ? ntiles : U);
   if (!a.round_robin && ntiles > ws.max_tiles) throw std::runtime_error("oz_gemm: scratch too small");
   if (G > ws.max_grid) throw std::runtime_error("oz_gemm: grid exceeds scratch");
-  const CUtensorMap tmA = make_tmap_3d_u8(a.A, a.K, a.M, OZ_S, a.lda, a.a_slice_stride, 128, 128, 1);
+  CUtensorMap tmA{};
+  if (!a.A_tiled)
+    tmA = make_tmap_3d_u8(a.A, a.K, a.M, OZ_S, a.lda, a.a_slice_stride, 128, 128, 1);
   const CUtensorMap tmB = make_tmap_3d_u8(a.B, a.K, listed ? a.N : NP, OZ_S, a.ldb, a.b_slice_stride,
                                           128, NP, OZ_S);
   static bool attr = false;
@@ -455,7 +506,7 @@ void launch_oz(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
   oz_gemm_kernel<NP><<<G, 224, C::SMEM, st>>>(tmA, tmB, a.eA, a.eB, a.out, a.out_rs, a.out_cs,
                                               (int)a.M, (int)a.N, nkc, ntiles, a.tiles,
                                               a.round_robin ? 1 : 0, a.alpha, ws.partial,
-                                              ws.counters);
+                                              ws.counters, a.A_tiled);
   DME_KCHECK();
 }
 
@@ -470,6 +521,21 @@ void oz_slice_rows(const double* X, int64_t ld, int64_t rows, int64_t cols, int8
   oz_rowmax_kernel<<<grid, SL_T, 0, st>>>(X, ld, cols, scratch);
   DME_KCHECK();
   oz_slice_kernel<<<grid, SL_T, 0, st>>>(X, ld, cols, scratch, q, ldk, slice_stride, ex);
+  DME_KCHECK();
+}
+
+int64_t oz_tiled_bytes(int64_t rows, int64_t cols) {
+  return ceil_div(rows, 128) * ceil_div(cols, 128) * (int64_t)OZ_S * 16384;
+}
+
+void oz_slice_rows_tiled(const double* X, int64_t ld, int64_t rows, int64_t cols, int8_t* q,
+                         int* ex, double* scratch, cudaStream_t st) {
+  if (rows <= 0) return;
+  DME_CUDA(cudaMemsetAsync(q, 0, (size_t)oz_tiled_bytes(rows, cols), st));
+  const dim3 grid((unsigned)std::max<int64_t>(1, ceil_div(cols, SL_CH)), (unsigned)rows);
+  oz_rowmax_kernel<<<grid, SL_T, 0, st>>>(X, ld, cols, scratch);
+  DME_KCHECK();
+  oz_slice_tiled_kernel<<<grid, SL_T, 0, st>>>(X, ld, cols, scratch, q, (int)ceil_div(cols, 128), ex);
   DME_KCHECK();
 }
 

@@ -57,7 +57,16 @@ struct OzGemmArgs {
   const int2* tiles = nullptr;
   int ntiles = 0;
   bool round_robin = false;
+  // E pass: A digits in the tiled, pre-swizzled image of oz_slice_rows_tiled (A, lda and
+  // a_slice_stride unused); streamed with plain 16 KB bulk copies instead of tensor-map TMA
+  const int8_t* A_tiled = nullptr;
 };
+
+// Tiled digit image of a row-major FP64 matrix (rows x cols): bytes needed, and the slicing
+// (clears the image first, then writes digits + per-row exponents ex[rows]; scratch as above).
+int64_t oz_tiled_bytes(int64_t rows, int64_t cols);
+void oz_slice_rows_tiled(const double* X, int64_t ld, int64_t rows, int64_t cols, int8_t* q,
+                         int* ex, double* scratch, cudaStream_t st);
 
 // out = alpha * E * Y (K <= OZ_KMAX). Without a tile list (N <= OZ_NMAX): persistent Stream-K
 // over 128-row tiles x 128-deep K chunks, deterministic in-kernel fixup of split tiles. With a
