@@ -181,6 +181,20 @@ dme_status dme_split_step(dme_ctx* ctx, dme_scheme scheme, dme_composition comp,
 /* Copy the factor to the host: *r <- rank; if L != NULL, L (n x r) and, if D != NULL, D (r x r)
  * with P = L D L^T. Returns DME_ERR_CAPACITY (and sets *r) when r > capacity_cols. */
 dme_status dme_get_factor(dme_ctx* ctx, int64_t* r, double* L, double* D, int64_t capacity_cols);
+/* Richardson extrapolation of the Strang composition (the paper cites higher-order
+ * splitting, and uses Strang): `fine` and `coarse` are two contexts of the same
+ * problem on one device, fine with step h/2 after 2N Strang steps, coarse with step h after N
+ * steps (DME_ERR_CONFIG otherwise). Strang's error expands in even powers of h, so
+ *   P = (4 P_fine - P_coarse) / 3 = Zc S Zc^T,  Zc = [Z_fine | Z_coarse],  S = diag(4/3 I, -1/3 I)
+ * is accurate to order 4. Computed on the device in the fine context's workspace: an orthonormal
+ * basis Q of span(Zc) by classical Gram-Schmidt with reorthogonalisation (columns inside the span
+ * to 1e-14 dropped), R^T = Zc^T Q, eigen-decomposition of the signed core R S R^T (parallel
+ * Jacobi, indefinite), L = Q U, truncation by |lambda| relative to max |lambda| (trunc_tol);
+ * returns L (n x r, row-major, orthonormal columns) and the diagonal, possibly indefinite, core
+ * D (r x r) on the host. L = D = NULL: only *r. DME_ERR_CAPACITY when r > capacity_cols,
+ * DME_ERR_DIM when the combined rank exceeds 224 (or 112 after the Gram truncation). */
+dme_status dme_extrapolate(dme_ctx* fine, dme_ctx* coarse, int64_t* r, double* L, double* D,
+                           int64_t capacity_cols);
 dme_status dme_get_stats(dme_ctx* ctx, dme_stats* st);
 /* Turn CUDA-event timing of the kernel classes on (1) or off (0); resets the prof_* counters. */
 dme_status dme_set_profiling(dme_ctx* ctx, int32_t on);

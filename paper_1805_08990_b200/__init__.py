@@ -80,6 +80,7 @@ for _name, _args in {
     "dme_dre_init": [ctypes.POINTER(_Problem), ctypes.POINTER(_Options), ctypes.POINTER(_ctx_p)],
     "dme_split_step": [_ctx_p, ctypes.c_int, ctypes.c_int, ctypes.c_int64],
     "dme_get_factor": [_ctx_p, ctypes.POINTER(ctypes.c_int64), _dp, _dp, ctypes.c_int64],
+    "dme_extrapolate": [_ctx_p, _ctx_p, ctypes.POINTER(ctypes.c_int64), _dp, _dp, ctypes.c_int64],
     "dme_get_stats": [_ctx_p, ctypes.POINTER(_Stats)],
     "dme_set_profiling": [_ctx_p, ctypes.c_int32],
     "dme_destroy": [_ctx_p],
@@ -97,7 +98,7 @@ for _name, _args in {
 
 EXPORTED = ["dme_default_options", "dme_status_string", "dme_last_error", "dme_workspace_size",
             "dme_get_unique_id", "dme_shard_rows", "dme_dle_init", "dme_dre_init", "dme_split_step",
-            "dme_get_factor", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
+            "dme_get_factor", "dme_extrapolate", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
             "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_get_integral",
             "dme_debug_small_stats", "dme_debug_matmul", "dme_debug_matmul_ozaki"]
 
@@ -273,6 +274,19 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def extrapolate(fine: "Solver", coarse: "Solver"):
+    """Richardson-extrapolated Strang: (4 P_fine - P_coarse)/3 as (L, D), D diagonal and possibly
+    indefinite (dme_extrapolate; fine: step h/2 after 2N steps, coarse: step h after N steps)."""
+    r = ctypes.c_int64(0)
+    _check(_lib.dme_extrapolate(fine._ctx, coarse._ctx, ctypes.byref(r), None, None, 0),
+           "dme_extrapolate")
+    L = np.zeros((fine.n, r.value))
+    D = np.zeros((r.value, r.value))
+    _check(_lib.dme_extrapolate(fine._ctx, coarse._ctx, ctypes.byref(r), _ptr(L), _ptr(D), r.value),
+           "dme_extrapolate")
+    return L, D
 
 
 def matmul_ozaki(A, B):

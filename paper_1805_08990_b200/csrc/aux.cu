@@ -394,6 +394,175 @@ void gram_congruence(const double* Gh, int64_t ldh, int q, int m, int kp, const 
   DME_KCHECK();
 }
 
+// Signed core of a Richardson combination (dme_extrapolate). Tm (k x r1, ld ldt) = W_kept Theta^{1/2}
+// from the Gram eigen-compression of Zc = [Z_fine | Z_coarse]; S = diag(wf I_kf, wc I_(k-kf)).
+// M = Tm^T S Tm (r1 x r1, symmetric indefinite) is diagonalised by parallel cyclic Jacobi
+// (round-robin pair ordering, one CTA), eigenvalues kept by |lambda| > tol max|lambda| in
+// descending |lambda|, and T2 = Tm Theta^{-1} U_kept (k x r2) is written so that
+// L = Zc T2 (orthonormal columns) and D = diag(lambda_kept) give P = L D L^T.
+constexpr int SC_MAX = 112;
+__global__ void __launch_bounds__(512) signed_core_kernel(const double* __restrict__ Tm, int64_t ldt,
+                                                          int k, int r1, int kf, double wf, double wc,
+                                                          double tol, double* __restrict__ T2,
+                                                          int64_t ldt2, double* __restrict__ lam,
+                                                          int* __restrict__ r2_out, int raw) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int n2 = (r1 + 1) & ~1;  // even number of players (one dummy when r1 is odd)
+  double* M = sm;                  // n2 x n2 (row-major, ld n2)
+  double* U = M + n2 * n2;         // n2 x n2
+  __shared__ double th[SC_MAX + 1], cs[SC_MAX / 2 + 1], sn[SC_MAX / 2 + 1], red[32];
+  __shared__ int pp[SC_MAX / 2 + 1], qq[SC_MAX / 2 + 1], perm[SC_MAX + 1];
+  __shared__ int s_stop, s_r2;
+  for (int j = tid; j < r1; j += nt) {
+    double a = 0.0;
+    for (int i = 0; i < k; ++i) a = fma(Tm[i + (size_t)j * ldt], Tm[i + (size_t)j * ldt], a);
+    th[j] = a;  // theta_j (W columns are unit vectors)
+  }
+  for (int e = tid; e < n2 * n2; e += nt) {
+    const int i = e / n2, j = e % n2;
+    double a = 0.0;
+    if (i < r1 && j < r1) {
+      for (int l = 0; l < k; ++l)
+        a = fma(Tm[l + (size_t)i * ldt] * (l < kf ? wf : wc), Tm[l + (size_t)j * ldt], a);
+    }
+    M[e] = a;
+    U[e] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < n2 * n2; e += nt) {  // exact symmetry
+    const int i = e / n2, j = e % n2;
+    if (i < j) {
+      const double v = 0.5 * (M[i * n2 + j] + M[j * n2 + i]);
+      M[i * n2 + j] = v;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < n2 * n2; e += nt) {
+    const int i = e / n2, j = e % n2;
+    if (i > j) M[i * n2 + j] = M[j * n2 + i];
+  }
+  __syncthreads();
+  const int half = n2 / 2;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    // convergence: off-diagonal mass relative to the diagonal
+    double off = 0.0, dia = 0.0;
+    for (int e = tid; e < n2 * n2; e += nt) {
+      const int i = e / n2, j = e % n2;
+      const double v = M[e] * M[e];
+      if (i == j) dia += v; else off += v;
+    }
+    for (int o = 16; o; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      dia += __shfl_xor_sync(0xffffffffu, dia, o);
+    }
+    if ((tid & 31) == 0) {
+      red[tid >> 5] = off;
+      red[16 + (tid >> 5)] = dia;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double o2 = 0.0, d2 = 0.0;
+      for (int w = 0; w < (nt >> 5); ++w) { o2 += red[w]; d2 += red[16 + w]; }
+      s_stop = o2 <= 1e-32 * d2;  // off-diagonal Frobenius mass below (1e-16)^2 of the diagonal
+    }
+    __syncthreads();
+    if (s_stop) break;
+    for (int round = 0; round < n2 - 1; ++round) {
+      if (tid < half) {  // round-robin: player 0 fixed, the others rotate
+        int a = tid == 0 ? 0 : 1 + (tid - 1 + round) % (n2 - 1);
+        int b = 1 + (n2 - 2 - tid + round) % (n2 - 1);
+        if (a > b) { const int t = a; a = b; b = t; }
+        pp[tid] = a;
+        qq[tid] = b;
+        double c = 1.0, sv = 0.0;
+        const double apq = M[a * n2 + b];
+        if (a < r1 && b < r1 && apq != 0.0) {
+          const double tau = (M[b * n2 + b] - M[a * n2 + a]) / (2.0 * apq);
+          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          sv = t * c;
+        }
+        cs[tid] = c;
+        sn[tid] = sv;
+      }
+      __syncthreads();
+      for (int e = tid; e < half * n2; e += nt) {  // rows p, q
+        const int pr = e / n2, j = e % n2;
+        const int a = pp[pr], b = qq[pr];
+        const double c = cs[pr], sv = sn[pr];
+        const double x = M[a * n2 + j], y = M[b * n2 + j];
+        M[a * n2 + j] = c * x - sv * y;
+        M[b * n2 + j] = sv * x + c * y;
+      }
+      __syncthreads();
+      for (int e = tid; e < half * n2; e += nt) {  // columns p, q of M and U
+        const int pr = e / n2, i = e % n2;
+        const int a = pp[pr], b = qq[pr];
+        const double c = cs[pr], sv = sn[pr];
+        const double x = M[i * n2 + a], y = M[i * n2 + b];
+        M[i * n2 + a] = c * x - sv * y;
+        M[i * n2 + b] = sv * x + c * y;
+        const double u = U[i * n2 + a], w = U[i * n2 + b];
+        U[i * n2 + a] = c * u - sv * w;
+        U[i * n2 + b] = sv * u + c * w;
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {  // order by |lambda| descending (stable), truncate
+    double mx = 0.0;
+    for (int i = 0; i < r1; ++i) { perm[i] = i; mx = fmax(mx, fabs(M[i * n2 + i])); }
+    for (int i = 1; i < r1; ++i) {
+      const int v = perm[i];
+      int j = i - 1;
+      while (j >= 0 && fabs(M[perm[j] * n2 + perm[j]]) < fabs(M[v * n2 + v])) { perm[j + 1] = perm[j]; --j; }
+      perm[j + 1] = v;
+    }
+    int r2 = 0;
+    while (r2 < r1 && mx > 0.0 && fabs(M[perm[r2] * n2 + perm[r2]]) > tol * mx) ++r2;
+    s_r2 = r2;
+    *r2_out = r2;
+    for (int c = 0; c < r2; ++c) lam[c] = M[perm[c] * n2 + perm[c]];
+  }
+  __syncthreads();
+  const int r2 = s_r2;
+  if (raw) {  // T2 = U_kept (r1 x r2): the caller's basis is already orthonormal
+    for (int e = tid; e < r1 * r2; e += nt) {
+      const int i = e % r1, c = e / r1;
+      T2[i + (size_t)c * ldt2] = U[i * n2 + perm[c]];
+    }
+  } else {
+    for (int e = tid; e < k * r2; e += nt) {  // T2 = Tm Theta^{-1} U_kept
+      const int i = e % k, c = e / k;
+      const int col = perm[c];
+      double a = 0.0;
+      for (int j = 0; j < r1; ++j) a = fma(Tm[i + (size_t)j * ldt] / th[j], U[j * n2 + col], a);
+      T2[i + (size_t)c * ldt2] = a;
+    }
+  }
+}
+
+void signed_core(const double* Tm, int64_t ldt, int k, int r1, int kf, double wf, double wc, double tol,
+                 double* T2, int64_t ldt2, double* lam, int* r2_dev, cudaStream_t st, bool raw) {
+  if (r1 <= 0) {
+    DME_CUDA(cudaMemsetAsync(r2_dev, 0, sizeof(int), st));
+    return;
+  }
+  if (r1 > SC_MAX) throw std::runtime_error("signed_core: rank of the combined factor exceeds 112");
+  const int n2 = (r1 + 1) & ~1;
+  const size_t smem = sizeof(double) * 2 * (size_t)n2 * n2;
+  static bool attr = false;
+  if (!attr) {
+    DME_CUDA(cudaFuncSetAttribute(signed_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * 2 * (SC_MAX + 1) * (SC_MAX + 1))));
+    attr = true;
+  }
+  signed_core_kernel<<<1, 512, smem, st>>>(Tm, ldt, k, r1, kf, wf, wc, tol, T2, ldt2, lam, r2_dev,
+                                            raw ? 1 : 0);
+  DME_KCHECK();
+}
+
 void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                 int64_t M, int64_t N, int64_t K, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;

@@ -36,6 +36,11 @@ void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, doub
 //   G = [[Gh_II, Gh_I,LA Tm], [Tm^T Gh_LA,I, Tm^T Gh_LA,LA Tm]]  (k = q + r, column-major, ld ldg)
 //   H = [Gh_I,B; Tm^T Gh_LA,B]  stored at G + k * ldg  (k x m)
 // One CTA; kp, r <= 224, q + m + kp <= 224.
+// Signed r1 x r1 core M = Tm^T S Tm of a Richardson combination (see aux.cu); r1 <= 112. Writes
+// lam (r2), *r2_dev and T2: raw = false: Tm Theta^{-1} U_kept (k x r2, Tm = W Theta^{1/2});
+// raw = true: U_kept (r1 x r2).
+void signed_core(const double* Tm, int64_t ldt, int k, int r1, int kf, double wf, double wc, double tol,
+                 double* T2, int64_t ldt2, double* lam, int* r2_dev, cudaStream_t st, bool raw);
 size_t gram_congruence_smem(int q, int m, int kp, int r);  // <= 220 KB required
 void gram_congruence(const double* Gh, int64_t ldh, int q, int m, int kp, const double* Tm,
                      int64_t ldt, int r, double* G, int64_t ldg, cudaStream_t st);

@@ -1381,6 +1381,106 @@ dme_status dme_get_factor(dme_ctx* c, int64_t* r, double* L, double* D, int64_t 
   });
 }
 
+dme_status dme_extrapolate(dme_ctx* fine, dme_ctx* coarse, int64_t* r, double* L, double* D,
+                           int64_t cap) {
+  if (!fine || !coarse) { g_last_error = "NULL ctx"; return DME_ERR_INVALID; }
+  return guarded(fine, [&] {
+    dme_ctx* c = fine;
+    dme_ctx* d = coarse;
+    DME_REQUIRE(r, DME_ERR_INVALID, "NULL r");
+    DME_REQUIRE(c != d && c->n == d->n && c->ldn == d->ldn && c->opt.device == d->opt.device,
+                DME_ERR_CONFIG, "fine and coarse must be two contexts of one problem on one device");
+    DME_REQUIRE(std::fabs(2.0 * c->h - d->h) <= 1e-12 * d->h, DME_ERR_CONFIG,
+                "the fine step must be half the coarse step");
+    DME_REQUIRE(c->stats.steps == 2 * d->stats.steps && d->stats.steps > 0, DME_ERR_CONFIG,
+                "the fine run must have taken twice the coarse run's steps (same time t > 0)");
+    const int64_t n = c->n, ld = c->ldn, kf = c->r, kc = d->r, k = kf + kc;
+    DME_REQUIRE(k <= KMAX, DME_ERR_DIM, "combined rank exceeds the factor capacity");
+    cudaStream_t st = c->st;
+    // both states ready, on the fine context's stream
+    DME_CUDA(cudaStreamSynchronize(d->st));
+    *r = 0;
+    if (k > 0) {
+      // Zc = [Z_fine | Z_coarse],  P = Zc S Zc^T,  S = diag(4/3 I, -1/3 I). A Gram-based basis
+      // loses ~eps kappa(Zc)^2 here (the two factors span nearly the same space: measured 5e-9
+      // in P), so the basis is built by classical Gram-Schmidt with reorthogonalisation (CGS2,
+      // backward stable like Householder for kappa < 1/eps): Q (n x r1) orthonormal, then
+      // R^T = Zc^T Q, the signed core M = R S R^T = U Lambda U^T, L = Q U_kept, D = Lambda_kept.
+      double* Zc = c->Zc2;
+      double* Q = c->Ztmp;
+      double* v = c->X2;          // init-only n x n scratch, free after init
+      double* w = c->X2 + ld;     // second column
+      double* hcol = c->Vg;       // Q^T v (KMAX)
+      double* nrm = c->norm_dev + 8;
+      copy_cols(Zc, ld, c->Z, ld, n, kf, 1.0, st);
+      copy_cols(Zc + kf * ld, ld, d->Z, ld, n, kc, 1.0, st);
+      int64_t r1 = 0;
+      for (int64_t j = 0; j < k; ++j) {
+        copy_cols(v, ld, Zc + j * ld, ld, n, 1, 1.0, st);
+        double z2 = 0.0;
+        {
+          GemmNTArgs g;
+          g.A = v; g.lda = ld; g.B = v; g.ldb = ld; g.M = 1; g.N = 1; g.K = n;
+          g.out = nrm; g.out_rs = 1; g.out_cs = 1;
+          gemm_nt(g, c->gs, st);
+          DME_CUDA(cudaMemcpyAsync(&z2, nrm, 8, cudaMemcpyDeviceToHost, st));
+        }
+        for (int pass = 0; pass < 2 && r1 > 0; ++pass) {  // v -= Q (Q^T v), twice
+          GemmNTArgs g;
+          g.A = Q; g.lda = ld; g.B = v; g.ldb = ld; g.M = r1; g.N = 1; g.K = n;
+          g.out = hcol; g.out_rs = 1; g.out_cs = KMAX;
+          gemm_nt(g, c->gs, st);
+          tall_small(Q, ld, hcol, KMAX, w, ld, n, 1, r1, st);
+          axpy_cols(v, ld, w, ld, n, 1, -1.0, st);
+        }
+        double v2 = 0.0;
+        {
+          GemmNTArgs g;
+          g.A = v; g.lda = ld; g.B = v; g.ldb = ld; g.M = 1; g.N = 1; g.K = n;
+          g.out = nrm; g.out_rs = 1; g.out_cs = 1;
+          gemm_nt(g, c->gs, st);
+          DME_CUDA(cudaMemcpyAsync(&v2, nrm, 8, cudaMemcpyDeviceToHost, st));
+          sync(c);
+        }
+        // a column inside span(Q) to working precision adds nothing (rank deficiency)
+        if (!(v2 > 1e-28 * z2) || !(v2 > 0.0)) continue;
+        copy_cols(Q + r1 * ld, ld, v, ld, n, 1, 1.0 / std::sqrt(v2), st);
+        ++r1;
+      }
+      DME_REQUIRE(r1 <= 112, DME_ERR_DIM, "combined rank exceeds 112");
+      // R^T = Zc^T Q (k x r1), as "Tm" of the signed core: M = Tm^T S Tm = R S R^T
+      {
+        GemmNTArgs g;
+        g.A = Zc; g.lda = ld; g.B = Q; g.ldb = ld; g.M = k; g.N = r1; g.K = n;
+        g.out = c->Tm; g.out_rs = 1; g.out_cs = KMAX;
+        gemm_nt(g, c->gs, st);
+      }
+      signed_core(c->Tm, KMAX, (int)k, (int)r1, (int)kf, 4.0 / 3.0, -1.0 / 3.0, c->opt.trunc_tol,
+                  c->Tm2, KMAX, c->H, c->r_dev + 1, st, true);
+      int r2 = 0;
+      DME_CUDA(cudaMemcpyAsync(&r2, c->r_dev + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+      sync(c);
+      *r = r2;
+      if (r2 > 0 && (L || D)) {
+        DME_REQUIRE(r2 <= cap, DME_ERR_CAPACITY, "factor has more columns than capacity_cols");
+        double* Lout = c->X4;  // init-only scratch
+        tall_small(Q, ld, c->Tm2, KMAX, Lout, ld, n, r2, r1, st);  // L = Q U_kept
+        std::vector<double> tmp((size_t)n * r2), lam(r2);
+        DME_CUDA(cudaMemcpy2DAsync(tmp.data(), n * 8, Lout, ld * 8, n * 8, r2,
+                                   cudaMemcpyDeviceToHost, st));
+        DME_CUDA(cudaMemcpyAsync(lam.data(), c->H, r2 * 8, cudaMemcpyDeviceToHost, st));
+        sync(c);
+        if (L)
+          for (int64_t j = 0; j < r2; ++j)
+            for (int64_t i = 0; i < n; ++i) L[i * r2 + j] = tmp[(size_t)j * n + i];
+        if (D)
+          for (int64_t i = 0; i < r2; ++i)
+            for (int64_t j = 0; j < r2; ++j) D[i * r2 + j] = i == j ? lam[i] : 0.0;
+      }
+    }
+  });
+}
+
 dme_status dme_get_stats(dme_ctx* c, dme_stats* st) {
   if (!c || !st) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
   return guarded(c, [&] {
