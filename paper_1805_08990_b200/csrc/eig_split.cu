@@ -55,10 +55,55 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
   __syncthreads();
   tridiagonalise<FK>(A, k, ld, d, e, tau, vec, pv, pv2);
   const long long t1 = clock64();
-  if (tid == 0) {
-    normalise_tridiagonal(k, d, e, e2, &s_scale, &s_lo, &s_hi);
-    s_lo_t = s_lo;
-    s_hi_t = s_hi;
+  {
+    // normalise T by a Gershgorin bound of ||T|| (same arithmetic as normalise_tridiagonal, in
+    // parallel: one row per thread, block max/min reductions)
+    __shared__ double rmax[NW], rlo[NW], rhi[NW];
+    const int lane = tid & 31, warp = tid >> 5;
+    double rr = 0.0, di = 0.0;
+    if (tid < k) {
+      di = d[tid];
+      rr = (tid > 0 ? fabs(e[tid - 1]) : 0.0) + (tid + 1 < k ? fabs(e[tid]) : 0.0);
+    }
+    double m = tid < k ? fabs(di) + rr : 0.0;
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) rmax[warp] = m;
+    __syncthreads();
+    double nrm = 0.0;
+    for (int w = 0; w < NW; ++w) nrm = fmax(nrm, rmax[w]);
+    if (!(nrm > 0.0)) nrm = 1.0;
+    const double inv = 1.0 / nrm;
+    __syncthreads();  // every thread has read the old d, e
+    if (tid < k) {
+      d[tid] = di * inv;
+      if (tid + 1 < k) {
+        const double en = e[tid] * inv;
+        e[tid] = en;
+        e2[tid] = en * en;
+      }
+    }
+    __syncthreads();
+    double lo = 1e300, hi = -1e300;
+    if (tid < k) {
+      const double r2 = (tid > 0 ? fabs(e[tid - 1]) : 0.0) + (tid + 1 < k ? fabs(e[tid]) : 0.0);
+      lo = d[tid] - r2;
+      hi = d[tid] + r2;
+    }
+    for (int o = 16; o; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) { rlo[warp] = lo; rhi[warp] = hi; }
+    __syncthreads();
+    if (tid == 0) {
+      double l2 = 1e300, h2 = -1e300;
+      for (int w = 0; w < NW; ++w) { l2 = fmin(l2, rlo[w]); h2 = fmax(h2, rhi[w]); }
+      s_scale = nrm;
+      s_lo = l2 - 1e-14;
+      s_hi = h2 + 1e-14;
+      s_lo_t = s_lo;
+      s_hi_t = s_hi;
+    }
   }
   __syncthreads();
   // theta_max to 16 bits (enough for the threshold; it is refined with the others in VEC)
