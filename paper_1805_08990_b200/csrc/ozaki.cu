@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(224, 1)
     if (lane == 0) {  // ---------------------------------------- TMA producers: A (warp 0), B (warp 6)
       const bool isA = warp == 0;
       if (isA) prefetch_tmap(&tmA); else prefetch_tmap(&tmB);
+      const uint64_t l2_first = policy_evict_first();  // E digits: streamed once per pass
       int as = 0, bs = 0;
       uint32_t pa = 0, pb = 0;
       SegIter it(rr != 0, ntiles, nkc);
@@ -225,10 +226,10 @@ __global__ void __launch_bounds__(224, 1)
           for (int a = 0; a < S; ++a) {
             mbar_wait(empty_a + as, pa ^ 1);
             mbar_arrive_expect_tx(full_a + as, C::AST);
-            if (a_tiled)  // pre-swizzled tile image: one contiguous 16 KB bulk copy
-              bulk_load(As + as * C::AST,
-                        a_tiled + (((size_t)rt * nkc + kc) * S + a) * (size_t)C::AST, C::AST,
-                        full_a + as);
+            if (a_tiled)  // pre-swizzled tile image: one contiguous 16 KB bulk copy, read once
+              bulk_load_hint(As + as * C::AST,
+                             a_tiled + (((size_t)rt * nkc + kc) * S + a) * (size_t)C::AST, C::AST,
+                             full_a + as, l2_first);
             else
               tma_load_3d(As + as * C::AST, &tmA, full_a + as, kc * 128, rt * 128, a);
             if (++as == C::NA) { as = 0; pa ^= 1; }
