@@ -20,19 +20,28 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
   bool neg_prev = p1 <= 0.0;
   int cnt = neg_prev;
   int i = 1;
-  for (; i + 3 < k; i += 4) {
-    const double d0 = d[i], d1 = d[i + 1], d2 = d[i + 2], d3 = d[i + 3];
-    const double f0 = e2[i - 1], f1 = e2[i], f2 = e2[i + 1], f3 = e2[i + 2];
-    double p;
-    bool ng;
-    p = fma(d0 - x, p1, -f0 * p2); ng = p <= 0.0; cnt += ng != neg_prev; neg_prev = ng; p2 = p1; p1 = p;
-    p = fma(d1 - x, p1, -f1 * p2); ng = p <= 0.0; cnt += ng != neg_prev; neg_prev = ng; p2 = p1; p1 = p;
-    p = fma(d2 - x, p1, -f2 * p2); ng = p <= 0.0; cnt += ng != neg_prev; neg_prev = ng; p2 = p1; p1 = p;
-    p = fma(d3 - x, p1, -f3 * p2); ng = p <= 0.0; cnt += ng != neg_prev; neg_prev = ng; p2 = p1; p1 = p;
-    // growth per element <= 3 (||T|| <= 1): rescale rarely, by an exact power of two
+  // blocks of 8: the loads are independent of the recurrence and issue ahead of it; the exact
+  // power-of-two rescaling is checked once per block (|p| grows <= 3^8 per block for ||T|| <= 1,
+  // and a block cannot underflow from 2^-300 to below the normal range)
+  for (; i + 7 < k; i += 8) {
+    double dd[8], ff[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      dd[u] = d[i + u] - x;
+      ff[u] = e2[i - 1 + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double p = fma(dd[u], p1, -ff[u] * p2);
+      const bool ng = p <= 0.0;
+      cnt += ng != neg_prev;
+      neg_prev = ng;
+      p2 = p1;
+      p1 = p;
+    }
     const double m1 = fmax(fabs(p1), fabs(p2));
-    if (m1 > 0x1p400) { p1 *= 0x1p-400; p2 *= 0x1p-400; }
-    else if (m1 < 0x1p-400) { p1 *= 0x1p400; p2 *= 0x1p400; }
+    if (m1 > 0x1p300) { p1 *= 0x1p-300; p2 *= 0x1p-300; }
+    else if (m1 < 0x1p-300) { p1 *= 0x1p300; p2 *= 0x1p300; }
   }
   for (; i < k; ++i) {
     const double p = fma(d[i] - x, p1, -e2[i - 1] * p2);
