@@ -339,10 +339,20 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
         }
         am[mm] = sv;
       }
+      {  // transposed butterfly: 4 warp sums with 10 double shuffles instead of 20
+        const bool b4 = lane & 16, b3 = lane & 8;
+        double k0 = b4 ? am[2] : am[0], k1 = b4 ? am[3] : am[1];
+        const double s0 = b4 ? am[0] : am[2], s1 = b4 ? am[1] : am[3];
+        k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+        k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+        double kk = b3 ? k1 : k0;
+        kk += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 1);
 #pragma unroll
-      for (int o = 16; o; o >>= 1)
-#pragma unroll
-        for (int mm = 0; mm < 4; ++mm) am[mm] += __shfl_xor_sync(0xffffffffu, am[mm], o);
+        for (int mm = 0; mm < 4; ++mm) am[mm] = __shfl_sync(0xffffffffu, kk, (mm >> 1) * 16 + (mm & 1) * 8);
+      }
       const double* cp = cpair + b * 6;
       const double t0 = tau[jt], t1 = jt >= 1 ? tau[jt - 1] : 0.0;
       const double t2 = jt >= 2 ? tau[jt - 2] : 0.0, t3 = jt >= 3 ? tau[jt - 3] : 0.0;
