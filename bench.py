@@ -340,6 +340,42 @@ def run_ours(args):
         del s3
         torch.cuda.empty_cache()
 
+    # ------------------------------------------------------------ sparse-A variant
+    sparse = None
+    if not args.no_sparse and args.config == 5 and world == 1:
+        import scipy.sparse as sps
+        A_csr = sps.csr_matrix(prob.A)  # host CSR (the caller's sparse matrix)
+        kw_sp = dict(dme.problem_kwargs(prob), A=A_csr)
+        torch.cuda.synchronize()
+        t4 = time.perf_counter()
+        s4 = dme.Solver(**kw_sp, **kw)
+        torch.cuda.synchronize()
+        init4 = time.perf_counter() - t4
+        s4.split_step("strang", "F12F3", args.warmup)
+        torch.cuda.synchronize()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(s4.stream)
+        s4.split_step("strang", "F12F3", args.steps)
+        v1.record(s4.stream)
+        torch.cuda.synchronize()
+        ms4 = v0.elapsed_time(v1)
+        s4.set_profiling(True)
+        s4.split_step("strang", "F12F3", args.steps)
+        torch.cuda.synchronize()
+        st4 = s4.stats()
+        sparse = {"e_pass": "sparse A (CSR, 5-point stencil): Chebyshev action of exp(tau A^T) on the "
+                            "Gershgorin interval, one 8-CTA cluster per column group, vectors in "
+                            "distributed shared memory; no dense exponential (DESIGN.md 9c)",
+                  "value": args.steps / (ms4 * 1e-3), "unit": UNIT, "ms_per_step": ms4 / args.steps,
+                  "init_s_from_host_csr": init4,
+                  "time_to_T_s": init4 + NT * ms4 / args.steps * 1e-3,
+                  "cheb_degree_E_h": st4["cheb_degree"],
+                  "action_us_per_launch": 1e6 * st4["prof_epass_seconds"] / max(st4["prof_passes"], 1),
+                  "action_fp64_gflops": (st4["prof_epass_flops"] / st4["prof_epass_seconds"] / 1e9
+                                         if st4["prof_epass_seconds"] > 0 else None)}
+        s4.close()
+        del s4
+
     cb = None
     if args.config != 5:  # the oracle's dense E for a nonsymmetric A M^-1 takes minutes: not a bounded sample
         cb = {"skipped": "cpu_baseline is reported for the headline workload (config 5) only"}
@@ -374,7 +410,7 @@ def run_ours(args):
                 "init_s": init_wall, "init_lib_s": init_dev,
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(),
-                "fp64_dmma_variant": variant}
+                "fp64_dmma_variant": variant, "sparse_variant": sparse}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -393,6 +429,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variant", action="store_true", help="skip the native-FP64 E-pass run")
+    ap.add_argument("--no-sparse", action="store_true", help="skip the sparse-A (Chebyshev) run")
     args = ap.parse_args()
     if args.nx is None:
         args.nx = 100 if args.config == 5 else 70

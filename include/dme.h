@@ -75,7 +75,7 @@ typedef enum {
 
 typedef struct {
   int64_t n;          /* state dimension                                                    */
-  const double* A;    /* n x n                                                              */
+  const double* A;    /* n x n row-major (NULL with a sparse A, see A_rowptr below)         */
   int64_t p;          /* rows of C (p >= 0); Q = C^T C                                      */
   const double* C;    /* p x n (NULL iff p == 0)                                            */
   int64_t m;          /* columns of B; 0 for a DLE                                          */
@@ -93,6 +93,21 @@ typedef struct {
                          it, e.g. SPD mass matrices; DME_ERR_NUMERIC on a tiny pivot).
                          Same memory space as A (host, or device with big_inputs_on_device).
                          Callers that zero-initialise the struct get M = NULL.              */
+  /* Sparse A (the paper's own setting, P:L199 / P:L303-307: exp(tau A^T) L as a
+     polynomial in the sparse A, no dense matrix exponential). Used when A == NULL and
+     A_rowptr != NULL: A in CSR form (host arrays, 0-based, row-major: row i holds entries
+     A_colind[e], A_values[e] for e in [A_rowptr[i], A_rowptr[i+1]); duplicates are summed).
+     A must be exactly symmetric (DME_ERR_CONFIG otherwise). Every E_tau L action is then a
+     Chebyshev expansion of exp on the Gershgorin interval of tau A^T (truncation tail <= 2^-56,
+     degree fixed at init), the quadrature rule is unchanged (its panel count
+     still comes from ||(h/2) A^T||_1), and init builds no n x n matrix. n x (row width) must fit
+     the shared memory of one 8-CTA cluster (DME_ERR_DIM otherwise; n = 10^4 with a 5-point
+     stencil fits). Not combinable with M or with world_size > 1 (DME_ERR_CONFIG).
+     Callers that zero-initialise the struct get the dense path.                          */
+  int64_t A_nnz;
+  const int64_t* A_rowptr; /* n + 1 */
+  const int32_t* A_colind; /* A_nnz */
+  const double* A_values;  /* A_nnz */
 } dme_problem;
 
 typedef struct {
@@ -153,6 +168,7 @@ typedef struct {
   int64_t eig_fallbacks;    /* fast eigen-compressions that failed the orthogonality check and
                                were redone by the Jacobi kernel                                 */
   int64_t ozaki_passes;     /* E passes run on the int8 tensor cores (options.e_pass)          */
+  int64_t cheb_degree;      /* sparse A: polynomial degree of the E_h action (sum over substeps) */
 } dme_stats;
 
 void dme_default_options(dme_options* opt);
@@ -198,6 +214,12 @@ dme_status dme_extrapolate(dme_ctx* fine, dme_ctx* coarse, int64_t* r, double* L
 dme_status dme_get_stats(dme_ctx* ctx, dme_stats* st);
 /* Turn CUDA-event timing of the kernel classes on (1) or off (0); resets the prof_* counters. */
 dme_status dme_set_profiling(dme_ctx* ctx, int32_t on);
+/* Sparse-A path, host only (no device): chat[k] = e^{-gamma} I_k(gamma) for k = 0..*K, the
+ * Chebyshev coefficients of e^{gamma (x - 1)} on [-1, 1] (modified Bessel functions, Miller's
+ * backward recurrence normalised by I_0 + 2 sum I_k = e^gamma); *K is the smallest degree with
+ * 2 sum_{j > K} chat[j] <= tol. out holds cap doubles (DME_ERR_CAPACITY if K + 1 > cap). */
+dme_status dme_cheb_coeffs(double gamma, double tol, double* out, int64_t cap, int32_t* K);
+
 dme_status dme_destroy(dme_ctx* ctx);
 
 /* ---- test hooks (same semantics as the step, one flow at a time) ----------------------------- */

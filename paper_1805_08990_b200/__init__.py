@@ -37,7 +37,9 @@ _dp = ctypes.POINTER(ctypes.c_double)
 class _Problem(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("A", _dp), ("p", ctypes.c_int64), ("C", _dp),
                 ("m", ctypes.c_int64), ("B", _dp), ("R", _dp), ("S", _dp),
-                ("r0", ctypes.c_int64), ("L0", _dp), ("D0", _dp), ("M", _dp)]
+                ("r0", ctypes.c_int64), ("L0", _dp), ("D0", _dp), ("M", _dp),
+                ("A_nnz", ctypes.c_int64), ("A_rowptr", ctypes.POINTER(ctypes.c_int64)),
+                ("A_colind", ctypes.POINTER(ctypes.c_int32)), ("A_values", _dp)]
 
 
 class _Options(ctypes.Structure):
@@ -63,7 +65,7 @@ class _Stats(ctypes.Structure):
                 ("prof_epass_flops", ctypes.c_double), ("prof_epass_bytes", ctypes.c_double),
                 ("prof_gram_seconds", ctypes.c_double), ("prof_small_seconds", ctypes.c_double),
                 ("prof_apply_seconds", ctypes.c_double), ("eig_fallbacks", ctypes.c_int64),
-                ("ozaki_passes", ctypes.c_int64)]
+                ("ozaki_passes", ctypes.c_int64), ("cheb_degree", ctypes.c_int64)]
 
 
 _ctx_p = ctypes.c_void_p
@@ -92,6 +94,8 @@ for _name, _args in {
     "dme_debug_matmul": [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp],
     "dme_debug_matmul_ozaki": [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp],
     "dme_debug_small_stats": [_ctx_p, _dp],
+    "dme_cheb_coeffs": [ctypes.c_double, ctypes.c_double, _dp, ctypes.c_int64,
+                        ctypes.POINTER(ctypes.c_int32)],
 }.items():
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = ctypes.c_int
@@ -100,7 +104,7 @@ EXPORTED = ["dme_default_options", "dme_status_string", "dme_last_error", "dme_w
             "dme_get_unique_id", "dme_shard_rows", "dme_dle_init", "dme_dre_init", "dme_split_step",
             "dme_get_factor", "dme_extrapolate", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
             "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_get_integral",
-            "dme_debug_small_stats", "dme_debug_matmul", "dme_debug_matmul_ozaki"]
+            "dme_debug_small_stats", "dme_debug_matmul", "dme_debug_matmul_ozaki", "dme_cheb_coeffs"]
 
 
 class DmeError(RuntimeError):
@@ -153,6 +157,19 @@ def unique_id() -> bytes:
 E_PASS = {"auto": 0, "dmma": 1}
 
 
+def cheb_coeffs(gamma: float, tol: float = 2.0 ** -56) -> np.ndarray:
+    """Host routine of the sparse-A path: e^{-gamma} I_k(gamma), k = 0..K, K the degree whose
+    coefficient tail 2 sum_{j>K} is <= tol (dme_cheb_coeffs; no device needed)."""
+    out = np.zeros(4096)
+    K = ctypes.c_int32(0)
+    _check(_lib.dme_cheb_coeffs(gamma, tol, _ptr(out), out.size, ctypes.byref(K)), "dme_cheb_coeffs")
+    return out[:K.value + 1].copy()
+
+
+def _is_sparse(A) -> bool:
+    return hasattr(A, "tocsr") and hasattr(A, "nnz")
+
+
 class Solver:
     """One problem on one GPU (or one rank of a row-sharded multi-GPU run)."""
 
@@ -169,7 +186,16 @@ class Solver:
         self.device = dev
         # A and S may be CUDA tensors (float64, contiguous): then they are read device-to-device
         on_dev = isinstance(A, torch.Tensor) and A.is_cuda
-        if on_dev:
+        sparse = _is_sparse(A)
+        if sparse:  # CSR host arrays; the library builds its device layout from them
+            csr = A.tocsr()
+            self._csr = (np.ascontiguousarray(csr.indptr, dtype=np.int64),
+                         np.ascontiguousarray(csr.indices, dtype=np.int32),
+                         np.ascontiguousarray(csr.data, dtype=np.float64))
+            self._keep = [None, _f64(C), _f64(B), _f64(R), _f64(S), _f64(L0), _f64(D0), _f64(M)]
+            A_, C_, B_, R_, S_, L0_, D0_, M_ = self._keep
+            pA, pS, pM = None, _ptr(S_), _ptr(M_)
+        elif on_dev:
             if A.dtype != torch.float64 or not A.is_contiguous():
                 raise ValueError("device A must be a contiguous float64 CUDA tensor")
             if S is not None and not (isinstance(S, torch.Tensor) and S.is_cuda and
@@ -186,11 +212,17 @@ class Solver:
             self._keep = [_f64(A), _f64(C), _f64(B), _f64(R), _f64(S), _f64(L0), _f64(D0), _f64(M)]
             A_, C_, B_, R_, S_, L0_, D0_, M_ = self._keep
             pA, pS, pM = _ptr(A_), _ptr(S_), _ptr(M_)
-        n = A_.shape[0]
+        n = A.shape[0]
         self.n = n
         pr = _Problem(n=n, A=pA, p=0 if C_ is None else C_.shape[0], C=_ptr(C_),
                       m=0 if B_ is None else B_.shape[1], B=_ptr(B_), R=_ptr(R_), S=pS,
                       r0=0 if L0_ is None else L0_.shape[1], L0=_ptr(L0_), D0=_ptr(D0_), M=pM)
+        if sparse:
+            rp, ci, vv = self._csr
+            pr.A_nnz = vv.size
+            pr.A_rowptr = rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+            pr.A_colind = ci.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            pr.A_values = _ptr(vv)
         self._pr = pr
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
         uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid is not None else None

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdme.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["gemm_nt.cu", "ozaki.cu", "small.cu", "eig_fast.cu", "eig_split.cu", "aux.cu", "lu.cu", "dme.cu"]
+SOURCES = ["gemm_nt.cu", "ozaki.cu", "cheb.cu", "small.cu", "eig_fast.cu", "eig_split.cu", "aux.cu", "lu.cu", "dme.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

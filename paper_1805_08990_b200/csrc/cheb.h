@@ -1,0 +1,62 @@
+// Sparse exponential action exp(tau A^T) X for a sparse symmetric A (the paper's
+// own kernel class, "expleja", P:L199 / P:L303-307: a polynomial in A built from sparse
+// matrix x skinny-matrix products, one-time spectrum estimate by Gershgorin discs).
+//
+// Polynomial: Chebyshev expansion of exp on the Gershgorin interval [a, b] of tau A^T,
+//   exp(tau A^T) = e^{c} sum'_k 2 I_k(gamma) T_k(Xs),   Xs = (tau A^T - c I) / gamma,
+//   c = tau (a + b) / 2, gamma = tau (b - a) / 2,
+// with the degree K fixed a priori from the coefficient tail (no norm reductions in the loop).
+// For a symmetric A the truncation error is <= tail * ||X|| (spectrum inside [a, b]).
+//
+// Device layout (cheb.cu): A^T in ELL form, partitioned over the CHEB_CLUSTER CTAs of a thread-block
+// cluster (rows [r R, (r + 1) R) on CTA r); one cluster per group of C columns of X. The three
+// Chebyshev vectors live in the cluster's distributed shared memory; neighbours' rows are gathered
+// with ld.shared::cluster, one cluster barrier per polynomial degree.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dme {
+
+constexpr int CHEB_CLUSTER = 8;
+constexpr int CHEB_KMAX = 640;     // polynomial degree per substep (coefficients are kernel params)
+constexpr int CHEB_THREADS = 512;
+constexpr int CHEB_CMAX = 8;       // columns per cluster
+
+struct ChebOp {
+  int64_t n = 0, R = 0;   // rows, rows per CTA (n <= CHEB_CLUSTER * R)
+  int w = 0;              // ELL width (max nonzeros per row of A^T)
+  int C = 0;              // columns per cluster (shared-memory budget)
+  double a = 0, b = 0;    // Gershgorin interval of A^T
+  double norm1 = 0;       // ||A^T||_1
+  double* val = nullptr;  // [w][CHEB_CLUSTER * R] (device)
+  uint32_t* idx = nullptr;  // [w][CHEB_CLUSTER * R]: (owner CTA << 24) | row within the owner
+};
+
+// Host: from the CSR of A (0-based, n x n) build the partitioned ELL of A^T and the Gershgorin data.
+// Returns 0, or a dme_status code with *err set: DME_ERR_INVALID (bad CSR / non-finite values),
+// DME_ERR_CONFIG (A not exactly symmetric), DME_ERR_DIM (the layout does not fit a cluster).
+struct ChebHost {
+  int64_t n = 0, R = 0, nnz = 0;  // nnz: stored entries of A^T (duplicates merged)
+  int w = 0, C = 0;
+  double a = 0, b = 0, norm1 = 0;
+  std::vector<double> val;
+  std::vector<uint32_t> idx;
+};
+int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* colind,
+                 const double* values, ChebHost& out, std::string* err);
+size_t cheb_smem_bytes(int64_t R, int w, int C);
+
+// chat[k] = e^{-gamma} I_k(gamma), k = 0..K, with K the smallest degree whose tail
+// 2 sum_{j > K} chat[j] <= tol. Returns K (chat resized to K + 1). Miller's backward recurrence,
+// normalised by e^{gamma} = I_0 + 2 sum I_k (all terms positive).
+int cheb_coeffs(double gamma, double tol, std::vector<double>& chat);
+
+// out[:, j] = alpha * exp(tau A^T) X[:, j], j < k (column-major, leading dims ldx / ldo; out != X).
+// Returns the total polynomial degree applied (sum over substeps).
+int cheb_action(const ChebOp& op, double tau, const double* X, int64_t ldx, int64_t k, double* out,
+                int64_t ldo, double alpha, cudaStream_t st);
+
+}  // namespace dme

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "aux.h"
+#include "cheb.h"
 #include "common.cuh"
 #include "dme.h"
 #include "gemm_nt.h"
@@ -151,6 +152,10 @@ struct dme_ctx {
   bool force_jacobi = false;
   bool symA = false;  // A == A^T exactly (host check): symmetric Padé products
   bool fsal = true;
+  // sparse A: Chebyshev exponential actions instead of dense E (cheb.h)
+  bool sparse = false;
+  ChebHost chost;
+  ChebOp cop;
   ncclComm_t comm = nullptr;
   // profiling: (start, stop, class, flops, bytes) event records drained at sync points
   bool profile = false;
@@ -177,8 +182,16 @@ namespace {
 void plan_buffers(dme_ctx* c, Planner& P) {
   const int64_t n = c->n, ld = c->ldn;
   const size_t nn = (size_t)n * ld, fk = (size_t)ld * KMAX;
-  c->E_half = P.take<double>(nn);
-  c->E_full = P.take<double>(nn);
+  if (!c->sparse) {
+    c->E_half = P.take<double>(nn);
+    c->E_full = P.take<double>(nn);
+  } else {  // partitioned ELL of A^T (cheb.h); no n x n matrix in sparse mode
+    const size_t ell = (size_t)c->chost.w * CHEB_CLUSTER * c->chost.R;
+    c->cop.n = c->chost.n; c->cop.R = c->chost.R; c->cop.w = c->chost.w; c->cop.C = c->chost.C;
+    c->cop.a = c->chost.a; c->cop.b = c->chost.b; c->cop.norm1 = c->chost.norm1;
+    c->cop.val = P.take<double>(ell);
+    c->cop.idx = P.take<uint32_t>(ell);
+  }
   if (c->has_S) c->S = P.take<double>(nn);
   c->Bcol = P.take<double>((size_t)ld * std::max<int64_t>(c->m, 1));
   c->LQ = P.take<double>((size_t)ld * std::max<int64_t>(c->p, 1));
@@ -247,17 +260,19 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   }
   if (c->world > 1) c->stage = P.take<double>((size_t)c->world * c->nloc * KMAX);
   // init-only
-  c->Aup = P.take<double>(nn);
-  c->X0 = P.take<double>(nn);
-  c->BT = P.take<double>(nn);
-  c->X2 = P.take<double>(nn);
-  c->X4 = P.take<double>(nn);
-  c->X6 = P.take<double>(nn);
-  c->T1 = P.take<double>(nn);
-  c->U = P.take<double>(nn);
-  c->V = P.take<double>(nn);
-  c->lu_scr = P.take<double>(lu_scratch_doubles(n));
-  c->Wa = P.take<double>((size_t)ld * std::max<int64_t>(c->p, 1));
+  if (!c->sparse) {
+    c->Aup = P.take<double>(nn);
+    c->X0 = P.take<double>(nn);
+    c->BT = P.take<double>(nn);
+    c->X2 = P.take<double>(nn);
+    c->X4 = P.take<double>(nn);
+    c->X6 = P.take<double>(nn);
+    c->T1 = P.take<double>(nn);
+    c->U = P.take<double>(nn);
+    c->V = P.take<double>(nn);
+    c->lu_scr = P.take<double>(lu_scratch_doubles(n));
+  }
+  c->Wa = P.take<double>((size_t)ld * std::max<int64_t>(std::max(c->p, c->m), 1));
   c->Wb = P.take<double>((size_t)ld * std::max<int64_t>(c->p, 1));
   c->Yn = P.take<double>((size_t)ld * std::max<int64_t>(c->p * c->qn, 1));
   c->L0d = P.take<double>((size_t)ld * std::max<int64_t>(c->r0, 1));
@@ -289,8 +304,14 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->rank_cap = (int32_t)std::min<int64_t>(cap, KMAX);
   c->h = o->h;
   c->fsal = o->no_fsal == 0;
+  c->sparse = pr->A == nullptr && pr->A_rowptr != nullptr;
+  if (c->sparse) {
+    std::string err;
+    const int code = cheb_prepare(pr->n, pr->A_nnz, pr->A_rowptr, pr->A_colind, pr->A_values, c->chost, &err);
+    if (code) throw DmeError((dme_status)code, err);
+  }
   // E pass on the int8 tensor cores (exact digit slicing) unless disabled or out of its range
-  c->oz = o->e_pass != DME_EPASS_DMMA && c->n <= OZ_KMAX && c->rows_loc > 0;
+  c->oz = !c->sparse && o->e_pass != DME_EPASS_DMMA && c->n <= OZ_KMAX && c->rows_loc > 0;
   // the Padé products and squarings on the int8 tensor cores too (digits of both operands live
   // in the E-digit buffers until E is sliced; the init is replicated on every rank, local work)
   c->oz_init = c->oz;
@@ -304,7 +325,12 @@ bool all_finite(const double* x, size_t cnt) {
 
 void validate(const dme_problem* pr, const dme_options* o, bool dre) {
   DME_REQUIRE(pr && o, DME_ERR_INVALID, "NULL problem or options");
-  DME_REQUIRE(pr->n > 0 && pr->A, DME_ERR_INVALID, "n must be positive and A non-NULL");
+  DME_REQUIRE(pr->n > 0 && (pr->A || pr->A_rowptr), DME_ERR_INVALID,
+              "n must be positive and A (dense) or A_rowptr (sparse) non-NULL");
+  if (!pr->A) {
+    DME_REQUIRE(!pr->M, DME_ERR_CONFIG, "a mass matrix M is not supported with a sparse A");
+    DME_REQUIRE(o->world_size <= 1, DME_ERR_CONFIG, "a sparse A runs on one GPU (world_size 1)");
+  }
   DME_REQUIRE(std::isfinite(o->h) && o->h > 0, DME_ERR_INVALID, "h must be positive and finite");
   DME_REQUIRE(pr->p >= 0 && (pr->p == 0 || pr->C), DME_ERR_INVALID, "C must be non-NULL when p > 0");
   DME_REQUIRE(pr->r0 >= 0 && (pr->r0 == 0 || pr->L0), DME_ERR_INVALID, "L0 must be non-NULL when r0 > 0");
@@ -537,6 +563,32 @@ void epass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out,
   epass_on(c, E, X, k, out, ldo, alpha, c->st, c->gs);
 }
 
+// out = exp(tau A^T) X for a sparse A: Chebyshev action (cheb.h), on chip in one cluster per
+// column group. Profiled as the E pass; algorithmic work per degree and column: 2 nnz + 6 n flops.
+void sparse_pass(dme_ctx* c, double tau, const double* X, int64_t k, double* out, int64_t ldo,
+                 cudaStream_t st) {
+  if (k <= 0) return;
+  c->stats.e_passes++;
+  const double bytes = 16.0 * c->n * k + 12.0 * c->cop.w * CHEB_CLUSTER * c->cop.R;
+  ProfScope ps(c, PROF_EPASS, 0.0, bytes, st);
+  const int deg = cheb_action(c->cop, tau, X, c->ldn, k, out, ldo, 1.0, st);
+  ps.r.flops = (double)deg * k * (2.0 * c->chost.nnz + 6.0 * c->n);
+  if (tau == c->h) c->stats.cheb_degree = deg;
+}
+
+// out = E_tau X, tau = h (full) or h/2: the dense E pass or the sparse Chebyshev action
+void eact_on(dme_ctx* c, bool full, const double* X, int64_t k, double* out, int64_t ldo,
+             cudaStream_t st, GemmScratch& gs) {
+  if (c->sparse) {
+    sparse_pass(c, full ? c->h : c->h / 2, X, k, out, ldo, st);
+    return;
+  }
+  epass_on(c, full ? c->E_full : c->E_half, X, k, out, ldo, 1.0, st, gs);
+}
+void eact(dme_ctx* c, bool full, const double* X, int64_t k, double* out, int64_t ldo) {
+  eact_on(c, full, X, k, out, ldo, c->st, c->gs);
+}
+
 // Launch the Gram matrix (extended by B when T3 is fused: the B columns are copied next to the
 // factor, so G_ext = [Zc, B]^T [Zc, B] yields G and H = Zc^T B in one pass) and the small kernel.
 // Zc must have KMAX columns of capacity.
@@ -669,8 +721,7 @@ int64_t compress(dme_ctx* c, double* Zc, int64_t k, double* out, bool t3, double
 void swapZ(dme_ctx* c) { std::swap(c->Z, c->Ztmp); }
 
 void flow_T1(dme_ctx* c, double tau) {
-  const double* E = (tau == c->h) ? c->E_full : c->E_half;
-  epass(c, E, c->Z, c->r, c->Ztmp, c->ldn, 1.0);
+  eact(c, tau == c->h, c->Z, c->r, c->Ztmp, c->ldn);
   swapZ(c);
 }
 
@@ -690,7 +741,7 @@ void flow_T12(dme_ctx* c, double tau, bool t3, double tau3) {
   const bool full = (tau == c->h);
   double* Zc = full ? c->Zc12f : c->Zc12h;
   const int64_t q = full ? c->qf : c->qh;
-  epass(c, full ? c->E_full : c->E_half, c->Z, c->r, Zc + q * c->ldn, c->ldn, 1.0);
+  eact(c, full, c->Z, c->r, Zc + q * c->ldn, c->ldn);
   finish_compress(c, Zc, q + c->r, t3, tau3);
 }
 
@@ -793,7 +844,7 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
   const int64_t ld = c->ldn, q = c->qf, n = c->n, m = c->m;
   double* Zc = c->Zc12f;
   double* Tmb[2] = {c->Tm, c->Tm2};
-  epass(c, c->E_full, c->Z, c->r, Zc + q * ld, ld, 1.0);  // Y_0 = E_h Z
+  eact(c, true, c->Z, c->r, Zc + q * ld, ld);  // Y_0 = E_h Z
   const int rc = (int)std::min<int64_t>(c->rank_cap, n);  // bound on every rank of the body
   const bool pipe = c->lookahead && nb > 1 && 2 * q + m + rc <= KMAX &&
                     gram_congruence_smem((int)q, (int)m, (int)(q + rc), rc) <= 220 * 1024;
@@ -804,7 +855,7 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
   compress_launch(c, Zc, q + r_prev, true, h, true, a, fast, c->ev_gram, Tmb[0]);
   if (pipe) {  // second stream: E_h Y_0 into GB, Ghat_0
     DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_gram, 0));
-    epass_on(c, c->E_full, Zc + q * ld, r_prev, c->GB + (2 * q + m) * ld, ld, 1.0, c->st2, c->gs2);
+    eact_on(c, true, Zc + q * ld, r_prev, c->GB + (2 * q + m) * ld, ld, c->st2, c->gs2);
     GemmNTArgs g;
     g.A = c->GB; g.lda = ld; g.B = c->GB; g.ldb = ld;
     g.M = g.N = 2 * q + m + r_prev; g.K = n;
@@ -835,7 +886,7 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
         tall_small(c->GB + (q + m) * ld, ld, Tm_cur, KMAX, Zc + q * ld, ld, n, rn, kp, c->st2);
       }
       if (it + 2 < nb) {  // Ghat_{t+1} is needed only if step t+2 exists
-        epass_on(c, c->E_full, Zc + q * ld, rn, c->GB + (2 * q + m) * ld, ld, 1.0, c->st2, c->gs2);
+        eact_on(c, true, Zc + q * ld, rn, c->GB + (2 * q + m) * ld, ld, c->st2, c->gs2);
         DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_cong, 0));
         GemmNTArgs g;
         g.A = c->GB; g.lda = ld; g.B = c->GB; g.ldb = ld;
@@ -851,7 +902,7 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
         ProfScope ps(c, PROF_APPLY);
         tall_small(Zc, ld, Tm_cur, KMAX, c->Ztmp, ld, n, rn, kp, c->st);
       }
-      epass(c, c->E_full, c->Ztmp, rn, Zc + q * ld, ld, 1.0);
+      eact(c, true, c->Ztmp, rn, Zc + q * ld, ld);
       r_prev = rn;
       SmallArgs an;
       bool fastn = false;
@@ -907,11 +958,13 @@ void matmul_sq(dme_ctx* c, const double* X, const double* Y, double* out) {
   if (sym) mirror_lower(out, c->n, c->ldn, false, c->st);
 }
 
-// L_I(2w) = compress([L_I(w), E_w L_I(w)])  (exact doubling of the composite rule, reading G6)
-void ladder_double(dme_ctx* c, double* LI, int64_t& q, const double* Ew) {
+// L_I(2w) = compress([L_I(w), E_w L_I(w)])  (exact doubling of the composite rule, reading G6);
+// E_w is the dense Ew, or (sparse A) the Chebyshev action with tau = w
+void ladder_double(dme_ctx* c, double* LI, int64_t& q, const double* Ew, double w) {
   if (q == 0) return;
   DME_REQUIRE(2 * q <= KMAX, DME_ERR_DIM, "quadrature factor rank exceeds 112");
-  epass(c, Ew, LI, q, LI + q * c->ldn, c->ldn, 1.0);
+  if (c->sparse) sparse_pass(c, w, LI, q, LI + q * c->ldn, c->ldn, c->st);
+  else epass(c, Ew, LI, q, LI + q * c->ldn, c->ldn, 1.0);
   const int64_t qn = compress(c, LI, 2 * q, c->Ztmp, false, 0.0);
   copy_cols(LI, c->ldn, c->Ztmp, c->ldn, c->n, qn, 1.0, c->st);
   q = qn;
@@ -935,7 +988,14 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   // ---------------------------------------------------------------- upload (H2D boundary)
   // A and S: host memory (pageable or pinned) or, with options.big_inputs_on_device, device memory
   const cudaMemcpyKind kbig = c->opt.big_inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, kbig, st));
+  if (c->sparse) {  // partitioned ELL of A^T (built on the host from the CSR by cheb_prepare)
+    DME_CUDA(cudaMemcpyAsync(c->cop.val, c->chost.val.data(), c->chost.val.size() * 8,
+                             cudaMemcpyHostToDevice, st));
+    DME_CUDA(cudaMemcpyAsync(c->cop.idx, c->chost.idx.data(), c->chost.idx.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+  } else {
+    DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, kbig, st));
+  }
   if (c->has_S)
     DME_CUDA(cudaMemcpy2DAsync(c->S, ld * 8, pr->S, n * 8, n * 8, n, kbig, st));
   // mass matrix (Example 4): A <- A M^-1, C <- C M^-1 by a dense LU of M
@@ -965,7 +1025,8 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   {
     int flags_host[4] = {0, 0, 0, 0};
     DME_CUDA(cudaMemsetAsync(c->r_dev, 0, 4 * sizeof(int), st));
-    check_square(c->Aup, n, ld, c->r_dev, st);           // r_dev[0]: non-finite, r_dev[1]: asymmetric
+    if (!c->sparse)  // (a sparse A was validated on the host by cheb_prepare)
+      check_square(c->Aup, n, ld, c->r_dev, st);         // r_dev[0]: non-finite, r_dev[1]: asymmetric
     if (c->has_S) check_square(c->S, n, ld, c->r_dev + 2, st);
     DME_CUDA(cudaMemcpyAsync(flags_host, c->r_dev, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     sync(c);
@@ -995,10 +1056,14 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     sync(c);
   }
   // ---------------------------------------------------------------- scaling: s from ||(h/2) A^T||_1
-  rowabs_max(c->Aup, n, ld, c->red_scratch, c->norm_dev, st);
   double nrm = 0;
-  DME_CUDA(cudaMemcpyAsync(&nrm, c->norm_dev, 8, cudaMemcpyDeviceToHost, st));
-  sync(c);
+  if (c->sparse) {
+    nrm = c->chost.norm1;
+  } else {
+    rowabs_max(c->Aup, n, ld, c->red_scratch, c->norm_dev, st);
+    DME_CUDA(cudaMemcpyAsync(&nrm, c->norm_dev, 8, cudaMemcpyDeviceToHost, st));
+    sync(c);
+  }
   DME_REQUIRE(std::isfinite(nrm), DME_ERR_NUMERIC, "non-finite norm of A");
   const double tau0 = c->h / 2;
   const double tn = tau0 * nrm;
@@ -1012,7 +1077,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   c->stats.quad_panels = 1 << s_total;
   c->stats.panel_width = delta;
   // X0 = delta * A^T
-  transpose_scale(c->Aup, n, ld, delta, c->X0, ld, st);
+  if (!c->sparse) transpose_scale(c->Aup, n, ld, delta, c->X0, ld, st);
 
   // ---------------------------------------------------------------- first-panel node actions
   // Y_i = exp(c_i delta A^T) L_Q = sum_j c_i^j W_j,  W_j = (delta A^T) W_{j-1} / j   (Taylor)
@@ -1020,7 +1085,10 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   std::vector<double> cn, wn;
   gauss_legendre01(q, cn, wn);
   int64_t qI = 0;
-  if (c->p > 0) {
+  if (c->p > 0 && c->sparse) {  // Y_i = exp(c_i delta A^T) L_Q by the Chebyshev action
+    for (int i = 0; i < q; ++i)
+      sparse_pass(c, cn[i] * delta, c->LQ, c->p, c->Yn + (size_t)i * c->p * ld, ld, st);
+  } else if (c->p > 0) {
     const double nx0 = delta * nrm;  // ||delta A^T||_1 bound for the truncation
     int J = 1;
     double term = 1.0;
@@ -1048,6 +1116,8 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
         axpy_cols(Yi, ld, Wcur, ld, n, c->p, cpow[i], st);  // Y_i += c_i^j W_j
       }
     }
+  }
+  if (c->p > 0) {
     // L_I(delta) = [sqrt(w_i delta) Y_i]  (D_I = blkdiag(w_i D_Q), D_Q = I; square-root form)
     for (int i = 0; i < q; ++i)
       copy_cols(c->Zc12h + (size_t)i * c->p * ld, ld, c->Yn + (size_t)i * c->p * ld, ld, n, c->p,
@@ -1056,6 +1126,16 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     copy_cols(c->Zc12h, ld, c->Ztmp, ld, n, qI, 1.0, st);
   }
 
+  if (c->sparse) {
+    // ---------------------------------------------------------------- ladder by sparse actions
+    int64_t q_cur = qI;
+    for (int j = 0; j < s_total; ++j) ladder_double(c, c->Zc12h, q_cur, nullptr, std::ldexp(delta, j));
+    c->qh = q_cur;
+    copy_cols(c->Zc12f, ld, c->Zc12h, ld, n, c->qh, 1.0, st);
+    int64_t qf = c->qh;
+    ladder_double(c, c->Zc12f, qf, nullptr, tau0);
+    c->qf = qf;
+  } else {
   // ---------------------------------------------------------------- Padé-13 on X0 (Higham 2005)
   const double* b = PADE_B;
   matmul_sq(c, c->X0, c->X0, c->X2);
@@ -1085,7 +1165,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   int si = 0;
   int64_t q_cur = qI;
   for (int j = 0; j < s_total; ++j) {
-    ladder_double(c, c->Zc12h, q_cur, Ecur);  // L_I(2w) from E_w, w = delta 2^j
+    ladder_double(c, c->Zc12h, q_cur, Ecur, 0.0);  // L_I(2w) from E_w, w = delta 2^j
     double* En = spare[si];
     matmul_sq(c, Ecur, Ecur, En);
     spare[si] = (Ecur == c->X6) ? c->V : Ecur;
@@ -1097,7 +1177,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   // L_I(h) = compress([L_I(h/2), E_{h/2} L_I(h/2)]),  E_h = E_{h/2}^2
   copy_cols(c->Zc12f, ld, c->Zc12h, ld, n, c->qh, 1.0, st);
   int64_t qf = c->qh;
-  ladder_double(c, c->Zc12f, qf, c->E_half);
+  ladder_double(c, c->Zc12f, qf, c->E_half, 0.0);
   c->qf = qf;
   matmul_sq(c, c->E_half, c->E_half, c->E_full);
   if (c->oz) {  // digit slices of the local rows of E_{h/2} and E_h (after the last product)
@@ -1105,8 +1185,9 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     oz_slice_rows_tiled(c->E_full + c->row0 * ld, ld, c->rows_loc, n, c->ozEf, c->exEf, c->ozpm, st);
     c->oz_ready = true;
   }
+  }  // dense E
   // look-ahead operand: E_h L_I(h) stays in the leading columns of LA
-  epass(c, c->E_full, c->Zc12f, c->qf, c->LA, ld, 1.0);
+  eact(c, true, c->Zc12f, c->qf, c->LA, ld);
   // fixed columns of the congruence pipeline's GB = [L_I(h) | B | E_h L_I(h) | (E_h Y)]
   if (c->m > 0 && 2 * c->qf + c->m <= KMAX) {
     copy_cols(c->GB, ld, c->Zc12f, ld, n, c->qf, 1.0, st);
@@ -1502,6 +1583,18 @@ dme_status dme_set_profiling(dme_ctx* c, int32_t on) {
   });
 }
 
+dme_status dme_cheb_coeffs(double gamma, double tol, double* out, int64_t cap, int32_t* K) {
+  return guarded(nullptr, [&] {
+    DME_REQUIRE(out && K && std::isfinite(gamma) && gamma >= 0 && tol > 0, DME_ERR_INVALID,
+                "bad Chebyshev coefficient arguments");
+    std::vector<double> chat;
+    const int k = cheb_coeffs(gamma, tol, chat);
+    DME_REQUIRE(k + 1 <= cap, DME_ERR_CAPACITY, "coefficient buffer too small");
+    std::memcpy(out, chat.data(), chat.size() * 8);
+    *K = k;
+  });
+}
+
 dme_status dme_destroy(dme_ctx* c) {
   delete c;  // ~dme_ctx releases streams, events and the NCCL communicator
   return DME_OK;
@@ -1547,6 +1640,7 @@ dme_status dme_debug_set_factor(dme_ctx* c, int64_t r, const double* L) {
 dme_status dme_debug_get_exp(dme_ctx* c, int32_t which, double* E) {
   if (!c || !E) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
   return guarded(c, [&] {
+    DME_REQUIRE(!c->sparse, DME_ERR_CONFIG, "no dense E with a sparse A");
     const double* src = which ? c->E_full : c->E_half;
     DME_CUDA(cudaMemcpy2DAsync(E, c->n * 8, src, c->ldn * 8, c->n * 8, c->n,
                                cudaMemcpyDeviceToHost, c->st));

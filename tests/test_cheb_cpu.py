@@ -1,0 +1,49 @@
+"""Host logic of the sparse-A path (no GPU): the Chebyshev coefficients e^{-gamma} I_k(gamma) of
+e^{gamma (x - 1)} on [-1, 1] that the library computes by Miller's backward recurrence
+(dme_cheb_coeffs, csrc/cheb.cu), pinned against
+  * scipy.special.ive (an independent Bessel implementation),
+  * the closed forms of the expansion at x = 1, 0, -1 (T_k(1) = 1, T_k(0) = cos(k pi / 2),
+    T_k(-1) = (-1)^k): 1, e^{-gamma}, e^{-2 gamma},
+  * the degree rule: the tail beyond K is <= tol and the tail beyond K - 1 is not.
+"""
+import numpy as np
+import pytest
+import scipy.special as sp
+
+import paper_1805_08990_b200 as dme
+
+GAMMAS = [0.0, 1e-8, 0.3, 2.7, 25.0, 204.0, 408.0, 1500.0]
+
+
+@pytest.mark.parametrize("gamma", GAMMAS)
+def test_coeffs_vs_scipy_ive(gamma):
+    c = dme.cheb_coeffs(gamma)
+    ref = sp.ive(np.arange(c.size), gamma)
+    big = ref > 1e-250
+    assert np.all(np.abs(c[big] - ref[big]) <= 1e-12 * ref[big])
+
+
+@pytest.mark.parametrize("gamma", GAMMAS)
+def test_expansion_closed_forms(gamma):
+    c = dme.cheb_coeffs(gamma)
+    k = np.arange(c.size)
+    w = np.where(k == 0, 1.0, 2.0) * c
+    assert abs(w.sum() - 1.0) <= 1e-14                                     # x = 1
+    assert abs((w * np.cos(k * np.pi / 2)).sum() - np.exp(-gamma)) <= 1e-14   # x = 0
+    assert abs((w * (-1.0) ** k).sum() - np.exp(-2 * gamma)) <= 1e-14          # x = -1
+
+
+@pytest.mark.parametrize("gamma", [0.3, 25.0, 204.0])
+@pytest.mark.parametrize("tol", [1e-8, 2.0 ** -56])
+def test_degree_rule(gamma, tol):
+    c = dme.cheb_coeffs(gamma, tol)
+    K = c.size - 1
+    tail = lambda k0: 2 * sp.ive(np.arange(k0 + 1, k0 + 3000), gamma).sum()
+    assert tail(K) <= tol * (1 + 1e-6)
+    assert tail(K - 1) > tol * (1 - 1e-6)
+
+
+def test_degree_growth_is_sublinear():
+    # the reason for a Chebyshev (or Leja) polynomial on the heat spectrum: degree ~ sqrt(gamma)
+    K = [dme.cheb_coeffs(g).size - 1 for g in (100.0, 400.0, 1600.0)]
+    assert K[1] < 2.2 * K[0] and K[2] < 2.2 * K[1]  # (linear growth would be 4x)

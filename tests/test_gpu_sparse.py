@@ -1,0 +1,161 @@
+"""Sparse-A path (include/dme.h A_rowptr): every E_tau L action is a Chebyshev
+expansion of exp on the Gershgorin interval of tau A^T (csrc/cheb.cu), no dense exponential is
+built. The result it approximates has a plain definition, exp(tau A^T) L, so the checks are:
+  * one action against scipy.linalg.expm (small n, ragged column counts, substepped degrees);
+  * whole schemes against the oracle (dense exponential, same quadrature rule) at 1e-10 (P-level)
+    and against the dense GPU path;
+  * invariants: A = 0 (empty CSR) gives exp(0) = I, so Strang F1F2 yields P0 + T Q exactly (P13);
+  * the configuration errors of the boundary (nonsymmetric A, M with a sparse A, bad CSR).
+"""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import scipy.sparse as sps
+
+pytestmark = pytest.mark.gpu
+
+from oracle import lowrank  # noqa: E402
+from oracle.schemes import OracleOptions, OracleSolver  # noqa: E402
+from workloads import make_config  # noqa: E402
+
+TOL_P = 1e-10
+
+
+@pytest.fixture(scope="module")
+def dme():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1805_08990_b200 as m
+    return m
+
+
+def _kw(dme, prob):
+    kw = dme.problem_kwargs(prob)
+    kw["A"] = sps.csr_matrix(prob.A)
+    return kw
+
+
+@pytest.mark.parametrize("cfg,kw,k,which", [(5, dict(nx=20), 37, "half"), (5, dict(nx=20), 64, "full"),
+                                            (2, dict(nx=23), 9, "full"), (1, dict(n=100), 1, "half")])
+def test_action_vs_expm(dme, cfg, kw, k, which):
+    prob = make_config(cfg, **kw)
+    h = 0.005 if cfg != 1 else 1e-3
+    tau = h if which == "full" else h / 2
+    s = dme.Solver(A=sps.csr_matrix(prob.A), h=h)
+    L = np.random.default_rng(k).random((prob.n, k))
+    s.debug_set_factor(L)
+    s.debug_apply("T1", tau)
+    Y, _ = s.get_factor()
+    st = s.stats()
+    s.close()
+    ref = sla.expm(tau * prob.A.T) @ L
+    # absolute error per column relative to the column scale (||exp(tau A^T)||_2 <= 1 here)
+    err = np.abs(Y - ref).max(axis=0) / np.abs(L).max(axis=0)
+    assert err.max() <= 1e-13, err.max()
+    assert st["e_passes"] >= 1
+
+
+def test_action_substepped_degree(dme):
+    """gamma beyond one substep's degree cap (1D heat, tau = 0.25: gamma ~ 5100): the kernel runs
+    several substeps; still FP64-accurate against expm."""
+    prob = make_config(1, n=100)
+    h = 0.5
+    s = dme.Solver(A=sps.csr_matrix(prob.A), h=h)
+    L = np.random.default_rng(3).random((prob.n, 5))
+    s.debug_set_factor(L)
+    s.debug_apply("T1", h)
+    Y, _ = s.get_factor()
+    s.close()
+    ref = sla.expm(h * prob.A.T) @ L
+    assert np.abs(Y - ref).max() <= 1e-13 * np.abs(L).max()
+
+
+SCHEME_CASES = [
+    (1, dict(n=100), "lie", "F1F2", 0.1, 40, {}),
+    (2, dict(nx=20), "strang", "F12", 0.5, 20, dict(quad_nodes=5, quad_subpanels=4)),
+    (2, dict(nx=20), "strang", "F1F2", 0.5, 20, {}),
+    (4, dict(nx=12), "strang", "F12F3F4", 0.5, 20, {}),
+    (4, dict(nx=12, dle=True), "strang", "F1F4F2", 0.5, 20, {}),
+    (5, dict(nx=24), "strang", "F12F3", 0.5, 20, dict(rank_cap=64)),
+    (5, dict(nx=33), "strang", "F1F2F3", 0.5, 20, dict(rank_cap=64)),
+]
+
+
+@pytest.mark.parametrize("cfg,kw,scheme,comp,T,N,opts", SCHEME_CASES)
+def test_scheme_vs_oracle(dme, cfg, kw, scheme, comp, T, N, opts):
+    prob = make_config(cfg, **kw)
+    h = T / N
+    s = dme.Solver(**_kw(dme, prob), h=h, **opts)
+    s.split_step(scheme, comp, N)
+    Lg, Dg = s.get_factor()
+    st = s.stats()
+    s.close()
+    oo = OracleOptions(rank_cap=opts.get("rank_cap"), quad_nodes=opts.get("quad_nodes", 14),
+                       quad_subpanels=opts.get("quad_subpanels", 1))
+    orc = OracleSolver(prob, h, oo)
+    orc.step(scheme, comp, N)
+    Lo, Do = orc.factor()
+    d = lowrank.rel_diff(Lg, Dg, Lo, Do)
+    assert d <= TOL_P, (d, Lg.shape[1], Lo.shape[1])
+    assert st["ozaki_passes"] == 0 and st["cheb_degree"] > 0
+    # same rule as the dense GPU path
+    sd = dme.Solver(**dme.problem_kwargs(prob), h=h, **opts)
+    sd.split_step(scheme, comp, N)
+    Ld, Dd = sd.get_factor()
+    sd.close()
+    assert lowrank.rel_diff(Lg, Dg, Ld, Dd) <= TOL_P
+
+
+def test_zero_A_strang_F1F2_exact(dme):
+    """A = 0 (CSR with no entries): exp(0) = I, so Strang F1F2 gives P0 + T Q (P13)."""
+    prob = make_config(2, nx=7, dle=True)
+    n, T, N = prob.n, 0.5, 10
+    kw = _kw(dme, prob)
+    kw["A"] = sps.csr_matrix((n, n))
+    s = dme.Solver(**kw, h=T / N)
+    s.split_step("strang", "F1F2", N)
+    Lg, Dg = s.get_factor()
+    s.close()
+    P0 = prob.L0 @ prob.L0.T
+    ref = P0 + T * prob.C.T @ prob.C
+    P = Lg @ Dg @ Lg.T
+    assert np.linalg.norm(P - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_sparse_errors(dme):
+    prob = make_config(3, nx=8)  # convection-diffusion: nonsymmetric
+    with pytest.raises(dme.DmeError) as e:
+        dme.Solver(**_kw(dme, prob), h=0.01)
+    assert e.value.code == 3
+    prob = make_config(5, nx=8)
+    A = sps.csr_matrix(prob.A)
+    s = dme.Solver(A=A, h=0.01)
+    with pytest.raises(dme.DmeError) as e:
+        s.debug_get_exp(0)
+    assert e.value.code == 3
+    s.close()
+    with pytest.raises(dme.DmeError) as e:
+        dme.Solver(A=A, M=np.eye(prob.n), h=0.01)
+    assert e.value.code == 3
+    bad = A.copy()
+    bad.indices = bad.indices.copy()
+    bad.indices[3] = prob.n + 5  # column index out of range
+    with pytest.raises(dme.DmeError) as e:
+        dme.Solver(A=bad, h=0.01)
+    assert e.value.code == 1
+
+
+@pytest.mark.slow
+def test_fullsize_sparse_three_steps(dme):
+    """BASELINE config 5 at full size (n = 10^4) through the sparse path: oracle parity (1e-10)."""
+    prob = make_config(5)
+    h = 0.005
+    s = dme.Solver(**_kw(dme, prob), h=h, rank_cap=64)
+    s.split_step("strang", "F12F3", 3)
+    Lg, Dg = s.get_factor()
+    s.close()
+    orc = OracleSolver(prob, h, OracleOptions(rank_cap=64))
+    orc.step("strang", "F12F3", 3)
+    Lo, Do = orc.factor()
+    d = lowrank.rel_diff(Lg, Dg, Lo, Do)
+    assert d <= TOL_P, d
