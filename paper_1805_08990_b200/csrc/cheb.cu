@@ -15,10 +15,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 
 #include "cheb.h"
 #include "common.cuh"
 #include "dme.h"
+#include "small.h"
 
 namespace dme {
 
@@ -27,10 +29,11 @@ namespace {
 struct ChebParams {
   const double* val;
   const uint32_t* idx;
+  const uint32_t* push;
   const double* X;
   double* out;
   int64_t ldx, ldo, n;
-  int R, w, k, K, substeps;
+  int R, w, H, P, k, K, substeps;
   double alpha, beta, out_scale;
   double coef[CHEB_KMAX + 1];  // coef_k = e^{c + gamma} chat_k (k ? 2 : 1), one substep
 };
@@ -40,10 +43,8 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ double ld_dsmem_f64(uint32_t addr) {
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-  return v;
+__device__ __forceinline__ void st_dsmem_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
@@ -55,21 +56,25 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
-template <int C>
+// Shared memory of CTA r: val [w][R], buf0 / buf1 [C][R + H] (own rows, then halo slots),
+// y [C][R], idx [w][R] (local indices), push [P][2].
+// C columns per cluster; W: ELL entries gathered per batch (all loads of a batch are issued before
+// the first FMA: the row's matrix entries, then its W x C neighbour values)
+template <int C, int W>
 __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_THREADS, 1)
     cheb_kernel(const __grid_constant__ ChebParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int R = p.R, w = p.w;
-  double* val_s = reinterpret_cast<double*>(smem);                      // [w][R]
-  double* buf0 = val_s + (size_t)w * R;                                 // [C][R]
-  double* buf1 = buf0 + (size_t)C * R;                                  // [C][R]
-  double* y_s = buf1 + (size_t)C * R;                                   // [C][R]
-  uint32_t* idx_s = reinterpret_cast<uint32_t*>(y_s + (size_t)C * R);   // [w][R]
-  __shared__ uint32_t rbase[2][CHEB_CLUSTER];                           // DSMEM bases of buf0/buf1
+  const int R = p.R, w = p.w, LD = p.R + p.H, P = p.P;
+  double* val_s = reinterpret_cast<double*>(smem);
+  double* buf0 = val_s + (size_t)w * R;
+  double* buf1 = buf0 + (size_t)C * LD;
+  double* y_s = buf1 + (size_t)C * LD;
+  uint32_t* idx_s = reinterpret_cast<uint32_t*>(y_s + (size_t)C * R);
+  uint32_t* push_s = idx_s + (size_t)w * R;
+  __shared__ uint32_t rbase[2][CHEB_CLUSTER];  // DSMEM addresses of buf0 / buf1 in every CTA
 
   const uint32_t me = cluster_rank();
-  const int group = blockIdx.x / CHEB_CLUSTER;
-  const int col0 = group * C;
+  const int col0 = (blockIdx.x / CHEB_CLUSTER) * C;
   const int ncol = min(C, p.k - col0);
   const int64_t row0 = (int64_t)me * R;
   const int tid = threadIdx.x;
@@ -77,54 +82,82 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_THRE
     rbase[0][tid] = mapa_u32(smem_u32(buf0), tid);
     rbase[1][tid] = mapa_u32(smem_u32(buf1), tid);
   }
-  // matrix slice and v_0 (zero rows beyond n, zero columns beyond k)
   const int64_t ldm = (int64_t)CHEB_CLUSTER * R;
   for (int e = tid; e < w * R; e += CHEB_THREADS) {
     const int q = e / R, i = e - q * R;
     val_s[e] = p.val[q * ldm + row0 + i];
     idx_s[e] = p.idx[q * ldm + row0 + i];
   }
+  for (int e = tid; e < 2 * P; e += CHEB_THREADS) push_s[e] = p.push[(int64_t)me * 2 * P + e];
   for (int e = tid; e < C * R; e += CHEB_THREADS) {
     const int j = e / R, i = e - j * R;
     const int64_t gi = row0 + i;
-    buf0[e] = (j < ncol && gi < p.n) ? p.X[(col0 + j) * p.ldx + gi] : 0.0;
+    buf0[j * LD + i] = (j < ncol && gi < p.n) ? p.X[(col0 + j) * p.ldx + gi] : 0.0;
   }
+  __syncthreads();
+  // owners store the rows other CTAs read into those CTAs' halo slots of buffer b
+  auto push_rows = [&](const double* b, int bi) {
+    for (int e = tid; e < P; e += CHEB_THREADS) {
+      const uint32_t src = push_s[2 * e], d = push_s[2 * e + 1];
+      if (src == 0xFFFFFFFFu) continue;
+      const uint32_t base = rbase[bi][d >> 24] + (d & 0xFFFFFFu) * 8u;
+#pragma unroll
+      for (int j = 0; j < C; ++j) st_dsmem_f64(base + (uint32_t)(j * LD) * 8u, b[j * LD + src]);
+    }
+  };
   const double alpha = p.alpha, beta = p.beta;
   for (int sub = 0; sub < p.substeps; ++sub) {
-    if (sub > 0)  // v_0 of the next substep = y (own rows); the last degree's barrier freed buf0
-      for (int e = tid; e < C * R; e += CHEB_THREADS) buf0[e] = y_s[e];
-    for (int e = tid; e < C * R; e += CHEB_THREADS) y_s[e] = p.coef[0] * buf0[e];
+    if (sub > 0) {  // v_0 of the next substep = y (own rows)
+      for (int e = tid; e < C * R; e += CHEB_THREADS) {
+        const int j = e / R, i = e - j * R;
+        buf0[j * LD + i] = y_s[e];
+      }
+      __syncthreads();
+    }
+    push_rows(buf0, 0);
+    for (int e = tid; e < C * R; e += CHEB_THREADS) {
+      const int j = e / R, i = e - j * R;
+      y_s[e] = p.coef[0] * buf0[j * LD + i];
+    }
     cluster_sync_all();
     for (int kd = 1; kd <= p.K; ++kd) {
       const int cur = (kd - 1) & 1;
-      double* bc = cur ? buf1 : buf0;  // v_{k-1}
-      double* bp = cur ? buf0 : buf1;  // v_{k-2}, overwritten by v_k
+      const double* bc = cur ? buf1 : buf0;  // v_{k-1} (own rows + halo)
+      double* bp = cur ? buf0 : buf1;        // v_{k-2}, overwritten by v_k
       const double ck = p.coef[kd];
       for (int i = tid; i < R; i += CHEB_THREADS) {
         double acc[C];
 #pragma unroll
         for (int j = 0; j < C; ++j) acc[j] = 0.0;
-        for (int q = 0; q < w; ++q) {
-          const double a = val_s[q * R + i];
-          const uint32_t e = idx_s[q * R + i];
-          const uint32_t own = e >> 24, off = e & 0xFFFFFFu;
-          if (own == me) {
+        for (int q0 = 0; q0 < w; q0 += W) {
+          double a[W];
+          uint32_t e[W];
 #pragma unroll
-            for (int j = 0; j < C; ++j) acc[j] = fma(a, bc[j * R + off], acc[j]);
-          } else {
-            const uint32_t base = rbase[cur][own] + off * 8u;
-#pragma unroll
-            for (int j = 0; j < C; ++j) acc[j] = fma(a, ld_dsmem_f64(base + (uint32_t)(j * R) * 8u), acc[j]);
+          for (int u = 0; u < W; ++u) {
+            const bool in = (W == 1) || q0 + u < w;  // (w is a multiple of W unless W > w)
+            a[u] = in ? val_s[(q0 + u) * R + i] : 0.0;
+            e[u] = in ? idx_s[(q0 + u) * R + i] : (uint32_t)i;
           }
+          double g[W][C];
+#pragma unroll
+          for (int u = 0; u < W; ++u)
+#pragma unroll
+            for (int j = 0; j < C; ++j) g[u][j] = bc[j * LD + e[u]];
+#pragma unroll
+          for (int u = 0; u < W; ++u)
+#pragma unroll
+            for (int j = 0; j < C; ++j) acc[j] = fma(a[u], g[u][j], acc[j]);
         }
 #pragma unroll
         for (int j = 0; j < C; ++j) {
-          const double t = alpha * acc[j] - beta * bc[j * R + i];
-          const double vn = kd == 1 ? t : 2.0 * t - bp[j * R + i];
-          bp[j * R + i] = vn;
+          const double t = alpha * acc[j] - beta * bc[j * LD + i];
+          const double vn = kd == 1 ? t : 2.0 * t - bp[j * LD + i];
+          bp[j * LD + i] = vn;
           y_s[j * R + i] = fma(ck, vn, y_s[j * R + i]);
         }
       }
+      __syncthreads();
+      push_rows(bp, cur ^ 1);
       cluster_sync_all();
     }
   }
@@ -135,9 +168,159 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_THRE
   }
 }
 
-template <int C>
-void launch_c(const ChebParams& prm, int groups, size_t smem, cudaStream_t st) {
-  auto kern = cheb_kernel<C>;
+// Register-resident variant (R <= 2 * CHEB_REG_THREADS, w <= W): every thread owns the rows
+// tid and tid + blockDim.x; their v_{k-1}, v_{k-2} and y stay in registers, so per degree and
+// column the shared-memory traffic is the w gathers plus one store of v_k (the halo copy of the
+// other CTAs and the gathers need it there).
+constexpr int CHEB_REG_THREADS = 640;
+template <int C, int W>
+__global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_THREADS, 1)
+    cheb_reg_kernel(const __grid_constant__ ChebParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = p.R, w = p.w, LD = p.R + p.H, P = p.P;
+  double* val_s = reinterpret_cast<double*>(smem);
+  double* buf0 = val_s + (size_t)w * R;
+  double* buf1 = buf0 + (size_t)C * LD;
+  uint32_t* idx_s = reinterpret_cast<uint32_t*>(buf1 + (size_t)C * LD);
+  uint32_t* push_s = idx_s + (size_t)w * R;
+  __shared__ uint32_t rbase[2][CHEB_CLUSTER];
+
+  const uint32_t me = cluster_rank();
+  const int col0 = (blockIdx.x / CHEB_CLUSTER) * C;
+  const int ncol = min(C, p.k - col0);
+  const int64_t row0 = (int64_t)me * R;
+  const int tid = threadIdx.x, T = blockDim.x;
+  if (tid < CHEB_CLUSTER) {
+    rbase[0][tid] = mapa_u32(smem_u32(buf0), tid);
+    rbase[1][tid] = mapa_u32(smem_u32(buf1), tid);
+  }
+  const int64_t ldm = (int64_t)CHEB_CLUSTER * R;
+  for (int e = tid; e < w * R; e += T) {
+    const int q = e / R, i = e - q * R;
+    val_s[e] = p.val[q * ldm + row0 + i];
+    idx_s[e] = p.idx[q * ldm + row0 + i];
+  }
+  for (int e = tid; e < 2 * P; e += T) push_s[e] = p.push[(int64_t)me * 2 * P + e];
+  const int i0 = tid, i1 = tid + T;
+  const bool h0 = i0 < R, h1 = i1 < R;
+  double vc[2][C], vp[2][C], y[2][C];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = u ? i1 : i0;
+    const bool has = u ? h1 : h0;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int64_t gi = row0 + i;
+      const double x = (has && j < ncol && gi < p.n) ? p.X[(col0 + j) * p.ldx + gi] : 0.0;
+      vc[u][j] = x;
+      vp[u][j] = 0.0;
+      y[u][j] = 0.0;
+      if (has) buf0[j * LD + i] = x;
+    }
+  }
+  __syncthreads();
+  auto push_rows = [&](const double* b, int bi) {
+    for (int e = tid; e < P; e += T) {
+      const uint32_t src = push_s[2 * e], d = push_s[2 * e + 1];
+      if (src == 0xFFFFFFFFu) continue;
+      const uint32_t base = rbase[bi][d >> 24] + (d & 0xFFFFFFu) * 8u;
+#pragma unroll
+      for (int j = 0; j < C; ++j) st_dsmem_f64(base + (uint32_t)(j * LD) * 8u, b[j * LD + src]);
+    }
+  };
+  const double alpha = p.alpha, beta = p.beta;
+  for (int sub = 0; sub < p.substeps; ++sub) {
+    if (sub > 0) {  // v_0 of the next substep = y
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = u ? i1 : i0;
+        const bool has = u ? h1 : h0;
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          vc[u][j] = y[u][j];
+          if (has) buf0[j * LD + i] = y[u][j];
+        }
+      }
+      __syncthreads();
+    }
+    push_rows(buf0, 0);
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int j = 0; j < C; ++j) y[u][j] = p.coef[0] * vc[u][j];
+    cluster_sync_all();
+    for (int kd = 1; kd <= p.K; ++kd) {
+      const int cur = (kd - 1) & 1;
+      const double* bc = cur ? buf1 : buf0;  // v_{k-1} with halo
+      double* bn = cur ? buf0 : buf1;        // receives v_k
+      const double ck = p.coef[kd];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = u ? i1 : i0;
+        if (!(u ? h1 : h0)) continue;
+        double a[W];
+        uint32_t e[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          const bool in = q < w;
+          a[q] = in ? val_s[q * R + i] : 0.0;
+          e[q] = in ? idx_s[q * R + i] : (uint32_t)i;
+        }
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < W; ++q) acc = fma(a[q], bc[j * LD + e[q]], acc);
+          const double t = alpha * acc - beta * vc[u][j];
+          const double vn = kd == 1 ? t : 2.0 * t - vp[u][j];
+          vp[u][j] = vc[u][j];
+          vc[u][j] = vn;
+          y[u][j] = fma(ck, vn, y[u][j]);
+          bn[j * LD + i] = vn;
+        }
+      }
+      __syncthreads();
+      push_rows(bn, cur ^ 1);
+      cluster_sync_all();
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = u ? i1 : i0;
+    const int64_t gi = row0 + i;
+    if (!(u ? h1 : h0) || gi >= p.n) continue;
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (j < ncol) p.out[(col0 + j) * p.ldo + gi] = p.out_scale * y[u][j];
+  }
+}
+
+template <int C, int W>
+void launch_reg(const ChebParams& prm, int groups, size_t smem, int threads, cudaStream_t st) {
+  auto kern = cheb_reg_kernel<C, W>;
+  static bool attr = false;
+  if (!attr) {
+    DME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+    attr = true;
+  }
+  kern<<<groups * CHEB_CLUSTER, threads, smem, st>>>(prm);
+  DME_KCHECK();
+}
+template <int W>
+void launch_reg_w(const ChebParams& prm, int C, int groups, size_t smem, int threads, cudaStream_t st) {
+  switch (C) {
+    case 1: launch_reg<1, W>(prm, groups, smem, threads, st); break;
+    case 2: launch_reg<2, W>(prm, groups, smem, threads, st); break;
+    case 3: launch_reg<3, W>(prm, groups, smem, threads, st); break;
+    case 4: launch_reg<4, W>(prm, groups, smem, threads, st); break;
+    default: launch_reg<5, W>(prm, groups, smem, threads, st); break;
+  }
+}
+constexpr int CHEB_REG_CMAX = 5;
+
+template <int C, int W>
+void launch_cw(const ChebParams& prm, int groups, size_t smem, cudaStream_t st) {
+  auto kern = cheb_kernel<C, W>;
   static bool attr = false;
   if (!attr) {
     DME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
@@ -146,11 +329,45 @@ void launch_c(const ChebParams& prm, int groups, size_t smem, cudaStream_t st) {
   kern<<<groups * CHEB_CLUSTER, CHEB_THREADS, smem, st>>>(prm);
   DME_KCHECK();
 }
+template <int C>
+void launch_c(const ChebParams& prm, int groups, size_t smem, cudaStream_t st) {
+  if (prm.w <= 3) launch_cw<C, 3>(prm, groups, smem, st);
+  else if (prm.w <= 5) launch_cw<C, 5>(prm, groups, smem, st);
+  else if (prm.w <= 8) launch_cw<C, 8>(prm, groups, smem, st);
+  else launch_cw<C, 4>(prm, groups, smem, st);  // wide rows: batches of 4
+}
+
+// co-resident 8-CTA clusters of cheb_kernel<C, .> at this shared-memory size (cached per C)
+int max_active_clusters(int C, size_t smem) {
+  static int cache[CHEB_CMAX + 1][2] = {};
+  if (cache[C][0] > 0 && cache[C][1] == (int)smem) return cache[C][0];
+  auto kern = cheb_kernel<1, 5>;  // same launch shape for every instance (1 CTA per SM, 512 threads)
+  DME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CHEB_CLUSTER * 64);
+  cfg.blockDim = dim3(CHEB_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CHEB_CLUSTER;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  DME_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+  cache[C][0] = std::max(1, n);
+  cache[C][1] = (int)smem;
+  return cache[C][0];
+}
 
 }  // namespace
 
-size_t cheb_smem_bytes(int64_t R, int w, int C) {
-  return (size_t)R * (size_t)w * 12 + (size_t)R * C * 24 + 64;
+size_t cheb_smem_bytes_reg(int64_t R, int w, int H, int P, int C) {
+  return (size_t)R * w * 12 + (size_t)(R + H) * C * 16 + (size_t)P * 8 + 64;
+}
+size_t cheb_smem_bytes(int64_t R, int w, int H, int P, int C) {
+  return (size_t)R * w * 12 + (size_t)(R + H) * C * 16 + (size_t)R * C * 8 + (size_t)P * 8 + 64;
 }
 
 int cheb_coeffs(double gamma, double tol, std::vector<double>& chat) {
@@ -250,28 +467,60 @@ int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* c
     w = std::max<int>(w, (int)rowsT[i].size());
   }
   const int64_t R = ceil_div(n, CHEB_CLUSTER);
-  if (R >= (1 << 24)) return fail(DME_ERR_DIM, "sparse A: too many rows per CTA");
+  if (R + (int64_t)n >= (1 << 24)) return fail(DME_ERR_DIM, "sparse A: too many rows per CTA");
+  // halo of CTA r: the rows of other CTAs its rows read (sorted), slot s at local index R + s;
+  // push list of CTA o: (own row, (reader << 24) | reader's local index) for every such row
+  std::vector<std::vector<std::pair<uint32_t, uint32_t>>> pushes(CHEB_CLUSTER);
+  std::vector<std::vector<int32_t>> halo(CHEB_CLUSTER);
+  int H = 0;
+  for (int r = 0; r < CHEB_CLUSTER; ++r) {
+    std::vector<int32_t>& hl = halo[r];
+    for (int64_t i = r * R; i < std::min<int64_t>(n, (r + 1) * R); ++i)
+      for (auto& x : rowsT[i])
+        if (x.first / R != r) hl.push_back(x.first);
+    std::sort(hl.begin(), hl.end());
+    hl.erase(std::unique(hl.begin(), hl.end()), hl.end());
+    H = std::max<int>(H, (int)hl.size());
+    for (size_t s = 0; s < hl.size(); ++s)
+      pushes[hl[s] / R].push_back({(uint32_t)(hl[s] % R), (uint32_t)(r << 24) | (uint32_t)(R + s)});
+  }
+  int P = 0;
+  for (auto& pl : pushes) P = std::max<int>(P, (int)pl.size());
   int C = 0;
   for (int c = CHEB_CMAX; c >= 1; --c)
-    if (cheb_smem_bytes(R, w, c) <= 225 * 1024) { C = c; break; }
-  if (C == 0) return fail(DME_ERR_DIM, "sparse A: n x (ELL width) too large for one cluster's shared memory");
+    if (cheb_smem_bytes(R, w, H, P, c) <= 225 * 1024) { C = c; break; }
+  if (C == 0) return fail(DME_ERR_DIM, "sparse A: rows x (ELL width + halo) too large for one cluster's shared memory");
   out.nnz = 0;
   for (auto& r : rowsT) out.nnz += (int64_t)r.size();
-  out.n = n; out.R = R; out.w = w; out.C = C; out.a = a; out.b = b; out.norm1 = norm1;
+  out.n = n; out.R = R; out.w = w; out.H = H; out.P = P; out.C = C;
+  out.a = a; out.b = b; out.norm1 = norm1;
   const int64_t ldm = (int64_t)CHEB_CLUSTER * R;
   out.val.assign((size_t)w * ldm, 0.0);
   out.idx.assign((size_t)w * ldm, 0u);
   for (int64_t i = 0; i < ldm; ++i) {
-    const uint32_t self = (uint32_t)((i / R) << 24) | (uint32_t)(i % R);
-    for (int q = 0; q < w; ++q) out.idx[q * ldm + i] = self;  // padding: zero times own row
+    const int r = (int)(i / R);
+    for (int q = 0; q < w; ++q) out.idx[q * ldm + i] = (uint32_t)(i % R);  // padding: 0 x own row
     if (i >= n) continue;
     int q = 0;
     for (auto& x : rowsT[i]) {
+      uint32_t li;
+      if (x.first / R == r) {
+        li = (uint32_t)(x.first % R);
+      } else {
+        const auto& hl = halo[r];
+        li = (uint32_t)(R + (std::lower_bound(hl.begin(), hl.end(), x.first) - hl.begin()));
+      }
       out.val[q * ldm + i] = x.second;
-      out.idx[q * ldm + i] = (uint32_t)((x.first / R) << 24) | (uint32_t)(x.first % R);
+      out.idx[q * ldm + i] = li;
       ++q;
     }
   }
+  out.push.assign((size_t)CHEB_CLUSTER * P * 2, 0xFFFFFFFFu);
+  for (int o = 0; o < CHEB_CLUSTER; ++o)
+    for (size_t e = 0; e < pushes[o].size(); ++e) {
+      out.push[((size_t)o * P + e) * 2] = pushes[o][e].first;
+      out.push[((size_t)o * P + e) * 2 + 1] = pushes[o][e].second;
+    }
   return 0;
 }
 
@@ -294,15 +543,34 @@ int cheb_action(const ChebOp& op, double tau, const double* X, int64_t ldx, int6
   }
   const double scale = std::exp(c + gamma);
   for (int j = 0; j <= K; ++j) prm.coef[j] = scale * chat[j] * (j ? 2.0 : 1.0);
-  prm.val = op.val; prm.idx = op.idx; prm.X = X; prm.out = out;
+  prm.val = op.val; prm.idx = op.idx; prm.push = op.push; prm.X = X; prm.out = out;
   prm.ldx = ldx; prm.ldo = ldo; prm.n = op.n;
-  prm.R = (int)op.R; prm.w = op.w; prm.k = (int)k; prm.K = K; prm.substeps = substeps;
+  prm.R = (int)op.R; prm.w = op.w; prm.H = op.H; prm.P = op.P;
+  prm.k = (int)k; prm.K = K; prm.substeps = substeps;
   prm.alpha = gamma > 0 ? (tau / substeps) / gamma : 0.0;
   prm.beta = gamma > 0 ? c / gamma : 0.0;
   prm.out_scale = alpha;
-  const int C = op.C;
+  // columns per cluster: the smallest C whose ceil(k / C) clusters are co-resident in one wave
+  // (cudaOccupancyMaxActiveClusters: clusters are placed within a GPC, 15 x 8 CTAs on a B200 at
+  // this shared-memory size), less one cluster's SMs for the eigen kernels that run concurrently
+  // on the critical stream (a second wave doubles the time per degree)
+  int C = op.C;
+  for (int c = 1; c <= op.C; ++c)
+    if (ceil_div(k, c) <= std::max(1, max_active_clusters(c, cheb_smem_bytes(op.R, op.w, op.H, op.P, c)) - 1)) {
+      C = c;
+      break;
+    }
   const int groups = (int)ceil_div(k, C);
-  const size_t smem = cheb_smem_bytes(op.R, op.w, C);
+  const bool reg = op.R <= 2 * CHEB_REG_THREADS && op.w <= 5 && C <= CHEB_REG_CMAX &&
+                   !getenv("DME_CHEB_NOREG");
+  if (reg) {
+    const size_t sm = cheb_smem_bytes_reg(op.R, op.w, op.H, op.P, C);
+    const int threads = (int)std::min<int64_t>(CHEB_REG_THREADS, ceil_div(ceil_div(op.R, 2), 32) * 32);
+    if (op.w <= 3) launch_reg_w<3>(prm, C, groups, sm, threads, st);
+    else launch_reg_w<5>(prm, C, groups, sm, threads, st);
+    return K * substeps;
+  }
+  const size_t smem = cheb_smem_bytes(op.R, op.w, op.H, op.P, C);
   switch (C) {
     case 1: launch_c<1>(prm, groups, smem, st); break;
     case 2: launch_c<2>(prm, groups, smem, st); break;

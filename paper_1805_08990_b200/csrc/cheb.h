@@ -9,9 +9,11 @@
 // For a symmetric A the truncation error is <= tail * ||X|| (spectrum inside [a, b]).
 //
 // Device layout (cheb.cu): A^T in ELL form, partitioned over the CHEB_CLUSTER CTAs of a thread-block
-// cluster (rows [r R, (r + 1) R) on CTA r); one cluster per group of C columns of X. The three
-// Chebyshev vectors live in the cluster's distributed shared memory; neighbours' rows are gathered
-// with ld.shared::cluster, one cluster barrier per polynomial degree.
+// cluster (rows [r R, (r + 1) R) on CTA r); one cluster per group of C columns of X. Each CTA keeps
+// its rows of the two Chebyshev vectors plus a halo (the other CTAs' rows its matrix rows read) in
+// shared memory; after every degree the owners push the halo rows into the readers' shared memory
+// (st.shared::cluster), so the gathers of the next degree are all local. One cluster barrier per
+// polynomial degree.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -28,11 +30,14 @@ constexpr int CHEB_CMAX = 8;       // columns per cluster
 struct ChebOp {
   int64_t n = 0, R = 0;   // rows, rows per CTA (n <= CHEB_CLUSTER * R)
   int w = 0;              // ELL width (max nonzeros per row of A^T)
-  int C = 0;              // columns per cluster (shared-memory budget)
+  int H = 0;              // halo slots per CTA (max over the CTAs)
+  int P = 0;              // halo pushes per CTA (max over the CTAs)
+  int C = 0;              // max columns per cluster (shared-memory budget)
   double a = 0, b = 0;    // Gershgorin interval of A^T
   double norm1 = 0;       // ||A^T||_1
-  double* val = nullptr;  // [w][CHEB_CLUSTER * R] (device)
-  uint32_t* idx = nullptr;  // [w][CHEB_CLUSTER * R]: (owner CTA << 24) | row within the owner
+  double* val = nullptr;    // [w][CHEB_CLUSTER * R] (device)
+  uint32_t* idx = nullptr;  // [w][CHEB_CLUSTER * R]: local index into [0, R + H) (own row or halo slot)
+  uint32_t* push = nullptr; // [CHEB_CLUSTER][P][2]: (own row, (dest CTA << 24) | dest slot), ~0 = none
 };
 
 // Host: from the CSR of A (0-based, n x n) build the partitioned ELL of A^T and the Gershgorin data.
@@ -40,14 +45,14 @@ struct ChebOp {
 // DME_ERR_CONFIG (A not exactly symmetric), DME_ERR_DIM (the layout does not fit a cluster).
 struct ChebHost {
   int64_t n = 0, R = 0, nnz = 0;  // nnz: stored entries of A^T (duplicates merged)
-  int w = 0, C = 0;
+  int w = 0, H = 0, P = 0, C = 0;
   double a = 0, b = 0, norm1 = 0;
   std::vector<double> val;
-  std::vector<uint32_t> idx;
+  std::vector<uint32_t> idx, push;
 };
 int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* colind,
                  const double* values, ChebHost& out, std::string* err);
-size_t cheb_smem_bytes(int64_t R, int w, int C);
+size_t cheb_smem_bytes(int64_t R, int w, int H, int P, int C);
 
 // chat[k] = e^{-gamma} I_k(gamma), k = 0..K, with K the smallest degree whose tail
 // 2 sum_{j > K} chat[j] <= tol. Returns K (chat resized to K + 1). Miller's backward recurrence,

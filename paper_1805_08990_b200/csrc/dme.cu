@@ -188,9 +188,11 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   } else {  // partitioned ELL of A^T (cheb.h); no n x n matrix in sparse mode
     const size_t ell = (size_t)c->chost.w * CHEB_CLUSTER * c->chost.R;
     c->cop.n = c->chost.n; c->cop.R = c->chost.R; c->cop.w = c->chost.w; c->cop.C = c->chost.C;
+    c->cop.H = c->chost.H; c->cop.P = c->chost.P;
     c->cop.a = c->chost.a; c->cop.b = c->chost.b; c->cop.norm1 = c->chost.norm1;
     c->cop.val = P.take<double>(ell);
     c->cop.idx = P.take<uint32_t>(ell);
+    c->cop.push = P.take<uint32_t>(std::max<size_t>(c->chost.push.size(), 1));
   }
   if (c->has_S) c->S = P.take<double>(nn);
   c->Bcol = P.take<double>((size_t)ld * std::max<int64_t>(c->m, 1));
@@ -993,6 +995,9 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
                              cudaMemcpyHostToDevice, st));
     DME_CUDA(cudaMemcpyAsync(c->cop.idx, c->chost.idx.data(), c->chost.idx.size() * 4,
                              cudaMemcpyHostToDevice, st));
+    if (!c->chost.push.empty())
+      DME_CUDA(cudaMemcpyAsync(c->cop.push, c->chost.push.data(), c->chost.push.size() * 4,
+                               cudaMemcpyHostToDevice, st));
   } else {
     DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, kbig, st));
   }

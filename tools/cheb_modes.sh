@@ -1,0 +1,4 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+
+
+python tools/cheb_probe.py | head -6
