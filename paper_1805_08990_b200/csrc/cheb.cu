@@ -30,6 +30,8 @@ struct ChebParams {
   const double* val;
   const uint32_t* idx;
   const uint32_t* push;
+  const uint32_t* rptr;
+  const uint32_t* rent;
   const double* X;
   double* out;
   int64_t ldx, ldo, n;
@@ -182,7 +184,8 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
   double* buf0 = val_s + (size_t)w * R;
   double* buf1 = buf0 + (size_t)C * LD;
   uint32_t* idx_s = reinterpret_cast<uint32_t*>(buf1 + (size_t)C * LD);
-  uint32_t* push_s = idx_s + (size_t)w * R;
+  uint32_t* rptr_s = idx_s + (size_t)w * R;   // [R + 1]
+  uint32_t* rent_s = rptr_s + (R + 1);        // [P]
   __shared__ uint32_t rbase[2][CHEB_CLUSTER];
 
   const uint32_t me = cluster_rank();
@@ -190,6 +193,7 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
   const int ncol = min(C, p.k - col0);
   const int64_t row0 = (int64_t)me * R;
   const int tid = threadIdx.x, T = blockDim.x;
+  const int Pm = max(P, 1);
   if (tid < CHEB_CLUSTER) {
     rbase[0][tid] = mapa_u32(smem_u32(buf0), tid);
     rbase[1][tid] = mapa_u32(smem_u32(buf1), tid);
@@ -200,7 +204,8 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
     val_s[e] = p.val[q * ldm + row0 + i];
     idx_s[e] = p.idx[q * ldm + row0 + i];
   }
-  for (int e = tid; e < 2 * P; e += T) push_s[e] = p.push[(int64_t)me * 2 * P + e];
+  for (int e = tid; e <= R; e += T) rptr_s[e] = p.rptr[(int64_t)me * (R + 1) + e];
+  for (int e = tid; e < P; e += T) rent_s[e] = p.rent[(int64_t)me * Pm + e];
   const int i0 = tid, i1 = tid + T;
   const bool h0 = i0 < R, h1 = i1 < R;
   double vc[2][C], vp[2][C], y[2][C];
@@ -218,32 +223,32 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
       if (has) buf0[j * LD + i] = x;
     }
   }
-  __syncthreads();
-  auto push_rows = [&](const double* b, int bi) {
-    for (int e = tid; e < P; e += T) {
-      const uint32_t src = push_s[2 * e], d = push_s[2 * e + 1];
-      if (src == 0xFFFFFFFFu) continue;
+  __syncthreads();  // rptr / rent / rbase
+  // the owner of row i stores its new values straight into the halo slots of the CTAs that read
+  // it (fire-and-forget DSMEM stores, ordered by the cluster barrier's release)
+  auto push_row = [&](int i, const double (&v)[C], int bi) {
+    for (uint32_t e = rptr_s[i]; e < rptr_s[i + 1]; ++e) {
+      const uint32_t d = rent_s[e];
       const uint32_t base = rbase[bi][d >> 24] + (d & 0xFFFFFFu) * 8u;
 #pragma unroll
-      for (int j = 0; j < C; ++j) st_dsmem_f64(base + (uint32_t)(j * LD) * 8u, b[j * LD + src]);
+      for (int j = 0; j < C; ++j) st_dsmem_f64(base + (uint32_t)(j * LD) * 8u, v[j]);
     }
   };
   const double alpha = p.alpha, beta = p.beta;
   for (int sub = 0; sub < p.substeps; ++sub) {
-    if (sub > 0) {  // v_0 of the next substep = y
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int i = u ? i1 : i0;
-        const bool has = u ? h1 : h0;
+    for (int u = 0; u < 2; ++u) {
+      const int i = u ? i1 : i0;
+      if (!(u ? h1 : h0)) continue;
+      if (sub > 0) {  // v_0 of the next substep = y
 #pragma unroll
         for (int j = 0; j < C; ++j) {
           vc[u][j] = y[u][j];
-          if (has) buf0[j * LD + i] = y[u][j];
+          buf0[j * LD + i] = y[u][j];
         }
       }
-      __syncthreads();
+      push_row(i, vc[u], 0);
     }
-    push_rows(buf0, 0);
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -278,9 +283,8 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
           y[u][j] = fma(ck, vn, y[u][j]);
           bn[j * LD + i] = vn;
         }
+        push_row(i, vc[u], cur ^ 1);
       }
-      __syncthreads();
-      push_rows(bn, cur ^ 1);
       cluster_sync_all();
     }
   }
@@ -364,7 +368,7 @@ int max_active_clusters(int C, size_t smem) {
 }  // namespace
 
 size_t cheb_smem_bytes_reg(int64_t R, int w, int H, int P, int C) {
-  return (size_t)R * w * 12 + (size_t)(R + H) * C * 16 + (size_t)P * 8 + 64;
+  return (size_t)R * w * 12 + (size_t)(R + H) * C * 16 + (size_t)(R + 1 + P) * 4 + 64;
 }
 size_t cheb_smem_bytes(int64_t R, int w, int H, int P, int C) {
   return (size_t)R * w * 12 + (size_t)(R + H) * C * 16 + (size_t)R * C * 8 + (size_t)P * 8 + 64;
@@ -515,6 +519,16 @@ int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* c
       ++q;
     }
   }
+  out.rptr.assign((size_t)CHEB_CLUSTER * (R + 1), 0u);
+  out.rent.assign((size_t)CHEB_CLUSTER * std::max(P, 1), 0u);
+  for (int o = 0; o < CHEB_CLUSTER; ++o) {
+    std::vector<std::pair<uint32_t, uint32_t>> pl = pushes[o];
+    std::stable_sort(pl.begin(), pl.end(), [](auto& x, auto& y) { return x.first < y.first; });
+    uint32_t* rp = out.rptr.data() + (size_t)o * (R + 1);
+    for (auto& x : pl) rp[x.first + 1]++;
+    for (int64_t i = 0; i < R; ++i) rp[i + 1] += rp[i];
+    for (size_t e = 0; e < pl.size(); ++e) out.rent[(size_t)o * std::max(P, 1) + e] = pl[e].second;
+  }
   out.push.assign((size_t)CHEB_CLUSTER * P * 2, 0xFFFFFFFFu);
   for (int o = 0; o < CHEB_CLUSTER; ++o)
     for (size_t e = 0; e < pushes[o].size(); ++e) {
@@ -543,7 +557,8 @@ int cheb_action(const ChebOp& op, double tau, const double* X, int64_t ldx, int6
   }
   const double scale = std::exp(c + gamma);
   for (int j = 0; j <= K; ++j) prm.coef[j] = scale * chat[j] * (j ? 2.0 : 1.0);
-  prm.val = op.val; prm.idx = op.idx; prm.push = op.push; prm.X = X; prm.out = out;
+  prm.val = op.val; prm.idx = op.idx; prm.push = op.push; prm.rptr = op.rptr; prm.rent = op.rent;
+  prm.X = X; prm.out = out;
   prm.ldx = ldx; prm.ldo = ldo; prm.n = op.n;
   prm.R = (int)op.R; prm.w = op.w; prm.H = op.H; prm.P = op.P;
   prm.k = (int)k; prm.K = K; prm.substeps = substeps;

@@ -38,6 +38,8 @@ struct ChebOp {
   double* val = nullptr;    // [w][CHEB_CLUSTER * R] (device)
   uint32_t* idx = nullptr;  // [w][CHEB_CLUSTER * R]: local index into [0, R + H) (own row or halo slot)
   uint32_t* push = nullptr; // [CHEB_CLUSTER][P][2]: (own row, (dest CTA << 24) | dest slot), ~0 = none
+  uint32_t* rptr = nullptr; // [CHEB_CLUSTER][R + 1]: the same pushes grouped by own row (CSR) ...
+  uint32_t* rent = nullptr; // [CHEB_CLUSTER][P]: ... destinations (dest CTA << 24) | dest slot
 };
 
 // Host: from the CSR of A (0-based, n x n) build the partitioned ELL of A^T and the Gershgorin data.
@@ -48,7 +50,7 @@ struct ChebHost {
   int w = 0, H = 0, P = 0, C = 0;
   double a = 0, b = 0, norm1 = 0;
   std::vector<double> val;
-  std::vector<uint32_t> idx, push;
+  std::vector<uint32_t> idx, push, rptr, rent;
 };
 int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* colind,
                  const double* values, ChebHost& out, std::string* err);

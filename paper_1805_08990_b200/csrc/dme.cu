@@ -193,6 +193,8 @@ void plan_buffers(dme_ctx* c, Planner& P) {
     c->cop.val = P.take<double>(ell);
     c->cop.idx = P.take<uint32_t>(ell);
     c->cop.push = P.take<uint32_t>(std::max<size_t>(c->chost.push.size(), 1));
+    c->cop.rptr = P.take<uint32_t>(std::max<size_t>(c->chost.rptr.size(), 1));
+    c->cop.rent = P.take<uint32_t>(std::max<size_t>(c->chost.rent.size(), 1));
   }
   if (c->has_S) c->S = P.take<double>(nn);
   c->Bcol = P.take<double>((size_t)ld * std::max<int64_t>(c->m, 1));
@@ -994,6 +996,10 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     DME_CUDA(cudaMemcpyAsync(c->cop.val, c->chost.val.data(), c->chost.val.size() * 8,
                              cudaMemcpyHostToDevice, st));
     DME_CUDA(cudaMemcpyAsync(c->cop.idx, c->chost.idx.data(), c->chost.idx.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+    DME_CUDA(cudaMemcpyAsync(c->cop.rptr, c->chost.rptr.data(), c->chost.rptr.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+    DME_CUDA(cudaMemcpyAsync(c->cop.rent, c->chost.rent.data(), c->chost.rent.size() * 4,
                              cudaMemcpyHostToDevice, st));
     if (!c->chost.push.empty())
       DME_CUDA(cudaMemcpyAsync(c->cop.push, c->chost.push.data(), c->chost.push.size() * 4,
