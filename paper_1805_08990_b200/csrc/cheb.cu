@@ -235,6 +235,23 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
     }
   };
   const double alpha = p.alpha, beta = p.beta;
+  // C <= 3: the thread's matrix rows stay in registers for the whole polynomial (wider column
+  // groups would spill); else they are re-read from shared memory every degree
+  constexpr bool MREG = C <= 3;
+  double a[2][W];
+  uint32_t e[2][W];
+  if (MREG)
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = u ? i1 : i0;
+    const bool has = u ? h1 : h0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const bool in = has && q < w;
+      a[u][q] = in ? val_s[q * R + i] : 0.0;
+      e[u][q] = in ? idx_s[q * R + i] : 0u;
+    }
+  }
   for (int sub = 0; sub < p.substeps; ++sub) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -263,19 +280,24 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
       for (int u = 0; u < 2; ++u) {
         const int i = u ? i1 : i0;
         if (!(u ? h1 : h0)) continue;
-        double a[W];
-        uint32_t e[W];
+        double am[W];
+        uint32_t em[W];
 #pragma unroll
         for (int q = 0; q < W; ++q) {
-          const bool in = q < w;
-          a[q] = in ? val_s[q * R + i] : 0.0;
-          e[q] = in ? idx_s[q * R + i] : (uint32_t)i;
+          if (MREG) {
+            am[q] = a[u][q];
+            em[q] = e[u][q];
+          } else {
+            const bool in = q < w;
+            am[q] = in ? val_s[q * R + i] : 0.0;
+            em[q] = in ? idx_s[q * R + i] : (uint32_t)i;
+          }
         }
 #pragma unroll
         for (int j = 0; j < C; ++j) {
           double acc = 0.0;
 #pragma unroll
-          for (int q = 0; q < W; ++q) acc = fma(a[q], bc[j * LD + e[q]], acc);
+          for (int q = 0; q < W; ++q) acc = fma(am[q], bc[j * LD + em[q]], acc);
           const double t = alpha * acc - beta * vc[u][j];
           const double vn = kd == 1 ? t : 2.0 * t - vp[u][j];
           vp[u][j] = vc[u][j];
