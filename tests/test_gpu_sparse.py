@@ -159,3 +159,42 @@ def test_fullsize_sparse_three_steps(dme):
     Lo, Do = orc.factor()
     d = lowrank.rel_diff(Lg, Dg, Lo, Do)
     assert d <= TOL_P, d
+
+
+def test_action_wide_rows_fallback_kernel(dme):
+    """Rows wider than 5 entries (w = 9..13) take the shared-memory kernel (vectors and accumulator in
+    shared memory, halo pushes in a separate phase): against expm."""
+    rng = np.random.default_rng(11)
+    n = 300
+    B = sps.random(n, n, density=3.0 / n, random_state=12, format="csr") + sps.eye(n)
+    A = -(B @ B.T) * 50.0  # symmetric negative semidefinite, a few dozen entries per row at most
+    A = sps.csr_matrix(A)
+    assert np.diff(A.indptr).max() > 5
+    h = 0.01
+    s = dme.Solver(A=A, h=h)
+    L = rng.random((n, 11))
+    s.debug_set_factor(L)
+    s.debug_apply("T1", h / 2)
+    Y, _ = s.get_factor()
+    s.close()
+    ref = sla.expm((h / 2) * A.toarray().T) @ L
+    assert np.abs(Y - ref).max() <= 1e-13 * np.abs(L).max()
+
+
+@pytest.mark.slow
+def test_action_large_n_fallback_kernel(dme):
+    """n = 110^2 > 8 x 1280 rows: the shared-memory kernel; sampled rows against the closed form of
+    the 2D heat exponential (pin P5)."""
+    from oracle import exact
+    nx, h = 110, 0.005
+    prob = make_config(5, nx=nx)
+    s = dme.Solver(A=sps.csr_matrix(prob.A), h=h)
+    L = np.random.default_rng(4).random((prob.n, 13))
+    s.debug_set_factor(L)
+    s.debug_apply("T1", h)
+    Y, _ = s.get_factor()
+    s.close()
+    E1 = exact.heat_expm_closed_form(nx, h, 1)
+    for i in np.random.default_rng(5).integers(0, prob.n, 40):
+        Erow = np.kron(E1[i // nx], E1[i % nx])
+        assert np.abs(Y[i] - Erow @ L).max() <= 1e-13 * np.abs(L).max()
