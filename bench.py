@@ -375,6 +375,22 @@ def run_ours(args):
                                          if st4["prof_epass_seconds"] > 0 else None)}
         s4.close()
         del s4
+        # end to end through the public API: host CSR in, factor on the host out
+        torch.cuda.synchronize()
+        t5 = time.perf_counter()
+        s5 = dme.Solver(**kw_sp, **kw)
+        s5.split_step("strang", "F12F3", NT)
+        L5, D5 = s5.get_factor()
+        torch.cuda.synchronize()
+        t_e2e5 = time.perf_counter() - t5
+        s5.close()
+        del s5
+        sparse["e2e"] = {"value": NT / t_e2e5, "unit": UNIT, "time_to_T_s": t_e2e5,
+                         "h2d_bytes_per_step": (A_csr.data.nbytes + A_csr.indices.nbytes +
+                                                A_csr.indptr.nbytes + sum(a.nbytes for a in (
+                                                    prob.C, prob.B, prob.R, prob.L0, prob.D0)
+                                                    if a is not None)) / NT,
+                         "d2h_bytes_per_step": (L5.nbytes + D5.nbytes) / NT}
 
     cb = None
     if args.config != 5:  # the oracle's dense E for a nonsymmetric A M^-1 takes minutes: not a bounded sample
