@@ -138,7 +138,16 @@ typedef struct {
                              squarings of the (replicated) init use the same int8 kernel
                              (square tiles); DME_EPASS_DMMA: every E pass and every init
                              product in native FP64 DMMA (mma.sync m8n8k4 f64)                  */
+  int32_t expm;           /* how the dense path builds E_{h/2} (dme_expm): DME_EXPM_AUTO
+                             (default): when A is exactly symmetric and sparse (<= 16 n nonzeros,
+                             found by a device scan of the uploaded A, one GPU), E_{h/2} =
+                             exp((h/2) A^T) I column block by column block with the Chebyshev
+                             actions of the sparse path and the quadrature factors
+                             by Chebyshev actions too; E_h = E_{h/2}^2 as before. Otherwise, or
+                             with DME_EXPM_PADE, scaling-and-squaring Padé-13                  */
 } dme_options;
+
+typedef enum { DME_EXPM_AUTO = 0, DME_EXPM_PADE = 1 } dme_expm;
 
 typedef enum { DME_EPASS_AUTO = 0, DME_EPASS_DMMA = 1 } dme_e_pass;
 
@@ -168,7 +177,9 @@ typedef struct {
   int64_t eig_fallbacks;    /* fast eigen-compressions that failed the orthogonality check and
                                were redone by the Jacobi kernel                                 */
   int64_t ozaki_passes;     /* E passes run on the int8 tensor cores (options.e_pass)          */
-  int64_t cheb_degree;      /* sparse A: polynomial degree of the E_h action (sum over substeps) */
+  int64_t cheb_degree;      /* sparse A: polynomial degree of the E_h action (sum over substeps);
+                               dense A with a Chebyshev-built E: the degree used for E_{h/2}     */
+  int64_t expm_chebyshev;   /* 1 if E_{h/2} was built by Chebyshev actions, 0 for Padé-13     */
 } dme_stats;
 
 void dme_default_options(dme_options* opt);

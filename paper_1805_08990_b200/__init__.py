@@ -50,7 +50,7 @@ class _Options(ctypes.Structure):
                 ("world_rank", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("big_inputs_on_device", ctypes.c_int32), ("no_fsal", ctypes.c_int32),
-                ("e_pass", ctypes.c_int32)]
+                ("e_pass", ctypes.c_int32), ("expm", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -65,7 +65,8 @@ class _Stats(ctypes.Structure):
                 ("prof_epass_flops", ctypes.c_double), ("prof_epass_bytes", ctypes.c_double),
                 ("prof_gram_seconds", ctypes.c_double), ("prof_small_seconds", ctypes.c_double),
                 ("prof_apply_seconds", ctypes.c_double), ("eig_fallbacks", ctypes.c_int64),
-                ("ozaki_passes", ctypes.c_int64), ("cheb_degree", ctypes.c_int64)]
+                ("ozaki_passes", ctypes.c_int64), ("cheb_degree", ctypes.c_int64),
+                ("expm_chebyshev", ctypes.c_int64)]
 
 
 _ctx_p = ctypes.c_void_p
@@ -155,6 +156,7 @@ def unique_id() -> bytes:
 
 
 E_PASS = {"auto": 0, "dmma": 1}
+EXPM = {"auto": 0, "pade": 1}
 
 
 def cheb_coeffs(gamma: float, tol: float = 2.0 ** -56) -> np.ndarray:
@@ -177,7 +179,7 @@ class Solver:
                  trunc_tol=1e-16,
                  rank_cap=0, quad_nodes=14, quad_subpanels=1, device=None, stream=None,
                  world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None, fsal=True,
-                 e_pass="auto", poison_workspace=False):
+                 e_pass="auto", expm="auto", poison_workspace=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1805_08990_b200.Solver needs a CUDA device (no CPU fallback)")
@@ -232,7 +234,7 @@ class Solver:
                        stream=self.stream.cuda_stream, world_size=world_size,
                        world_rank=world_rank, nccl_uid=ctypes.cast(uid, ctypes.c_void_p) if uid else None,
                        workspace=None, workspace_bytes=0, big_inputs_on_device=1 if on_dev else 0,
-                       no_fsal=0 if fsal else 1, e_pass=E_PASS[e_pass])
+                       no_fsal=0 if fsal else 1, e_pass=E_PASS[e_pass], expm=EXPM[expm])
         nbytes = ctypes.c_size_t(0)
         _check(_lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(opt), ctypes.byref(nbytes)),
                "dme_workspace_size")

@@ -389,6 +389,65 @@ int max_active_clusters(int C, size_t smem) {
 
 }  // namespace
 
+namespace {
+// one warp per row of the row-major A: nonzero count, then the entries in column order
+__global__ void csr_count_kernel(const double* A, int64_t n, int64_t ld, int64_t* cnt) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  int64_t c = 0;
+  for (int64_t j = lane; j < n; j += 32) c += A[row * ld + j] != 0.0;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[row] = c;
+}
+__global__ void csr_fill_kernel(const double* A, int64_t n, int64_t ld, const int64_t* rowptr,
+                                int32_t* col, double* val) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  int64_t pos = rowptr[row];
+  for (int64_t j0 = 0; j0 < n; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const double a = j < n ? A[row * ld + j] : 0.0;
+    const unsigned m = __ballot_sync(0xffffffffu, a != 0.0);
+    if (a != 0.0) {
+      const int64_t d = pos + __popc(m & ((1u << lane) - 1u));
+      col[d] = (int32_t)j;
+      val[d] = a;
+    }
+    pos += __popc(m);
+  }
+}
+}  // namespace
+
+int cheb_csr_from_dense(const double* A, int64_t n, int64_t ld, int64_t max_nnz, void* scratch,
+                        cudaStream_t st, std::vector<int64_t>& rowptr, std::vector<int32_t>& col,
+                        std::vector<double>& val) {
+  int64_t* cnt = reinterpret_cast<int64_t*>(scratch);
+  const unsigned blocks = (unsigned)ceil_div(n, 8);
+  csr_count_kernel<<<blocks, 256, 0, st>>>(A, n, ld, cnt);
+  DME_KCHECK();
+  std::vector<int64_t> c(n);
+  DME_CUDA(cudaMemcpyAsync(c.data(), cnt, n * 8, cudaMemcpyDeviceToHost, st));
+  DME_CUDA(cudaStreamSynchronize(st));
+  rowptr.assign(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) rowptr[i + 1] = rowptr[i] + c[i];
+  const int64_t nnz = rowptr[n];
+  if (nnz > max_nnz) return 0;
+  int64_t* rp = cnt;  // rowptr on the device (over the counts), then col / val behind it
+  int32_t* cd = reinterpret_cast<int32_t*>(rp + n + 1);
+  double* vd = reinterpret_cast<double*>(cd + ((nnz + 1) & ~int64_t(1)));
+  DME_CUDA(cudaMemcpyAsync(rp, rowptr.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  csr_fill_kernel<<<blocks, 256, 0, st>>>(A, n, ld, rp, cd, vd);
+  DME_KCHECK();
+  col.resize(nnz);
+  val.resize(nnz);
+  DME_CUDA(cudaMemcpyAsync(col.data(), cd, nnz * 4, cudaMemcpyDeviceToHost, st));
+  DME_CUDA(cudaMemcpyAsync(val.data(), vd, nnz * 8, cudaMemcpyDeviceToHost, st));
+  DME_CUDA(cudaStreamSynchronize(st));
+  return 1;
+}
+
 size_t cheb_smem_bytes_reg(int64_t R, int w, int H, int P, int C) {
   return (size_t)R * w * 12 + (size_t)(R + H) * C * 16 + (size_t)(R + 1 + P) * 4 + 64;
 }

@@ -56,6 +56,13 @@ int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* c
                  const double* values, ChebHost& out, std::string* err);
 size_t cheb_smem_bytes(int64_t R, int w, int H, int P, int C);
 
+// CSR of a dense row-major device matrix (nonzero pattern, exact values), if it has at most max_nnz
+// nonzeros (returns 1; 0 = too dense). scratch: device memory of >= (n + 1) * 8 + max_nnz * 12 + 8
+// bytes. Used by the dense path to evaluate E_{h/2} by Chebyshev actions when A is sparse.
+int cheb_csr_from_dense(const double* A, int64_t n, int64_t ld, int64_t max_nnz, void* scratch,
+                        cudaStream_t st, std::vector<int64_t>& rowptr, std::vector<int32_t>& col,
+                        std::vector<double>& val);
+
 // chat[k] = e^{-gamma} I_k(gamma), k = 0..K, with K the smallest degree whose tail
 // 2 sum_{j > K} chat[j] <= tol. Returns K (chat resized to K + 1). Miller's backward recurrence,
 // normalised by e^{gamma} = I_0 + 2 sum I_k (all terms positive).

@@ -154,6 +154,7 @@ struct dme_ctx {
   bool fsal = true;
   // sparse A: Chebyshev exponential actions instead of dense E (cheb.h)
   bool sparse = false;
+  bool cheb_e = false;  // dense path, sparse symmetric A: E_{h/2} and L_I by Chebyshev actions
   ChebHost chost;
   ChebOp cop;
   ncclComm_t comm = nullptr;
@@ -967,7 +968,7 @@ void matmul_sq(dme_ctx* c, const double* X, const double* Y, double* out) {
 void ladder_double(dme_ctx* c, double* LI, int64_t& q, const double* Ew, double w) {
   if (q == 0) return;
   DME_REQUIRE(2 * q <= KMAX, DME_ERR_DIM, "quadrature factor rank exceeds 112");
-  if (c->sparse) sparse_pass(c, w, LI, q, LI + q * c->ldn, c->ldn, c->st);
+  if (c->sparse || c->cheb_e) sparse_pass(c, w, LI, q, LI + q * c->ldn, c->ldn, c->st);
   else epass(c, Ew, LI, q, LI + q * c->ldn, c->ldn, 1.0);
   const int64_t qn = compress(c, LI, 2 * q, c->Ztmp, false, 0.0);
   copy_cols(LI, c->ldn, c->Ztmp, c->ldn, c->n, qn, 1.0, c->st);
@@ -1090,13 +1091,48 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   // X0 = delta * A^T
   if (!c->sparse) transpose_scale(c->Aup, n, ld, delta, c->X0, ld, st);
 
+  // dense A that is exactly symmetric and sparse: Chebyshev actions (cheb.h) build E_{h/2} and the
+  // quadrature factors; the partitioned ELL goes into the init-only Padé buffers (unused here)
+  c->cheb_e = false;
+  if (!c->sparse && c->symA && c->opt.expm != DME_EXPM_PADE && c->world == 1) {
+    std::vector<int64_t> rp;
+    std::vector<int32_t> ci;
+    std::vector<double> vv;
+    if (cheb_csr_from_dense(c->Aup, n, ld, 16 * n, c->X2, st, rp, ci, vv)) {
+      ChebHost ch;
+      std::string err;
+      if (cheb_prepare(n, (int64_t)vv.size(), rp.data(), ci.data(), vv.data(), ch, &err) == 0 &&
+          (size_t)ch.w * CHEB_CLUSTER * ch.R <= (size_t)n * ld && ch.push.size() <= (size_t)n * ld &&
+          ch.rptr.size() <= (size_t)n * ld && ch.rent.size() <= (size_t)n * ld) {
+        c->chost = std::move(ch);
+        ChebOp& op = c->cop;
+        op.n = c->chost.n; op.R = c->chost.R; op.w = c->chost.w; op.C = c->chost.C;
+        op.H = c->chost.H; op.P = c->chost.P;
+        op.a = c->chost.a; op.b = c->chost.b; op.norm1 = c->chost.norm1;
+        op.val = c->X4;
+        op.idx = reinterpret_cast<uint32_t*>(c->X6);
+        op.push = reinterpret_cast<uint32_t*>(c->U);
+        op.rptr = reinterpret_cast<uint32_t*>(c->V);
+        op.rent = reinterpret_cast<uint32_t*>(c->BT);
+        DME_CUDA(cudaMemcpyAsync(op.val, c->chost.val.data(), c->chost.val.size() * 8, cudaMemcpyHostToDevice, st));
+        DME_CUDA(cudaMemcpyAsync(op.idx, c->chost.idx.data(), c->chost.idx.size() * 4, cudaMemcpyHostToDevice, st));
+        if (!c->chost.push.empty())
+          DME_CUDA(cudaMemcpyAsync(op.push, c->chost.push.data(), c->chost.push.size() * 4, cudaMemcpyHostToDevice, st));
+        DME_CUDA(cudaMemcpyAsync(op.rptr, c->chost.rptr.data(), c->chost.rptr.size() * 4, cudaMemcpyHostToDevice, st));
+        DME_CUDA(cudaMemcpyAsync(op.rent, c->chost.rent.data(), c->chost.rent.size() * 4, cudaMemcpyHostToDevice, st));
+        c->cheb_e = true;
+      }
+    }
+  }
+  c->stats.expm_chebyshev = c->cheb_e ? 1 : 0;
+
   // ---------------------------------------------------------------- first-panel node actions
   // Y_i = exp(c_i delta A^T) L_Q = sum_j c_i^j W_j,  W_j = (delta A^T) W_{j-1} / j   (Taylor)
   const int q = c->qn;
   std::vector<double> cn, wn;
   gauss_legendre01(q, cn, wn);
   int64_t qI = 0;
-  if (c->p > 0 && c->sparse) {  // Y_i = exp(c_i delta A^T) L_Q by the Chebyshev action
+  if (c->p > 0 && (c->sparse || c->cheb_e)) {  // Y_i = exp(c_i delta A^T) L_Q by the Chebyshev action
     for (int i = 0; i < q; ++i)
       sparse_pass(c, cn[i] * delta, c->LQ, c->p, c->Yn + (size_t)i * c->p * ld, ld, st);
   } else if (c->p > 0) {
@@ -1137,7 +1173,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     copy_cols(c->Zc12h, ld, c->Ztmp, ld, n, qI, 1.0, st);
   }
 
-  if (c->sparse) {
+  if (c->sparse || c->cheb_e) {
     // ---------------------------------------------------------------- ladder by sparse actions
     int64_t q_cur = qI;
     for (int j = 0; j < s_total; ++j) ladder_double(c, c->Zc12h, q_cur, nullptr, std::ldexp(delta, j));
@@ -1146,6 +1182,19 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     int64_t qf = c->qh;
     ladder_double(c, c->Zc12f, qf, nullptr, tau0);
     c->qf = qf;
+    if (c->cheb_e) {
+      // E_{h/2} = exp((h/2) A^T) I (columns = rows: A symmetric), exactly symmetrised; E_h = E_{h/2}^2
+      lincomb(c->T1, n, ld, {}, {}, {}, {}, 1.0, st);
+      c->stats.cheb_degree = cheb_action(c->cop, tau0, c->T1, ld, n, c->E_half, ld, 1.0, st);
+      mirror_lower(c->E_half, n, ld, true, st);
+      matmul_sq(c, c->E_half, c->E_half, c->E_full);
+      if (c->oz) {
+        oz_slice_rows_tiled(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->exEh, c->ozpm, st);
+        oz_slice_rows_tiled(c->E_full + c->row0 * ld, ld, c->rows_loc, n, c->ozEf, c->exEf, c->ozpm, st);
+        c->oz_ready = true;
+      }
+      c->cheb_e = false;  // the passes of the run use the dense E
+    }
   } else {
   // ---------------------------------------------------------------- Padé-13 on X0 (Higham 2005)
   const double* b = PADE_B;

@@ -32,6 +32,7 @@ def solver(prob):
 
 
 def test_fullsize_expm_sampled(solver):
+    assert solver.stats()["expm_chebyshev"] == 1  # sparse symmetric A: Chebyshev-built E_{h/2}
     rng = np.random.default_rng(0)
     n = NX * NX
     rows = np.concatenate([rng.integers(0, n, 3000), np.arange(0, n, 97)])
@@ -48,6 +49,23 @@ def test_fullsize_expm_sampled(solver):
         assert err <= 2e-15 * np.abs(E).sum(axis=1).max(), (which, err)
         # symmetry of the symmetric-A path
         assert np.array_equal(E[rows, cols], E[cols, rows])
+
+
+def test_fullsize_expm_pade_sampled(prob):
+    """The same sampled check for the Padé-13 scaling-and-squaring E (options.expm = PADE; the
+    default builds E_{h/2} of this sparse symmetric A by Chebyshev actions)."""
+    import paper_1805_08990_b200 as dme
+    s = dme.Solver(**dme.problem_kwargs(prob), h=H, rank_cap=64, expm="pade")
+    assert s.stats()["expm_chebyshev"] == 0
+    rng = np.random.default_rng(7)
+    n = NX * NX
+    rows = rng.integers(0, n, 4000)
+    cols = np.clip(rows + rng.integers(-NX - 2, NX + 3, 4000), 0, n - 1)
+    for which, t in ((0, H / 2), (1, H)):
+        E = s.debug_get_exp(which)
+        ref = exact.heat_expm_entries(NX, t, rows, cols)
+        assert np.abs(E[rows, cols] - ref).max() <= 2e-15 * np.abs(E).sum(axis=1).max()
+    s.close()
 
 
 def test_fullsize_T1_sampled_rows(prob):
