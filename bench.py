@@ -166,7 +166,8 @@ def run_ours(args):
 
     # ------------------------------------------------------------ device-resident timed region
     # A (800 MB) resident in HBM before the clock starts (options.big_inputs_on_device); the init
-    # (validation, Padé expm, quadrature ladder, P0 compression) is timed as part of time-to-T.
+    # (validation, expm: Chebyshev actions for this sparse symmetric A or Padé-13, quadrature ladder,
+    # P0 compression) is timed as part of time-to-T.
     # one tiny solve first: loads the library's kernels into the context (lazy module loading is a
     # once-per-process cost, not part of solving) and allocates the pinned rank record
     tiny = make_config(args.config, nx=8)

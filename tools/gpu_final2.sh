@@ -11,3 +11,5 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:cheb
 ncu -i $O/cheb_one.ncu-rep --page details > $O/cheb_details.txt 2>&1
 tail -3 $O/pytest_gpu.log; tail -2 $O/smoke.log; python -c "
 import json; d=json.load(open('gpurun_out/bench5.json')); print(d['value'], d['time_to_T_s'], d['roofline']['frac']); print(json.dumps(d['sparse_variant']))"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_final.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-variant --no-sparse > /dev/null 2>&1
+python tools/launch_summary.py $O/launches_final.csv > $O/launches_summary.txt 2>&1; tail -3 $O/launches_summary.txt
