@@ -1094,7 +1094,9 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   // dense A that is exactly symmetric and sparse: Chebyshev actions (cheb.h) build E_{h/2} and the
   // quadrature factors; the partitioned ELL goes into the init-only Padé buffers (unused here)
   c->cheb_e = false;
-  if (!c->sparse && c->symA && c->opt.expm != DME_EXPM_PADE && c->world == 1) {
+  // (the CSR scratch lives in X2: (n + 1) rows offsets and up to 16 n entries must fit)
+  if (!c->sparse && c->symA && c->opt.expm != DME_EXPM_PADE && c->world == 1 &&
+      (size_t)(n + 1) * 8 + (size_t)16 * n * 12 + 16 <= (size_t)n * ld * 8) {
     std::vector<int64_t> rp;
     std::vector<int32_t> ci;
     std::vector<double> vv;
