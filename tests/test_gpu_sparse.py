@@ -198,3 +198,24 @@ def test_action_large_n_fallback_kernel(dme):
     for i in np.random.default_rng(5).integers(0, prob.n, 40):
         Erow = np.kron(E1[i // nx], E1[i % nx])
         assert np.abs(Y[i] - Erow @ L).max() <= 1e-13 * np.abs(L).max()
+
+
+@pytest.mark.parametrize("nx", [5, 20, 33])
+def test_dense_A_chebyshev_E_matches_pade(dme, nx):
+    """Dense input, sparse symmetric A: the default init builds E_{h/2} by Chebyshev actions
+    (options.expm = AUTO; n >= 17, else Padé); both E against the DST closed form (pin P5)."""
+    from oracle import exact
+    prob = make_config(5, nx=nx)
+    h = 0.005
+    sa = dme.Solver(**dme.problem_kwargs(prob), h=h, rank_cap=64)
+    sp = dme.Solver(**dme.problem_kwargs(prob), h=h, rank_cap=64, expm="pade")
+    assert sa.stats()["expm_chebyshev"] == (1 if prob.n >= 17 else 0)
+    assert sp.stats()["expm_chebyshev"] == 0
+    for which, t in ((0, h / 2), (1, h)):
+        ref = exact.heat_expm_closed_form(nx, t, 2)
+        for s in (sa, sp):
+            E = s.debug_get_exp(which)
+            assert np.abs(E - ref).max() <= 2e-15 * np.abs(ref).sum(axis=1).max()
+            assert np.array_equal(E, E.T)
+    sa.close()
+    sp.close()
