@@ -140,7 +140,7 @@ typedef struct {
                              product in native FP64 DMMA (mma.sync m8n8k4 f64)                  */
   int32_t expm;           /* how the dense path builds E_{h/2} (dme_expm): DME_EXPM_AUTO
                              (default): when A is exactly symmetric and sparse (<= 16 n nonzeros,
-                             found by a device scan of the uploaded A, one GPU), E_{h/2} =
+                             found by a device scan of the uploaded A; replicated per rank like the Padé init), E_{h/2} =
                              exp((h/2) A^T) I column block by column block with the Chebyshev
                              actions of the sparse path and the quadrature factors
                              by Chebyshev actions too; E_h = E_{h/2}^2 as before. Otherwise, or

@@ -1095,7 +1095,8 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   // quadrature factors; the partitioned ELL goes into the init-only Padé buffers (unused here)
   c->cheb_e = false;
   // (the CSR scratch lives in X2: (n + 1) rows offsets and up to 16 n entries must fit)
-  if (!c->sparse && c->symA && c->opt.expm != DME_EXPM_PADE && c->world == 1 &&
+  // (replicated on every rank like the Padé init: identical inputs, deterministic kernels)
+  if (!c->sparse && c->symA && c->opt.expm != DME_EXPM_PADE &&
       (size_t)(n + 1) * 8 + (size_t)16 * n * 12 + 16 <= (size_t)n * ld * 8) {
     std::vector<int64_t> rp;
     std::vector<int32_t> ci;
