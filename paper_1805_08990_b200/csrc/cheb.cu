@@ -619,9 +619,30 @@ int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* c
   return 0;
 }
 
+namespace {
+// First use in a process: set the shared-memory attribute of every kernel instance (which also
+// loads it under lazy module loading), so no later call pays a module load inside a timed init.
+template <int C>
+void preload_c() {
+  for (auto f : {cheb_kernel<C, 3>, cheb_kernel<C, 5>, cheb_kernel<C, 8>, cheb_kernel<C, 4>})
+    DME_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+  if constexpr (C <= CHEB_REG_CMAX)
+    for (auto f : {cheb_reg_kernel<C, 3>, cheb_reg_kernel<C, 5>})
+      DME_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+}
+void preload_all() {
+  static bool done = false;
+  if (done) return;
+  preload_c<1>(); preload_c<2>(); preload_c<3>(); preload_c<4>();
+  preload_c<5>(); preload_c<6>(); preload_c<7>(); preload_c<8>();
+  done = true;
+}
+}  // namespace
+
 int cheb_action(const ChebOp& op, double tau, const double* X, int64_t ldx, int64_t k, double* out,
                 int64_t ldo, double alpha, cudaStream_t st) {
   if (k <= 0) return 0;
+  preload_all();
   ChebParams prm;
   std::memset(&prm, 0, sizeof(prm));
   // interval of tau A^T (tau > 0): [tau a, tau b]; substeps keep the degree within CHEB_KMAX
