@@ -88,9 +88,9 @@ typedef struct {
   const double* M;    /* n x n mass matrix or NULL (Example 4): the equation is
                          M^T P' M = A^T P M + M^T P A + C^T C [- M^T P B R^-1 B^T P M]
                          [+ M^T S P S^T M is NOT supported with M]; init cancels M once
-                         (P:L357-359): A <- A M^-1, C <- C M^-1 (dense LU without pivoting,
-                         P:L362 "compute and store a dense LU factorization"; M must admit
-                         it, e.g. SPD mass matrices; DME_ERR_NUMERIC on a tiny pivot).
+                         (P:L357-359): A <- A M^-1, C <- C M^-1 (dense LU,
+                         P:L362 "compute and store a dense LU factorization", with partial
+                         pivoting; DME_ERR_NUMERIC on an exactly singular M).
                          Same memory space as A (host, or device with big_inputs_on_device).
                          Callers that zero-initialise the struct get M = NULL.              */
   /* Sparse A (the paper's own setting, P:L199 / P:L303-307: exp(tau A^T) L as a
@@ -145,7 +145,19 @@ typedef struct {
                              actions of the sparse path and the quadrature factors
                              by Chebyshev actions too; E_h = E_{h/2}^2 as before. Otherwise, or
                              with DME_EXPM_PADE, scaling-and-squaring Padé-13                  */
+  int32_t compression;    /* how a column compression resolves the eigenvalues of P = Zc Zc^T
+                             (dme_compression). DME_COMPRESS_REFINED (default): the FP64 Gram
+                             G = Zc^T Zc only resolves eigenvalues down to ~k eps theta_max, so a
+                             first eigen pass keeps theta > 1e-11 theta_max (accurate), and the
+                             rest is recomputed from the explicit projected factor
+                             Zs = Zc (I - W W^T) (its Gram resolves down to ~eps^2 theta_max):
+                             the truncation then honours trunc_tol down to 1e-16 as the paper's
+                             reduced-SVD compression does.
+                             DME_COMPRESS_GRAM: the single Gram pass, with the effective
+                             tolerance max(trunc_tol, 1e-14)                                    */
 } dme_options;
+
+typedef enum { DME_COMPRESS_REFINED = 0, DME_COMPRESS_GRAM = 1 } dme_compression;
 
 typedef enum { DME_EXPM_AUTO = 0, DME_EXPM_PADE = 1 } dme_expm;
 
@@ -197,8 +209,10 @@ dme_status dme_get_unique_id(void* uid128);
 dme_status dme_shard_rows(int64_t n, int32_t world, int32_t rank, int64_t* row0, int64_t* rows,
                           int64_t* nloc);
 
-/* Build the context: upload, Padé-13 expm of (h/2)A^T and its square, quadrature factors,
- * compression of P0. dle_init requires m == 0; dre_init requires m >= 1. Collective. */
+/* Build the context: upload, E_{h/2} = exp((h/2)A^T) (options.expm: Chebyshev actions for an
+ * exactly symmetric sparse-pattern A under AUTO, else scaling-and-squaring Padé-13 with a pivoted
+ * LU solve) and E_h = E_{h/2}^2, quadrature factors, compression of P0. dle_init requires m == 0;
+ * dre_init requires m >= 1. Collective. */
 dme_status dme_dle_init(const dme_problem* prob, const dme_options* opt, dme_ctx** ctx);
 dme_status dme_dre_init(const dme_problem* prob, const dme_options* opt, dme_ctx** ctx);
 
@@ -244,6 +258,10 @@ dme_status dme_debug_apply(dme_ctx* ctx, int32_t flow, double tau);
 dme_status dme_debug_set_factor(dme_ctx* ctx, int64_t r, const double* L);
 /* Copy E_{h/2} (which = 0) or E_h (which = 1) to the host (n x n). */
 dme_status dme_debug_get_exp(dme_ctx* ctx, int32_t which, double* E);
+/* Replace E_{h/2} (which = 0) or E_h (which = 1) by a host matrix (n x n, row-major; e.g. an oracle
+ * exponential: the SURVEY's "minimum slice" hook). The quadrature factors built at init are kept;
+ * the int8 digit image of the E pass is re-sliced. DME_ERR_CONFIG with a sparse A. */
+dme_status dme_debug_set_exp(dme_ctx* ctx, int32_t which, const double* E);
 /* Copy L_I(h/2) (which = 0) or L_I(h) (which = 1), P_I = L_I L_I^T, n x q, to the host. */
 dme_status dme_debug_get_integral(dme_ctx* ctx, int32_t which, int64_t* q, double* L,
                                   int64_t capacity_cols);

@@ -50,7 +50,8 @@ class _Options(ctypes.Structure):
                 ("world_rank", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("big_inputs_on_device", ctypes.c_int32), ("no_fsal", ctypes.c_int32),
-                ("e_pass", ctypes.c_int32), ("expm", ctypes.c_int32)]
+                ("e_pass", ctypes.c_int32), ("expm", ctypes.c_int32),
+                ("compression", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -90,6 +91,7 @@ for _name, _args in {
     "dme_debug_apply": [_ctx_p, ctypes.c_int32, ctypes.c_double],
     "dme_debug_set_factor": [_ctx_p, ctypes.c_int64, _dp],
     "dme_debug_get_exp": [_ctx_p, ctypes.c_int32, _dp],
+    "dme_debug_set_exp": [_ctx_p, ctypes.c_int32, _dp],
     "dme_debug_get_integral": [_ctx_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), _dp,
                                ctypes.c_int64],
     "dme_debug_matmul": [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp],
@@ -104,7 +106,7 @@ for _name, _args in {
 EXPORTED = ["dme_default_options", "dme_status_string", "dme_last_error", "dme_workspace_size",
             "dme_get_unique_id", "dme_shard_rows", "dme_dle_init", "dme_dre_init", "dme_split_step",
             "dme_get_factor", "dme_extrapolate", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
-            "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_get_integral",
+            "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_set_exp", "dme_debug_get_integral",
             "dme_debug_small_stats", "dme_debug_matmul", "dme_debug_matmul_ozaki", "dme_cheb_coeffs"]
 
 
@@ -157,6 +159,7 @@ def unique_id() -> bytes:
 
 E_PASS = {"auto": 0, "dmma": 1}
 EXPM = {"auto": 0, "pade": 1}
+COMPRESSION = {"refined": 0, "gram": 1}
 
 
 def cheb_coeffs(gamma: float, tol: float = 2.0 ** -56) -> np.ndarray:
@@ -179,7 +182,7 @@ class Solver:
                  trunc_tol=1e-16,
                  rank_cap=0, quad_nodes=14, quad_subpanels=1, device=None, stream=None,
                  world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None, fsal=True,
-                 e_pass="auto", expm="auto", poison_workspace=False):
+                 e_pass="auto", expm="auto", compression="refined", poison_workspace=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1805_08990_b200.Solver needs a CUDA device (no CPU fallback)")
@@ -234,7 +237,8 @@ class Solver:
                        stream=self.stream.cuda_stream, world_size=world_size,
                        world_rank=world_rank, nccl_uid=ctypes.cast(uid, ctypes.c_void_p) if uid else None,
                        workspace=None, workspace_bytes=0, big_inputs_on_device=1 if on_dev else 0,
-                       no_fsal=0 if fsal else 1, e_pass=E_PASS[e_pass], expm=EXPM[expm])
+                       no_fsal=0 if fsal else 1, e_pass=E_PASS[e_pass], expm=EXPM[expm],
+                       compression=COMPRESSION[compression])
         nbytes = ctypes.c_size_t(0)
         _check(_lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(opt), ctypes.byref(nbytes)),
                "dme_workspace_size")
@@ -284,6 +288,10 @@ class Solver:
         E = np.zeros((self.n, self.n))
         _check(_lib.dme_debug_get_exp(self._ctx, which, _ptr(E)), "dme_debug_get_exp")
         return E
+
+    def debug_set_exp(self, which: int, E):
+        E = _f64(E)
+        _check(_lib.dme_debug_set_exp(self._ctx, which, _ptr(E)), "dme_debug_set_exp")
 
     def debug_get_integral(self, which: int):
         q = ctypes.c_int64(0)

@@ -53,7 +53,12 @@ const double PADE_B[14] = {64764752532480000.0, 32382376266240000.0, 77717703038
 const double THETA13 = 5.371920351148152;
 
 constexpr int64_t KMAX = SMALL_K_MAX;  // column capacity of every factor buffer
-constexpr double GRAM_FLOOR = 1e-14;    // effective relative truncation floor of the Gram eigen-compression
+constexpr double GRAM_FLOOR = 1e-14;    // effective tolerance floor of the single-pass Gram compression
+constexpr double SPLIT_TOL = 1e-11;     // refined compression: first pass keeps theta > 1e-11 theta_max
+// The oracle compresses the whole composite rule once (reading G6); the ladder compresses at every
+// rung, so the rungs below the final L_I(h/2), L_I(h) keep 64x finer directions and only the final
+// factors are truncated at trunc_tol (their ranks then match a one-shot truncation)
+constexpr double LADDER_TOL = 1.0 / 64;
 
 // Gauss-Legendre nodes/weights on [0,1] by Newton on P_q (Golub-Welsch-free; own implementation)
 void gauss_legendre01(int q, std::vector<double>& c, std::vector<double>& w) {
@@ -112,6 +117,11 @@ struct dme_ctx {
   double *Zc12h = nullptr, *Zc12f = nullptr, *Zc2 = nullptr, *Z = nullptr, *Ztmp = nullptr;
   double *G = nullptr, *H = nullptr, *Tm = nullptr, *Vg = nullptr, *Es = nullptr, *LRinv = nullptr, *sstats = nullptr;
   double *norm_dev = nullptr, *red_scratch = nullptr, *stage = nullptr;
+  double *Zs = nullptr, *Gs = nullptr, *Pp = nullptr;  // refined compression: Zc (I - W W^T), its Gram, I - W W^T
+  bool refine = true;      // options.compression == DME_COMPRESS_REFINED
+  double tol_scale = 1.0;  // intermediate quadrature-ladder compressions run at trunc_tol * LADDER_TOL
+  double last_st[5] = {0, 0, 0, 0, 0};  // stats of the last small-kernel pass read by the host
+  cudaEvent_t ev_zc = nullptr, ev_tm = nullptr;
   double *LA = nullptr;  // look-ahead operand [E_h L_I(h) | E_h Y]  (ldn x KMAX)
   // Gram-congruence pipeline (run_f12f3_body): GB = [L_I(h) | B | E_h L_I(h) | E_h Y] (ldn x KMAX),
   // its Gram Ghat (KMAX^2), double-buffered eigen-compression output Tm / Tm2
@@ -172,7 +182,7 @@ struct dme_ctx {
     if (hmap) cudaFreeHost(hmap);
     if (ev_gram) cudaEventDestroy(ev_gram);
     if (ev_ahead) cudaEventDestroy(ev_ahead);
-    for (cudaEvent_t e : {ev_ghat, ev_cong, ev_y})
+    for (cudaEvent_t e : {ev_ghat, ev_cong, ev_y, ev_zc, ev_tm})
       if (e) cudaEventDestroy(e);
     if (tl_base) cudaEventDestroy(tl_base);
   }
@@ -225,6 +235,9 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   c->gs2.partial = P.take<double>(GemmScratch::partial_doubles(c->gs2.max_grid));
   c->gs2.counters = P.take<int>((size_t)c->gs2.max_tiles);
   c->LA = P.take<double>(fk);
+  c->Zs = P.take<double>(fk);
+  c->Gs = P.take<double>((size_t)KMAX * KMAX);
+  c->Pp = P.take<double>((size_t)KMAX * KMAX);
   c->GB = P.take<double>(fk);
   c->Ghat = P.take<double>((size_t)KMAX * KMAX);
   c->Tm2 = P.take<double>((size_t)KMAX * KMAX);
@@ -309,6 +322,7 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->rank_cap = (int32_t)std::min<int64_t>(cap, KMAX);
   c->h = o->h;
   c->fsal = o->no_fsal == 0;
+  c->refine = o->compression == DME_COMPRESS_REFINED;
   c->sparse = pr->A == nullptr && pr->A_rowptr != nullptr;
   if (c->sparse) {
     std::string err;
@@ -594,16 +608,49 @@ void eact(dme_ctx* c, bool full, const double* X, int64_t k, double* out, int64_
   eact_on(c, full, X, k, out, ldo, c->st, c->gs);
 }
 
+// Column compression of Zc (n x k) with the Riccati flow T3(tau3) optionally fused (t3).
+// Single pass (options.compression = GRAM, or trunc_tol >= SPLIT_TOL): G = Zc^T Zc = W Theta W^T,
+// Tm = W_kept (theta > tol theta_max), T3 fused in the eigen kernel.
+// Refined (default): the FP64 Gram resolves eigenvalues only down to ~k eps theta_max, so
+//   pass 1  keeps theta > SPLIT_TOL theta_max of G (accurate): W_b (k x kb);
+//   pass 2  Zs = Zc (I - W_b W_b^T) explicitly (n-row product), G_s = Zs^T Zs: its eigenvalues are
+//           the rest of P's spectrum resolved to ~eps^2 theta_max (the explicit columns carry an
+//           absolute error ~eps sqrt(theta_max), not eps theta_max); keep mu > tol theta_max, at
+//           most cap - kb: V_s;
+//   Tm = [W_b | V_s] (P = Zc W_b W_b^T Zc^T + Zs Zs^T exactly, the two projectors being
+//   complementary), then T3 on Tm.
+// This is the paper's truncation (reduced SVD + diagonalisation, tol 1e-16 P:L331):
+// every kept and dropped eigenvalue is resolved at the tolerance.
+struct Compression {
+  SmallArgs a;
+  bool fast = false, do_compress = true, t3 = false, refine = false;
+  double tau3 = 0.0;
+  double* Zc = nullptr;
+  int64_t k = 0;
+};
+
+void launch_eig(dme_ctx* c, SmallArgs& a, bool& fast) {
+  fast = a.compress && a.k <= FAST_K_MAX && !c->force_jacobi;
+  ProfScope ps(c, PROF_SMALL);
+  if (fast && a.k >= EIG_SPLIT_MIN) eig_split(a, c->st);
+  else if (fast) eig_fast(a, c->st);
+  else compress_t3(a, c->st);
+}
+
 // Launch the Gram matrix (extended by B when T3 is fused: the B columns are copied next to the
-// factor, so G_ext = [Zc, B]^T [Zc, B] yields G and H = Zc^T B in one pass) and the small kernel.
-// Zc must have KMAX columns of capacity.
+// factor, so G_ext = [Zc, B]^T [Zc, B] yields G and H = Zc^T B in one pass) and the first eigen
+// pass. Zc must have KMAX columns of capacity.
 void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bool do_compress,
-                     SmallArgs& a, bool& fast, cudaEvent_t after_gram = nullptr,
+                     Compression& cp, cudaEvent_t after_gram = nullptr,
                      double* Tm_out = nullptr, bool gram_ready = false) {
   DME_REQUIRE(k <= KMAX && (!t3 || k + c->m <= KMAX), DME_ERR_DIM,
               "factor width exceeds the small-system limit (224)");
   c->stats.compressions += do_compress ? 1 : 0;
-  a = SmallArgs();
+  cp = Compression();
+  cp.Zc = Zc; cp.k = k; cp.t3 = t3; cp.tau3 = tau3; cp.do_compress = do_compress;
+  const double tol = c->opt.trunc_tol * c->tol_scale;
+  cp.refine = do_compress && c->refine && tol < SPLIT_TOL;
+  SmallArgs& a = cp.a;
   if (gram_ready) {  // G (and H = G + k KMAX) assembled by the caller (gram_congruence)
     DME_REQUIRE(do_compress && t3, DME_ERR_CONFIG, "assembled Gram path needs compress + T3");
     a.H = c->G + k * KMAX;
@@ -633,11 +680,9 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
   a.k = (int)k;
   a.compress = do_compress ? 1 : 0;
   a.G = c->G; a.ldg = KMAX;
-  // The Gram matrix resolves eigenvalues of P only down to ~k*eps*theta_max: directions below the
-  // floor are numerically zero for this formulation (reading G7').
-  a.tol = std::max(c->opt.trunc_tol, GRAM_FLOOR);
+  a.tol = cp.refine ? SPLIT_TOL : (c->refine ? tol : std::max(tol, GRAM_FLOOR));
   a.cap = c->rank_cap;
-  a.t3 = t3 ? 1 : 0;
+  a.t3 = (t3 && !cp.refine) ? 1 : 0;
   a.m = (int)c->m;
   a.ldh = KMAX;
   a.LRinv = c->LRinv;
@@ -651,11 +696,7 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
     a.map = c->hmap_dev;
     a.map_seq = ++c->map_seq;
   }
-  fast = do_compress && k <= FAST_K_MAX && !c->force_jacobi;
-  ProfScope ps(c, PROF_SMALL);
-  if (fast && k >= EIG_SPLIT_MIN) eig_split(a, c->st);
-  else if (fast) eig_fast(a, c->st);
-  else compress_t3(a, c->st);
+  launch_eig(c, a, cp.fast);
 }
 
 // Wait until the small kernel launched with sequence number `seq` has published its rank in the
@@ -676,10 +717,11 @@ void wait_published(dme_ctx* c, int seq) {
   std::atomic_thread_fence(std::memory_order_acquire);
 }
 
-// Wait for the small kernel (main stream only), fall back to Jacobi if the fast path refused.
-int64_t compress_finish(dme_ctx* c, const SmallArgs& a, bool fast, bool do_compress) {
+// Wait for an eigen pass (main stream), fall back to Jacobi if the fast path refused; the pass's
+// stats land in c->last_st.
+int64_t eig_finish(dme_ctx* c, const SmallArgs& a, bool fast) {
   int r_host = 0;
-  double st_host[5] = {0, 0, 0, 0, 0};
+  double* st_host = c->last_st;
   auto fetch = [&](const SmallArgs& x) {
     if (x.map) {
       wait_published(c, x.map_seq);
@@ -702,21 +744,71 @@ int64_t compress_finish(dme_ctx* c, const SmallArgs& a, bool fast, bool do_compr
     }
     fetch(b);
   }
-  if (do_compress) c->stats.last_drop = st_host[2];
   return r_host;
+}
+
+// Finish a compression: first pass, then (refined) the tail pass and T3. zc_ready: an event after
+// which Zc is complete (the pipeline writes part of it on the second stream), or null.
+int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = nullptr) {
+  const int64_t kb = eig_finish(c, cp.a, cp.fast);
+  if (!cp.refine) {
+    if (cp.do_compress) c->stats.last_drop = c->last_st[2];
+    return kb;
+  }
+  const double tmax = c->last_st[1];
+  int64_t r = kb;
+  double drop = (kb < cp.k) ? SPLIT_TOL : 0.0;
+  const int64_t k = cp.k;
+  const int cap = cp.a.cap;
+  if (kb < k && tmax > 0.0 && kb < cap) {
+    if (zc_ready) DME_CUDA(cudaStreamWaitEvent(c->st, zc_ready, 0));
+    {
+      ProfScope ps(c, PROF_APPLY);
+      complement_projector(cp.a.Tm, KMAX, (int)k, (int)kb, c->Pp, KMAX, c->st);
+      tall_small(cp.Zc, c->ldn, c->Pp, KMAX, c->Zs, c->ldn, c->n, k, k, c->st);
+    }
+    {
+      ProfScope ps(c, PROF_GRAM);
+      GemmNTArgs g;
+      g.A = c->Zs; g.lda = c->ldn; g.B = c->Zs; g.ldb = c->ldn;
+      g.M = k; g.N = k; g.K = c->n;
+      g.out = c->Gs; g.out_rs = 1; g.out_cs = KMAX;
+      gemm_nt(g, c->gs, c->st);
+    }
+    SmallArgs b = cp.a;
+    b.G = c->Gs;
+    b.t3 = 0;
+    b.tol = c->opt.trunc_tol * c->tol_scale;
+    b.ref_max = tmax;
+    b.cap = cap - (int)kb;
+    b.Tm = cp.a.Tm + kb * KMAX;
+    if (b.map) b.map_seq = ++c->map_seq;
+    bool fast2 = false;
+    launch_eig(c, b, fast2);
+    const int64_t ks = eig_finish(c, b, fast2);
+    r = kb + ks;
+    drop = c->last_st[2];
+  }
+  if (cp.t3 && r > 0) {
+    SmallArgs t = cp.a;
+    t.k = (int)k;
+    ProfScope ps(c, PROF_SMALL);
+    t3_only(t, (int)r, c->st);
+  }
+  c->stats.last_drop = drop;
+  return r;
 }
 
 // Compress the factor Zc (n x k, col-major ldn) into out (n x r); optionally fuse T3(tau3).
 int64_t compress(dme_ctx* c, double* Zc, int64_t k, double* out, bool t3, double tau3,
                  bool do_compress = true) {
   if (k <= 0) return 0;
-  SmallArgs a;
-  bool fast = false;
-  compress_launch(c, Zc, k, t3, tau3, do_compress, a, fast);
-  const int64_t r_host = compress_finish(c, a, fast, do_compress);
+  Compression cp;
+  compress_launch(c, Zc, k, t3, tau3, do_compress, cp);
+  const int64_t r_host = compress_finish(c, cp);
   if (r_host > 0) {
     ProfScope ps(c, PROF_APPLY);
-    tall_small(Zc, c->ldn, c->Tm, KMAX, out, c->ldn, c->n, r_host, k, c->st);
+    tall_small(Zc, c->ldn, cp.a.Tm, KMAX, out, c->ldn, c->n, r_host, k, c->st);
   }
   if (c->profile) drain_profile(c);
   return r_host;
@@ -854,10 +946,9 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
   const bool pipe = c->lookahead && nb > 1 && 2 * q + m + rc <= KMAX &&
                     gram_congruence_smem((int)q, (int)m, (int)(q + rc), rc) <= 220 * 1024;
   int64_t r_prev = c->r;  // columns of Y_t
-  SmallArgs a;
-  bool fast = false;
+  Compression cp;
   // step 0: direct Gram of Zc_0 (main stream), eigen-compression 0
-  compress_launch(c, Zc, q + r_prev, true, h, true, a, fast, c->ev_gram, Tmb[0]);
+  compress_launch(c, Zc, q + r_prev, true, h, true, cp, c->ev_gram, Tmb[0]);
   if (pipe) {  // second stream: E_h Y_0 into GB, Ghat_0
     DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_gram, 0));
     eact_on(c, true, Zc + q * ld, r_prev, c->GB + (2 * q + m) * ld, ld, c->st2, c->gs2);
@@ -868,13 +959,14 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
     gemm_nt(g, c->gs2, c->st2);
     DME_CUDA(cudaEventRecord(c->ev_ghat, c->st2));
   }
-  int64_t rn = compress_finish(c, a, fast, true);
+  int64_t rn = compress_finish(c, cp);
+  DME_CUDA(cudaEventRecord(c->ev_tm, c->st));  // Tm_0 final (after the tail pass and T3)
   for (int64_t it = 0; it < nb; ++it) {
     double* Tm_cur = Tmb[it & 1];
     const int64_t kp = q + r_prev;  // columns of Zc_t = columns of LA_t
     const bool last = it + 1 == nb;
     if (!last && pipe) {
-      // critical path: congruence -> eigen-compression t+1
+      // critical path: congruence -> eigen-compression t+1 (first pass)
       DME_CUDA(cudaStreamWaitEvent(c->st, c->ev_ghat, 0));
       {
         ProfScope ps(c, PROF_GRAM);
@@ -882,14 +974,15 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
                         c->st);
       }
       DME_CUDA(cudaEventRecord(c->ev_cong, c->st));
-      SmallArgs an;
-      bool fastn = false;
-      compress_launch(c, Zc, q + rn, true, h, true, an, fastn, nullptr, Tmb[(it + 1) & 1], true);
+      Compression cn;
+      compress_launch(c, Zc, q + rn, true, h, true, cn, nullptr, Tmb[(it + 1) & 1], true);
       // underneath: Y_{t+1} = LA_t Tm_t, E_h Y_{t+1}, Ghat_{t+1}
+      DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_tm, 0));
       if (rn > 0) {
         ProfScope ps(c, PROF_APPLY, 0, 0, c->st2);
         tall_small(c->GB + (q + m) * ld, ld, Tm_cur, KMAX, Zc + q * ld, ld, n, rn, kp, c->st2);
       }
+      DME_CUDA(cudaEventRecord(c->ev_zc, c->st2));  // Zc_{t+1} = [L_I | Y_{t+1}] complete
       if (it + 2 < nb) {  // Ghat_{t+1} is needed only if step t+2 exists
         eact_on(c, true, Zc + q * ld, rn, c->GB + (2 * q + m) * ld, ld, c->st2, c->gs2);
         DME_CUDA(cudaStreamWaitEvent(c->st2, c->ev_cong, 0));
@@ -901,7 +994,8 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
         DME_CUDA(cudaEventRecord(c->ev_ghat, c->st2));
       }
       r_prev = rn;
-      rn = compress_finish(c, an, fastn, true);
+      rn = compress_finish(c, cn, c->ev_zc);
+      DME_CUDA(cudaEventRecord(c->ev_tm, c->st));
     } else if (!last) {  // no pipeline: Y_{t+1} = E_h (Zc_t Tm_t), direct Gram
       if (rn > 0) {
         ProfScope ps(c, PROF_APPLY);
@@ -909,10 +1003,9 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
       }
       eact(c, true, c->Ztmp, rn, Zc + q * ld, ld);
       r_prev = rn;
-      SmallArgs an;
-      bool fastn = false;
-      compress_launch(c, Zc, q + rn, true, h, true, an, fastn, nullptr, Tmb[(it + 1) & 1]);
-      rn = compress_finish(c, an, fastn, true);
+      Compression cn;
+      compress_launch(c, Zc, q + rn, true, h, true, cn, nullptr, Tmb[(it + 1) & 1]);
+      rn = compress_finish(c, cn);
     } else {  // last step: materialise Z = Zc_t Tm_t (Y_t was written on the second stream)
       if (pipe) {
         DME_CUDA(cudaEventRecord(c->ev_y, c->st2));
@@ -1020,7 +1113,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     DME_CUDA(cudaMemcpyAsync(mflags, c->r_dev, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     sync(c);
     DME_REQUIRE(mflags[0] == 0, DME_ERR_INVALID, "M has non-finite entries");
-    lu_nopiv_solve_right(c->X4, c->Aup, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 2);
+    lu_solve_right(c->X4, c->Aup, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 2);
     double mp = 0;
     DME_CUDA(cudaMemcpyAsync(&mp, c->norm_dev + 2, 8, cudaMemcpyDeviceToHost, st));
     sync(c);
@@ -1029,7 +1122,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
       DME_CUDA(cudaMemcpy2DAsync(c->X4, ld * 8, pr->M, n * 8, n * 8, n, kbig, st));
       DME_CUDA(cudaMemsetAsync(c->X6, 0, (size_t)n * ld * 8, st));
       DME_CUDA(cudaMemcpy2DAsync(c->X6, ld * 8, pr->C, n * 8, n * 8, c->p, cudaMemcpyHostToDevice, st));
-      lu_nopiv_solve_right(c->X4, c->X6, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 2);
+      lu_solve_right(c->X4, c->X6, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 2);
     }
   }
   // device-side validation of the big inputs: finiteness, and the exact symmetry of A that
@@ -1172,19 +1265,30 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     for (int i = 0; i < q; ++i)
       copy_cols(c->Zc12h + (size_t)i * c->p * ld, ld, c->Yn + (size_t)i * c->p * ld, ld, n, c->p,
                 std::sqrt(wn[i] * delta), st);
+    c->tol_scale = LADDER_TOL;
     qI = compress(c, c->Zc12h, (int64_t)q * c->p, c->Ztmp, false, 0.0);
     copy_cols(c->Zc12h, ld, c->Ztmp, ld, n, qI, 1.0, st);
   }
+  // final factors of the ladder: L_I(h) from the fine L_I(h/2), then L_I(h/2) itself at trunc_tol
+  auto finish_ladder = [&](int64_t q_half, const double* Eh) {
+    copy_cols(c->Zc12f, ld, c->Zc12h, ld, n, q_half, 1.0, st);
+    int64_t qf = q_half;
+    c->tol_scale = 1.0;
+    ladder_double(c, c->Zc12f, qf, Eh, Eh ? 0.0 : tau0);
+    c->qf = qf;
+    int64_t qh = q_half;
+    if (qh > 0) {
+      qh = compress(c, c->Zc12h, q_half, c->Ztmp, false, 0.0);
+      copy_cols(c->Zc12h, ld, c->Ztmp, ld, n, qh, 1.0, st);
+    }
+    c->qh = qh;
+  };
 
   if (c->sparse || c->cheb_e) {
     // ---------------------------------------------------------------- ladder by sparse actions
     int64_t q_cur = qI;
     for (int j = 0; j < s_total; ++j) ladder_double(c, c->Zc12h, q_cur, nullptr, std::ldexp(delta, j));
-    c->qh = q_cur;
-    copy_cols(c->Zc12f, ld, c->Zc12h, ld, n, c->qh, 1.0, st);
-    int64_t qf = c->qh;
-    ladder_double(c, c->Zc12f, qf, nullptr, tau0);
-    c->qf = qf;
+    finish_ladder(q_cur, nullptr);
     if (c->cheb_e) {
       // E_{h/2} = exp((h/2) A^T) I (columns = rows: A symmetric), exactly symmetrised; E_h = E_{h/2}^2
       lincomb(c->T1, n, ld, {}, {}, {}, {}, 1.0, st);
@@ -1213,14 +1317,16 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   lincomb(c->V, n, ld, {1.0, c->V}, {b[6], c->X6}, {b[4], c->X4}, {b[2], c->X2}, b[0], st);
   lincomb(c->X4, n, ld, {1.0, c->V}, {-1.0, c->U}, {}, {}, 0.0, st);  // Q = V - U
   lincomb(c->X6, n, ld, {1.0, c->V}, {1.0, c->U}, {}, {}, 0.0, st);   // P = V + U
-  lu_nopiv_solve_right(c->X4, c->X6, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 1);
+  lu_solve_right(c->X4, c->X6, n, ld, c->BT, c->lu_scr, c->gs, st, c->norm_dev + 1);
   if (c->symA) mirror_lower(c->X6, n, ld, true, st);  // exact symmetry of E_delta
   double minpiv = 0;
   DME_CUDA(cudaMemcpyAsync(&minpiv, c->norm_dev + 1, 8, cudaMemcpyDeviceToHost, st));
   sync(c);
   c->stats.pade_min_pivot = minpiv;
-  DME_REQUIRE(std::isfinite(minpiv) && minpiv > 1e-8 * b[0], DME_ERR_NUMERIC,
-              "Padé denominator factorisation hit a tiny pivot");
+  // partial pivoting: a pivot 13 orders below the scale b_0 of q13(X) would mean kappa(q13) >~ 1e13,
+  // which Higham's bound on ||X||_1 <= theta_13 excludes; only a corrupted input gets here
+  DME_REQUIRE(std::isfinite(minpiv) && minpiv > 1e-13 * b[0], DME_ERR_NUMERIC,
+              "Padé denominator is numerically singular");
 
   // ---------------------------------------------------------------- squaring ladder + quadrature
   double* Ecur = c->X6;
@@ -1236,12 +1342,8 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     Ecur = En;
   }
   DME_CUDA(cudaMemcpyAsync(c->E_half, Ecur, (size_t)n * ld * 8, cudaMemcpyDeviceToDevice, st));
-  c->qh = q_cur;
   // L_I(h) = compress([L_I(h/2), E_{h/2} L_I(h/2)]),  E_h = E_{h/2}^2
-  copy_cols(c->Zc12f, ld, c->Zc12h, ld, n, c->qh, 1.0, st);
-  int64_t qf = c->qh;
-  ladder_double(c, c->Zc12f, qf, c->E_half, 0.0);
-  c->qf = qf;
+  finish_ladder(q_cur, c->E_half);
   matmul_sq(c, c->E_half, c->E_half, c->E_full);
   if (c->oz) {  // digit slices of the local rows of E_{h/2} and E_h (after the last product)
     oz_slice_rows_tiled(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->exEh, c->ozpm, st);
@@ -1339,7 +1441,7 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     DME_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hmap_dev), c->hmap, 0));
     DME_CUDA(cudaEventCreateWithFlags(&c->ev_gram, cudaEventDisableTiming));
     DME_CUDA(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming));
-    for (cudaEvent_t* e : {&c->ev_ghat, &c->ev_cong, &c->ev_y})
+    for (cudaEvent_t* e : {&c->ev_ghat, &c->ev_cong, &c->ev_y, &c->ev_zc, &c->ev_tm})
       DME_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     Planner sizing;
     plan_buffers(c, sizing);
@@ -1696,6 +1798,25 @@ dme_status dme_debug_set_factor(dme_ctx* c, int64_t r, const double* L) {
       rowmajor_to_colmajor(c->Z, c->ldn, c->Ztmp, r, c->n, r, c->st);
     }
     c->r = r;
+    sync(c);
+  });
+}
+
+dme_status dme_debug_set_exp(dme_ctx* c, int32_t which, const double* E) {
+  if (!c || !E) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
+  return guarded(c, [&] {
+    DME_REQUIRE(!c->sparse, DME_ERR_CONFIG, "no dense E with a sparse A");
+    DME_REQUIRE(which == 0 || which == 1, DME_ERR_INVALID, "which must be 0 (E_{h/2}) or 1 (E_h)");
+    double* dst = which ? c->E_full : c->E_half;
+    DME_CUDA(cudaMemcpy2DAsync(dst, c->ldn * 8, E, c->n * 8, c->n * 8, c->n,
+                               cudaMemcpyHostToDevice, c->st));
+    if (c->oz && c->oz_ready)  // the int8 E pass reads the digit image: re-slice the local rows
+      oz_slice_rows_tiled(dst + c->row0 * c->ldn, c->ldn, c->rows_loc, c->n, which ? c->ozEf : c->ozEh,
+                          which ? c->exEf : c->exEh, c->ozpm, c->st);
+    if (which == 1 && c->qf > 0)  // the look-ahead operand E_h L_I(h) of the pipelined body
+      eact(c, true, c->Zc12f, c->qf, c->LA, c->ldn);
+    if (which == 1 && c->m > 0 && 2 * c->qf + c->m <= KMAX)
+      copy_cols(c->GB + (c->qf + c->m) * c->ldn, c->ldn, c->LA, c->ldn, c->n, c->qf, 1.0, c->st);
     sync(c);
   });
 }

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
       }
       __syncthreads();
     }
-    if (tid == 0) s_tmax = 0.5 * (s_lo_t + s_hi_t);
+    if (tid == 0) s_tmax = a.ref_max > 0.0 ? a.ref_max / s_scale : 0.5 * (s_lo_t + s_hi_t);
     __syncthreads();
   }
   t_ph[2] = clock64();

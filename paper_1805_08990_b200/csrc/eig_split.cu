@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
     __syncthreads();
   }
   if (tid == 0) {
-    const double tmax = 0.5 * (s_lo_t + s_hi_t);
+    double tmax = 0.5 * (s_lo_t + s_hi_t);
+    if (a.ref_max > 0.0) tmax = a.ref_max / s_scale;  // threshold and stats against the reference
     int r = 0;
     if (tmax > 0.0) r = k - sturm_count(d, e2, k, a.tol * tmax);
     if (r > a.cap) r = a.cap;

@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(NT, 1) compress_t3_kernel(SmallArgs a) {
     if (tid == 0) {
       double tmax = -1e300;
       for (int i = 0; i < k; ++i) tmax = fmax(tmax, theta[i]);
+      if (a.ref_max > 0.0) tmax = a.ref_max;
       int cnt = 0;
       for (int i = 0; i < k; ++i) cnt += (tmax > 0.0 && theta[i] > a.tol * tmax);
       s_r = cnt < a.cap ? cnt : a.cap;
@@ -200,7 +201,40 @@ __global__ void __launch_bounds__(NT, 1) compress_t3_kernel(SmallArgs a) {
   if (tid == 0) publish_rank(a, r);
 }
 
+// Riccati flow T3 alone on a finished compression output Tm (k x r) (after the tail refinement of
+// dme.cu, which assembles Tm from two eigen passes before T3 can be applied)
+__global__ void __launch_bounds__(NT) t3_only_kernel(SmallArgs a, int r) {
+  extern __shared__ double S[];
+  __shared__ double Gam[SMALL_M_MAX * SMALL_M_MAX];
+  __shared__ double Phi[SMALL_M_MAX * SMALL_M_MAX];
+  if (r > 0) t3_fuse(a, a.k, r, S, Gam, Phi);
+}
+
+// Pp (k x k, column-major ldp) = I - W W^T, W = the kb leading columns of Tm (k x kb, ldt):
+// the projector onto the orthogonal complement of the kept leading eigenvectors
+__global__ void complement_kernel(const double* __restrict__ W, int64_t ldw, int k, int kb,
+                                  double* __restrict__ Pp, int64_t ldp) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+    const int i = e % k, j = e / k;
+    double s = 0.0;
+    for (int c = 0; c < kb; ++c) s = fma(W[i + (size_t)c * ldw], W[j + (size_t)c * ldw], s);
+    Pp[i + (size_t)j * ldp] = (i == j ? 1.0 : 0.0) - s;
+  }
+}
+
 }  // namespace
+
+void t3_only(const SmallArgs& a, int r, cudaStream_t st) {
+  if (a.m > SMALL_M_MAX) throw std::runtime_error("t3_only: m exceeds SMALL_M_MAX");
+  t3_only_kernel<<<1, NT, sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX, st>>>(a, r);
+  DME_KCHECK();
+}
+
+void complement_projector(const double* W, int64_t ldw, int k, int kb, double* Pp, int64_t ldp,
+                          cudaStream_t st) {
+  complement_kernel<<<(k * k + 255) / 256, 256, 0, st>>>(W, ldw, k, kb, Pp, ldp);
+  DME_KCHECK();
+}
 
 void compress_t3(const SmallArgs& a, cudaStream_t st) {
   if (a.k > SMALL_K_MAX) throw std::runtime_error("compress_t3: k exceeds SMALL_K_MAX");

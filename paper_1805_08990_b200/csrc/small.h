@@ -25,6 +25,9 @@ struct SmallArgs {
   const double* G = nullptr; // k x k Gram matrix Zc^T Zc, column-major, leading dim ldg
   int64_t ldg = 0;
   double tol = 1e-16;        // relative truncation tolerance (reading G7)
+  double ref_max = 0.0;      // > 0: keep theta > tol * ref_max (the theta_max of an enclosing
+                             // compression: the refinement pass of the tail, dme.cu) instead of
+                             // tol * (this matrix's theta_max); stats[1], stats[2] refer to it
   int cap = 1 << 30;         // rank cap (reading G8)
   int t3 = 0;                // 1: fuse the Riccati flow T3(tau)
   int m = 0;                 // columns of B
@@ -50,5 +53,9 @@ void compress_t3(const SmallArgs& a, cudaStream_t st);  // Jacobi (any k <= SMAL
 void eig_fast(const SmallArgs& a, cudaStream_t st);     // k <= FAST_K_MAX; *r_out = -1 => fall back
 void eig_split(const SmallArgs& a, cudaStream_t st);    // 3 <= k <= FAST_K_MAX, same contract
 size_t eig_split_scratch_doubles();
+void t3_only(const SmallArgs& a, int r, cudaStream_t st);  // T3 on Tm (k x r) alone
+// Pp = I - W W^T (k x k), W: k x kb (the kept leading eigenvectors of the first pass)
+void complement_projector(const double* W, int64_t ldw, int k, int kb, double* Pp, int64_t ldp,
+                          cudaStream_t st);
 
 }  // namespace dme
