@@ -59,6 +59,7 @@ constexpr double SPLIT_TOL = 1e-11;     // refined compression: first pass keeps
 // rung, so the rungs below the final L_I(h/2), L_I(h) keep 64x finer directions and only the final
 // factors are truncated at trunc_tol (their ranks then match a one-shot truncation)
 constexpr double LADDER_TOL = 1.0 / 64;
+constexpr int LOOKAHEAD_RESERVE = EIG_SPLIT_CTAS;  // SMs the look-ahead stream leaves free
 
 // Gauss-Legendre nodes/weights on [0,1] by Newton on P_q (Golub-Welsch-free; own implementation)
 void gauss_legendre01(int q, std::vector<double>& c, std::vector<double>& w) {
@@ -117,7 +118,7 @@ struct dme_ctx {
   double *Zc12h = nullptr, *Zc12f = nullptr, *Zc2 = nullptr, *Z = nullptr, *Ztmp = nullptr;
   double *G = nullptr, *H = nullptr, *Tm = nullptr, *Vg = nullptr, *Es = nullptr, *LRinv = nullptr, *sstats = nullptr;
   double *norm_dev = nullptr, *red_scratch = nullptr, *stage = nullptr;
-  double *Zs = nullptr, *Gs = nullptr, *Pp = nullptr;  // refined compression: Zc (I - W W^T), its Gram, I - W W^T
+  double *Zs = nullptr, *Gs = nullptr, *Us = nullptr, *Ts = nullptr;  // refined compression: Zc U, its Gram, U, tail eigenvectors
   bool refine = true;      // options.compression == DME_COMPRESS_REFINED
   double tol_scale = 1.0;  // intermediate quadrature-ladder compressions run at trunc_tol * LADDER_TOL
   double last_st[5] = {0, 0, 0, 0, 0};  // stats of the last small-kernel pass read by the host
@@ -237,7 +238,8 @@ void plan_buffers(dme_ctx* c, Planner& P) {
   c->LA = P.take<double>(fk);
   c->Zs = P.take<double>(fk);
   c->Gs = P.take<double>((size_t)KMAX * KMAX);
-  c->Pp = P.take<double>((size_t)KMAX * KMAX);
+  c->Us = P.take<double>((size_t)KMAX * KMAX);
+  c->Ts = P.take<double>((size_t)KMAX * KMAX);
   c->GB = P.take<double>(fk);
   c->Ghat = P.take<double>((size_t)KMAX * KMAX);
   c->Tm2 = P.take<double>((size_t)KMAX * KMAX);
@@ -649,7 +651,9 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
   cp = Compression();
   cp.Zc = Zc; cp.k = k; cp.t3 = t3; cp.tau3 = tau3; cp.do_compress = do_compress;
   const double tol = c->opt.trunc_tol * c->tol_scale;
-  cp.refine = do_compress && c->refine && tol < SPLIT_TOL;
+  // (the tail pass needs the complement basis in one CTA's shared memory: k <= FAST_K_MAX; wider
+  // concatenations -- T4 at rank > 53, ladder rungs at q > 80 -- use the single Gram pass)
+  cp.refine = do_compress && c->refine && tol < SPLIT_TOL && k <= FAST_K_MAX;
   SmallArgs& a = cp.a;
   if (gram_ready) {  // G (and H = G + k KMAX) assembled by the caller (gram_congruence)
     DME_REQUIRE(do_compress && t3, DME_ERR_CONFIG, "assembled Gram path needs compress + T3");
@@ -760,40 +764,48 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
   double drop = (kb < cp.k) ? SPLIT_TOL : 0.0;
   const int64_t k = cp.k;
   const int cap = cp.a.cap;
+  int64_t ks = 0, s = 0;
   if (kb < k && tmax > 0.0 && kb < cap) {
+    // U (k x s): orthonormal basis of the complement of span(W_b); Zs = Zc U (n x s), Gs = Zs^T Zs
+    s = k - kb;
+    {
+      ProfScope ps(c, PROF_SMALL);
+      complement_basis(cp.a.Tm, KMAX, (int)k, (int)kb, c->Us, KMAX, c->st);
+    }
     if (zc_ready) DME_CUDA(cudaStreamWaitEvent(c->st, zc_ready, 0));
     {
       ProfScope ps(c, PROF_APPLY);
-      complement_projector(cp.a.Tm, KMAX, (int)k, (int)kb, c->Pp, KMAX, c->st);
-      tall_small(cp.Zc, c->ldn, c->Pp, KMAX, c->Zs, c->ldn, c->n, k, k, c->st);
+      tall_small(cp.Zc, c->ldn, c->Us, KMAX, c->Zs, c->ldn, c->n, s, k, c->st);
     }
     {
       ProfScope ps(c, PROF_GRAM);
       GemmNTArgs g;
       g.A = c->Zs; g.lda = c->ldn; g.B = c->Zs; g.ldb = c->ldn;
-      g.M = k; g.N = k; g.K = c->n;
+      g.M = s; g.N = s; g.K = c->n;
       g.out = c->Gs; g.out_rs = 1; g.out_cs = KMAX;
       gemm_nt(g, c->gs, c->st);
     }
     SmallArgs b = cp.a;
+    b.k = (int)s;
     b.G = c->Gs;
     b.t3 = 0;
     b.tol = c->opt.trunc_tol * c->tol_scale;
     b.ref_max = tmax;
     b.cap = cap - (int)kb;
-    b.Tm = cp.a.Tm + kb * KMAX;
+    b.Tm = c->Ts;
     if (b.map) b.map_seq = ++c->map_seq;
     bool fast2 = false;
     launch_eig(c, b, fast2);
-    const int64_t ks = eig_finish(c, b, fast2);
+    ks = eig_finish(c, b, fast2);
     r = kb + ks;
     drop = c->last_st[2];
   }
-  if (cp.t3 && r > 0) {
+  if (ks > 0 || (cp.t3 && r > 0)) {  // Tm[:, kb:r] = U V_s, then T3 on Tm
     SmallArgs t = cp.a;
     t.k = (int)k;
+    t.t3 = cp.t3 ? 1 : 0;
     ProfScope ps(c, PROF_SMALL);
-    t3_only(t, (int)r, c->st);
+    tail_assemble_t3(t, c->Us, KMAX, (int)s, c->Ts, KMAX, (int)kb, (int)ks, c->st);
   }
   c->stats.last_drop = drop;
   return r;
@@ -1450,9 +1462,14 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     Planner P;
     P.base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(o->workspace) + 255) & ~uintptr_t(255));
     plan_buffers(c, P);
-    c->gs2.max_grid = std::max(1, num_sms() - EIG_SPLIT_CTAS);  // SMs left to the eigen kernels
+    // the look-ahead stream (E pass, Gram) leaves SMs to the critical path: the eigen kernels and the
+    // n-row kernels of the refined compression (DME_LOOKAHEAD_SMS overrides, for measurements)
+    int la = num_sms() - LOOKAHEAD_RESERVE;
+    if (const char* e = std::getenv("DME_LOOKAHEAD_SMS")) la = std::atoi(e);
+    la = std::max(1, std::min(la, num_sms()));
+    c->gs2.max_grid = la;
     c->ozs.max_grid = std::min(256, num_sms());
-    c->ozs2.max_grid = std::max(1, num_sms() - EIG_SPLIT_CTAS);
+    c->ozs2.max_grid = la;
     if (c->world > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, o->nccl_uid, sizeof(uid));

@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   const int r = s_r;
   const int nr = r < k ? r + 1 : r;  // + the first dropped one, for the stats
   {
-    int P = nr > 0 ? 200 / nr : 1;
-    P = P < 1 ? 1 : (P > 16 ? 16 : P);
+    int P = nr > 0 ? ENT / nr : 1;
+    P = P < 1 ? 1 : (P > 64 ? 64 : P);
     const int grp = tid / P, t = tid % P;
     const bool act = grp < nr;
     const int jj = k - 1 - grp;
@@ -124,15 +124,15 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
         cnt_s[tid] = sturm_count(d, e2, k, a0 + (b0 - a0) * (t + 1) / (P + 1.0));
       }
       __syncthreads();
-      if (act && t == 0) {
+      if (act) {  // transition between probe t and t+1 (counts are monotone in the probe position)
         const double a0 = lo_s[grp], b0 = hi_s[grp];
-        double na = a0, nb = b0;
-        for (int q = 0; q < P; ++q) {
-          const double xq = a0 + (b0 - a0) * (q + 1) / (P + 1.0);
-          if (cnt_s[grp * P + q] <= jj) na = xq; else { nb = xq; break; }
+        const bool le = cnt_s[tid] <= jj;
+        const bool nxt = (t + 1 < P) ? (cnt_s[tid + 1] <= jj) : false;
+        if (le && !nxt) {
+          lo_s[grp] = a0 + (b0 - a0) * (t + 1) / (P + 1.0);
+          if (t + 1 < P) hi_s[grp] = a0 + (b0 - a0) * (t + 2) / (P + 1.0);
         }
-        lo_s[grp] = na;
-        hi_s[grp] = nb;
+        if (t == 0 && !le) hi_s[grp] = a0 + (b0 - a0) / (P + 1.0);
       }
       __syncthreads();
     }

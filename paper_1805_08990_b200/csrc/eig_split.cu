@@ -185,8 +185,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   // ------------------------------------------------------------ multisection on this slice
   t_ph[1] = clock64();
   {
+    // one Sturm count per thread and round: with few eigenvalues per CTA (the tail pass of the
+    // refined compression) up to 64 probes per eigenvalue cut the rounds from ~11 to ~7
     int P = ENT / nb;
-    P = P < 1 ? 1 : (P > 16 ? 16 : P);  // more probes: more busy warps, no fewer cycles (measured)
+    P = P < 1 ? 1 : (P > 64 ? 64 : P);
     const int grp = tid / P, t = tid % P;
     const bool act = grp < nb;
     const int jj = k - 1 - (c0 + grp);  // ascending index
@@ -571,7 +573,11 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     int mx = (int)(need_max > floor_b ? need_max : floor_b);
-    if (FK <= 96) mx += (int)(sizeof(double) * 2 * ((FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1) * FK);
+    if (FK <= 96) {  // the VEC (twisted-factorisation arrays) and FIN (W, U, F) extras at k = FK
+      const int vec_x = (int)(sizeof(double) * 2 * ((FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1) * FK);
+      const int fin_x = (int)(sizeof(double) * 3 * (size_t)FK * SMALL_M_MAX);
+      mx += vec_x > fin_x ? vec_x : fin_x;
+    }
     DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_vec_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_fin_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));

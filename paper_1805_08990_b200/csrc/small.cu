@@ -222,7 +222,226 @@ __global__ void complement_kernel(const double* __restrict__ W, int64_t ldw, int
   }
 }
 
+// Orthonormal basis U (k x s, column-major ldu) of the complement of span(W), W = the kb leading
+// columns of Tm (k x kb, orthonormal), s = k - kb: Householder QR of W, H_0 ... H_{kb-1} W = [R; 0],
+// then U = H_0 ... H_{kb-1} [0; I_s] (the trailing columns of the orthogonal factor).
+// One CTA of 32 warps; column c of W lives in the registers of warp c mod 32 (RPL rows per lane),
+// so a QR step is: one CTA barrier (reflector j published in shared memory), each warp's dots and
+// updates of its own columns, and the owner of column j+1 forming reflector j+1 right after its own
+// update. The second phase needs no barrier at all: each warp applies the kb stored reflectors to its
+// own columns of [0; I_s].
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int RPL, int CPW>
+__global__ void __launch_bounds__(NT) complement_basis_kernel(const double* __restrict__ W, int64_t ldw,
+                                                              int k, int kb, double* __restrict__ U,
+                                                              int64_t ldu) {
+  extern __shared__ double Vh[];  // reflectors: row j = v_j (k entries, ld k | 1)
+  __shared__ double tau_s[FAST_K_MAX];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ld = k | 1, s = k - kb;
+  double x[CPW][RPL];
+#pragma unroll
+  for (int q = 0; q < CPW; ++q)
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int c = warp + 32 * q, i = lane + 32 * u;
+      x[q][u] = (c < kb && i < k) ? W[i + (size_t)c * ldw] : 0.0;
+    }
+  // reflector j from this warp's column slot q (rows >= j)
+  auto reflector = [&](int j, int q) {
+    double xs[RPL];
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      double v = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < CPW; ++qq) v = (qq == q) ? x[qq][u] : v;
+      xs[u] = v;
+    }
+    double n2 = 0.0, xa = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int i = lane + 32 * u;
+      if (i > j && i < k) n2 = fma(xs[u], xs[u], n2);
+      if (i == j) xa = xs[u];
+    }
+    n2 = warp_sum(n2);
+    const double alpha = __shfl_sync(0xffffffffu, xa, j & 31);
+    double t = 0.0, scal = 0.0;
+    if (n2 > 0.0) {
+      const double beta = -copysign(sqrt(fma(alpha, alpha, n2)), alpha);
+      scal = 1.0 / (alpha - beta);
+      t = (beta - alpha) / beta;
+    }
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int i = lane + 32 * u;
+      if (i < k) Vh[j * ld + i] = (i < j || t == 0.0) ? 0.0 : (i == j ? 1.0 : xs[u] * scal);
+    }
+    if (lane == 0) tau_s[j] = t;
+  };
+  auto apply = [&](int j, int q) {  // column slot q <- H_j column
+    const double t = tau_s[j];
+    if (t == 0.0) return;
+    double vv[RPL], d = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int i = lane + 32 * u;
+      vv[u] = i < k ? Vh[j * ld + i] : 0.0;
+      double xv = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < CPW; ++qq) xv = (qq == q) ? x[qq][u] : xv;
+      d = fma(vv[u], xv, d);
+    }
+    d = t * warp_sum(d);
+#pragma unroll
+    for (int qq = 0; qq < CPW; ++qq)
+      if (qq == q)
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) x[qq][u] = fma(-d, vv[u], x[qq][u]);
+  };
+  if (warp == 0 && kb > 0) reflector(0, 0);
+  for (int j = 0; j < kb; ++j) {
+    __syncthreads();  // reflector j published
+    const int nxt = j + 1;
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      const int c = warp + 32 * q;
+      if (c > j && c < kb) {
+        apply(j, q);
+        if (c == nxt) reflector(nxt, q);  // look-ahead: owner of column j+1
+      }
+    }
+  }
+  __syncthreads();
+  // U = H_0 ... H_{kb-1} [0; I_s]: column t of U starts as e_{kb + t}
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int t = warp + 32 * q;
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) x[q][u] = (lane + 32 * u == kb + t) ? 1.0 : 0.0;
+  }
+  for (int j = kb - 1; j >= 0; --j)
+#pragma unroll
+    for (int q = 0; q < CPW; ++q)
+      if (warp + 32 * q < s) apply(j, q);
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int t = warp + 32 * q;
+    if (t < s)
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int i = lane + 32 * u;
+        if (i < k) U[i + (size_t)t * ldu] = x[q][u];
+      }
+  }
+}
+
+__global__ void tail_product_kernel(double* Tm, int64_t ldt, const double* __restrict__ U, int64_t ldu,
+                                    int s, const double* __restrict__ V, int64_t ldv, int k, int kb, int ks) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * ks) return;
+  const int i = e % k, c = e / k;
+  double acc = 0.0;
+  for (int j = 0; j < s; ++j) acc = fma(U[i + (size_t)j * ldu], V[j + (size_t)c * ldv], acc);
+  Tm[i + (size_t)(kb + c) * ldt] = acc;
+}
+
+// Tail of the refined compression: Tm[:, kb + c] = U V[:, c] (c < ks; U: k x s, V: s x ks), then
+// the Riccati flow T3 on the whole Tm (k x (kb + ks)) when a.t3 is set.
+__global__ void __launch_bounds__(NT) tail_assemble_kernel(SmallArgs a, const double* __restrict__ U,
+                                                           int64_t ldu, int s, const double* __restrict__ V,
+                                                           int64_t ldv, int kb, int ks) {
+  extern __shared__ double S[];
+  __shared__ double Gam[SMALL_M_MAX * SMALL_M_MAX];
+  __shared__ double Phi[SMALL_M_MAX * SMALL_M_MAX];
+  const int k = a.k, r = kb + ks, m = a.m, tid = threadIdx.x;
+  // shared layout: Tm (k x r, ld k) | H (k x m) | U (k x s) | V (s x ks) ; t3 scratch reuses U/V
+  double* Ts = S;
+  double* Hs = Ts + (size_t)k * r;
+  double* Us = Hs + (size_t)k * m;
+  double* Vs = Us + (size_t)k * s;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NWP = NT / 32;
+  for (int c = warp; c < kb; c += NWP)
+    for (int i = lane; i < k; i += 32) Ts[i + c * k] = a.Tm[i + (size_t)c * a.ldt];
+  for (int c = warp; c < m; c += NWP)
+    for (int i = lane; i < k; i += 32) Hs[i + c * k] = a.H[i + (size_t)c * a.ldh];
+  for (int c = warp; c < s; c += NWP)
+    for (int i = lane; i < k; i += 32) Us[i + c * k] = U[i + (size_t)c * ldu];
+  for (int c = warp; c < ks; c += NWP)
+    for (int i = lane; i < s; i += 32) Vs[i + c * s] = V[i + (size_t)c * ldv];
+  __syncthreads();
+  for (int c = warp; c < ks; c += NWP)
+    for (int i = lane; i < k; i += 32) {
+      double acc = 0.0;
+      for (int j = 0; j < s; ++j) acc = fma(Us[i + j * k], Vs[j + c * s], acc);
+      Ts[i + (kb + c) * k] = acc;
+    }
+  __syncthreads();
+  if (a.t3 && r > 0) {
+    SmallArgs b = a;
+    b.Tm = Ts; b.ldt = k;
+    b.H = Hs; b.ldh = k;
+    t3_fuse(b, k, r, Us, Gam, Phi);  // (U, V are free now: >= 2 SMALL_K_MAX SMALL_M_MAX doubles)
+    __syncthreads();
+  }
+  for (int c = warp; c < r; c += NWP)
+    for (int i = lane; i < k; i += 32) a.Tm[i + (size_t)c * a.ldt] = Ts[i + c * k];
+}
+
 }  // namespace
+
+void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, int64_t ldu,
+                      cudaStream_t st) {
+  if (k > FAST_K_MAX || kb > k || kb < 0) throw std::runtime_error("complement_basis: bad size");
+  static int attr_dev = -1;
+  int dev = 0;
+  DME_CUDA(cudaGetDevice(&dev));
+  const int mx = (int)(sizeof(double) * FAST_K_MAX * (FAST_K_MAX | 1));
+  if (attr_dev != dev) {
+    DME_CUDA(cudaFuncSetAttribute(complement_basis_kernel<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DME_CUDA(cudaFuncSetAttribute(complement_basis_kernel<5, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    attr_dev = dev;
+  }
+  const size_t smem = sizeof(double) * (size_t)(kb > 0 ? kb : 1) * (k | 1);
+  if (k <= 96) complement_basis_kernel<3, 3><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
+  else complement_basis_kernel<5, 5><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
+  DME_KCHECK();
+}
+
+void t3_only(const SmallArgs& a, int r, cudaStream_t st);
+
+void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, const double* V,
+                      int64_t ldv, int kb, int ks, cudaStream_t st) {
+  if (a.m > SMALL_M_MAX) throw std::runtime_error("tail_assemble_t3: m exceeds SMALL_M_MAX");
+  const int k = a.k, r = kb + ks;
+  size_t need = sizeof(double) * ((size_t)k * r + (size_t)k * a.m + (size_t)k * s + (size_t)s * ks);
+  const size_t t3s = sizeof(double) * ((size_t)k * r + (size_t)k * a.m + 2 * SMALL_K_MAX * SMALL_M_MAX);
+  if (need < t3s) need = t3s;
+  if (need > (size_t)SMALL_SMEM_MAX) {  // wide systems: the product in global memory, then T3 alone
+    if (ks > 0) {
+      tail_product_kernel<<<(k * ks + 255) / 256, 256, 0, st>>>(a.Tm, a.ldt, U, ldu, s, V, ldv, k, kb, ks);
+      DME_KCHECK();
+    }
+    if (a.t3 && r > 0) t3_only(a, r, st);
+    return;
+  }
+  static int attr_dev = -1;
+  int dev = 0;
+  DME_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    DME_CUDA(cudaFuncSetAttribute(tail_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SMALL_SMEM_MAX));
+    attr_dev = dev;
+  }
+  tail_assemble_kernel<<<1, NT, need, st>>>(a, U, ldu, s, V, ldv, kb, ks);
+  DME_KCHECK();
+}
 
 void t3_only(const SmallArgs& a, int r, cudaStream_t st) {
   if (a.m > SMALL_M_MAX) throw std::runtime_error("t3_only: m exceeds SMALL_M_MAX");

@@ -8,7 +8,7 @@ constexpr int SMALL_K_MAX = 224;          // packed k(k+1)/2 doubles fit in 201 
 constexpr int SMALL_M_MAX = 8;
 constexpr int FAST_K_MAX = 160;           // fast tridiagonal eigen-compression: k x (k|1) in smem
 constexpr int EIG_SPLIT_MIN = 48;         // k from which the eigen-compression runs as TRI/VEC/FIN
-constexpr int EIG_SPLIT_CTAS = 8;         // CTAs of the VEC kernel (the look-ahead E pass leaves them)            // columns of B handled by the fused Riccati flow
+constexpr int EIG_SPLIT_CTAS = 32;        // CTAs of the VEC kernel (the look-ahead E pass leaves them)            // columns of B handled by the fused Riccati flow
 constexpr int SMALL_SMEM_MAX = SMALL_K_MAX * (SMALL_K_MAX + 1) / 2 * 8;
 
 // Host-mapped (pinned, zero-copy) record through which the small kernels publish the new rank:
@@ -54,6 +54,12 @@ void eig_fast(const SmallArgs& a, cudaStream_t st);     // k <= FAST_K_MAX; *r_o
 void eig_split(const SmallArgs& a, cudaStream_t st);    // 3 <= k <= FAST_K_MAX, same contract
 size_t eig_split_scratch_doubles();
 void t3_only(const SmallArgs& a, int r, cudaStream_t st);  // T3 on Tm (k x r) alone
+// U (k x (k - kb), ldu): orthonormal basis of the complement of span(W), W = k x kb orthonormal
+void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, int64_t ldu,
+                      cudaStream_t st);
+// a.Tm[:, kb:kb+ks] = U V (U: k x s, V: s x ks), then T3 on a.Tm (k x (kb + ks)) if a.t3
+void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, const double* V,
+                      int64_t ldv, int kb, int ks, cudaStream_t st);
 // Pp = I - W W^T (k x k), W: k x kb (the kept leading eigenvectors of the first pass)
 void complement_projector(const double* W, int64_t ldw, int k, int kb, double* Pp, int64_t ldp,
                           cudaStream_t st);
