@@ -383,12 +383,12 @@ void gram_congruence(const double* Gh, int64_t ldh, int q, int m, int kp, const 
   if (q + r <= 0) return;
   const int ctas = std::max(1, std::min(CONG_CTAS, r));
   const size_t smem = gram_congruence_smem(q, m, kp, r);
-  static bool attr = false;
-  if (!attr) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(gram_congruence_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   220 * 1024));
-    attr = true;
-  }
+  });
   if (smem > 220 * 1024) throw std::runtime_error("gram_congruence: too large");
   gram_congruence_kernel<<<ctas, 512, smem, st>>>(Gh, ldh, q, m, kp, Tm, ldt, r, G, ldg);
   DME_KCHECK();
@@ -552,12 +552,12 @@ void signed_core(const double* Tm, int64_t ldt, int k, int r1, int kf, double wf
   if (r1 > SC_MAX) throw std::runtime_error("signed_core: rank of the combined factor exceeds 112");
   const int n2 = (r1 + 1) & ~1;
   const size_t smem = sizeof(double) * 2 * (size_t)n2 * n2;
-  static bool attr = false;
-  if (!attr) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(signed_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double) * 2 * (SC_MAX + 1) * (SC_MAX + 1))));
-    attr = true;
-  }
+  });
   signed_core_kernel<<<1, 512, smem, st>>>(Tm, ldt, k, r1, kf, wf, wc, tol, T2, ldt2, lam, r2_dev,
                                             raw ? 1 : 0);
   DME_KCHECK();

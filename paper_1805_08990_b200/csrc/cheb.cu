@@ -324,11 +324,11 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
 template <int C, int W>
 void launch_reg(const ChebParams& prm, int groups, size_t smem, int threads, cudaStream_t st) {
   auto kern = cheb_reg_kernel<C, W>;
-  static bool attr = false;
-  if (!attr) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
-    attr = true;
-  }
+  });
   kern<<<groups * CHEB_CLUSTER, threads, smem, st>>>(prm);
   DME_KCHECK();
 }
@@ -347,11 +347,11 @@ constexpr int CHEB_REG_CMAX = 5;
 template <int C, int W>
 void launch_cw(const ChebParams& prm, int groups, size_t smem, cudaStream_t st) {
   auto kern = cheb_kernel<C, W>;
-  static bool attr = false;
-  if (!attr) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
-    attr = true;
-  }
+  });
   kern<<<groups * CHEB_CLUSTER, CHEB_THREADS, smem, st>>>(prm);
   DME_KCHECK();
 }
@@ -631,11 +631,12 @@ void preload_c() {
       DME_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
 }
 void preload_all() {
-  static bool done = false;
-  if (done) return;
-  preload_c<1>(); preload_c<2>(); preload_c<3>(); preload_c<4>();
-  preload_c<5>(); preload_c<6>(); preload_c<7>(); preload_c<8>();
-  done = true;
+  static std::mutex mu;
+  static uint64_t mask = 0;
+  per_device_once(mu, mask, [] {
+    preload_c<1>(); preload_c<2>(); preload_c<3>(); preload_c<4>();
+    preload_c<5>(); preload_c<6>(); preload_c<7>(); preload_c<8>();
+  });
 }
 }  // namespace
 

@@ -6,7 +6,11 @@
 //   exp(tau A^T) = e^{c} sum'_k 2 I_k(gamma) T_k(Xs),   Xs = (tau A^T - c I) / gamma,
 //   c = tau (a + b) / 2, gamma = tau (b - a) / 2,
 // with the degree K fixed a priori from the coefficient tail (no norm reductions in the loop).
-// For a symmetric A the truncation error is <= tail * ||X|| (spectrum inside [a, b]).
+// For a symmetric A the truncation error is <= tail * e^{tau b} * ||X|| (spectrum inside [a, b]),
+// i.e. e^{tau (b - lambda_max)} times the tail relative to the action's size: dme.cu accepts the
+// expansion only when tau max(b, 0) <= ln 4 or, with a Lanczos estimate of lambda_max,
+// tau (b - lambda_max) <= ln 4 (dme.cu: cheb_accurate); otherwise the dense path uses Padé-13 and
+// the sparse path rejects A (DME_ERR_CONFIG).
 //
 // Device layout (cheb.cu): A^T in ELL form, partitioned over the CHEB_CLUSTER CTAs of a thread-block
 // cluster (rows [r R, (r + 1) R) on CTA r); one cluster per group of C columns of X. Each CTA keeps

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -28,6 +29,18 @@ int64_t launch_count();
     ::dme::note_launch();               \
     DME_CUDA(cudaGetLastError());       \
   } while (0)
+
+// Run f (kernel attribute setup: cudaFuncSetAttribute applies per device) once per device ordinal;
+// the mutex also makes concurrent first calls from several host threads safe.
+template <class F>
+inline void per_device_once(std::mutex& m, uint64_t& mask, F&& f) {
+  int dev = 0;
+  DME_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(m);
+  if ((mask >> (dev & 63)) & 1) return;
+  f();
+  mask |= 1ull << (dev & 63);
+}
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -307,6 +307,79 @@ void shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, in
   *rows = std::min<int64_t>(nl, n - *row0);
 }
 
+// Largest Ritz value of a symmetric CSR matrix after `iters` plain Lanczos steps (host; a lower
+// estimate of lambda_max: Ritz values lie inside the spectrum, and the extreme one converges first,
+// loss of orthogonality only adds ghost copies). Start vector: a fixed pseudo-random one.
+double lanczos_lmax(int64_t n, const int64_t* rp, const int32_t* ci, const double* vv, int iters) {
+  std::vector<double> q(n), qp(n, 0.0), w(n);
+  uint64_t s = 0x9E3779B97F4A7C15ull;
+  double nrm = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    s = s * 6364136223846793005ull + 1442695040888963407ull;
+    q[i] = (double)(s >> 11) * 0x1.0p-53 - 0.5;
+    nrm += q[i] * q[i];
+  }
+  nrm = std::sqrt(nrm);
+  for (auto& x : q) x /= nrm;
+  std::vector<double> al, be;
+  double beta = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    for (int64_t i = 0; i < n; ++i) {
+      double acc = 0.0;
+      for (int64_t e = rp[i]; e < rp[i + 1]; ++e) acc += vv[e] * q[ci[e]];
+      w[i] = acc - beta * qp[i];
+    }
+    double alpha = 0.0;
+    for (int64_t i = 0; i < n; ++i) alpha += w[i] * q[i];
+    for (int64_t i = 0; i < n; ++i) w[i] -= alpha * q[i];
+    double b2 = 0.0;
+    for (int64_t i = 0; i < n; ++i) b2 += w[i] * w[i];
+    al.push_back(alpha);
+    beta = std::sqrt(b2);
+    if (!(beta > 1e-300)) break;
+    be.push_back(beta);
+    for (int64_t i = 0; i < n; ++i) { qp[i] = q[i]; q[i] = w[i] / beta; }
+  }
+  // largest eigenvalue of the Lanczos tridiagonal by bisection on its Sturm sequence
+  const int m = (int)al.size();
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < m; ++i) {
+    const double r = (i > 0 ? std::fabs(be[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(be[i]) : 0.0);
+    lo = std::min(lo, al[i] - r);
+    hi = std::max(hi, al[i] + r);
+  }
+  auto count_below = [&](double x) {  // eigenvalues < x
+    int cnt = 0;
+    double dq = 1.0;
+    for (int i = 0; i < m; ++i) {
+      dq = (al[i] - x) - (i > 0 ? be[i - 1] * be[i - 1] / dq : 0.0);
+      if (dq == 0.0) dq = -1e-300;
+      cnt += dq < 0.0;
+    }
+    return cnt;
+  };
+  for (int it = 0; it < 200 && hi - lo > 1e-12 * std::max(std::fabs(lo), std::fabs(hi)); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (count_below(mid) < m) lo = mid; else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// Accuracy gate of the Chebyshev exponential action (cheb.h): its truncation error is
+// 2^-56 e^{tau b} ||X|| (b = the Gershgorin upper bound of A), so relative to the action's size
+// e^{tau lambda_max} it is amplified by e^{tau (b - lambda_max)}. Accept when tau max(b, 0) <= ln 4
+// (absolute error <= 4 2^-56 ||X||, the level of the FP64 Padé products) or when the Lanczos
+// estimate gives tau (b - lambda_max) <= ln 4 (it underestimates lambda_max: conservative).
+bool cheb_accurate(double tau, double b, int64_t n, const int64_t* rp, const int32_t* ci,
+                   const double* vv, double* lmax_out) {
+  const double lim = std::log(4.0);
+  *lmax_out = NAN;
+  if (tau * std::max(b, 0.0) <= lim) return true;
+  const double lm = lanczos_lmax(n, rp, ci, vv, 40);
+  *lmax_out = lm;
+  return tau * (b - lm) <= lim;
+}
+
 void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->n = pr->n;
   c->ldn = (pr->n + 15) / 16 * 16;
@@ -330,6 +403,11 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
     std::string err;
     const int code = cheb_prepare(pr->n, pr->A_nnz, pr->A_rowptr, pr->A_colind, pr->A_values, c->chost, &err);
     if (code) throw DmeError((dme_status)code, err);
+    double lm = 0;
+    DME_REQUIRE(cheb_accurate(o->h, c->chost.b, pr->n, pr->A_rowptr, pr->A_colind, pr->A_values, &lm),
+                DME_ERR_CONFIG,
+                "sparse A: the Gershgorin bound of A is too loose for an accurate Chebyshev action "
+                "(h (b - lambda_max) > ln 4); pass A dense (Padé-13)");
   }
   // E pass on the int8 tensor cores (exact digit slicing) unless disabled or out of its range
   c->oz = !c->sparse && o->e_pass != DME_EPASS_DMMA && c->n <= OZ_KMAX && c->rows_loc > 0;
@@ -1209,7 +1287,20 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     if (cheb_csr_from_dense(c->Aup, n, ld, 16 * n, c->X2, st, rp, ci, vv)) {
       ChebHost ch;
       std::string err;
-      if (cheb_prepare(n, (int64_t)vv.size(), rp.data(), ci.data(), vv.data(), ch, &err) == 0 &&
+      double lm_est = 0;
+      // (accuracy gate: ADVICE r1; cost model: the Chebyshev-built E costs ~K ceil(n/60) cluster
+      // waves of ~2.1 us per degree (measured, §9c), Padé-13 with int8 products ~0.33 s (n/1e4)^3)
+      const bool ok_prep = cheb_prepare(n, (int64_t)vv.size(), rp.data(), ci.data(), vv.data(), ch, &err) == 0;
+      bool take = ok_prep && cheb_accurate(c->h, ch.b, n, rp.data(), ci.data(), vv.data(), &lm_est);
+      if (take) {
+        std::vector<double> chat;
+        const double gamma = 0.5 * tau0 * (ch.b - ch.a);
+        const int K = cheb_coeffs(gamma, std::ldexp(1.0, -56), chat);
+        const double t_cheb = K * std::ceil(n / 60.0) * 2.1e-6;
+        const double t_pade = 0.33 * std::pow(n / 1e4, 3.0) + 2e-3;
+        take = t_cheb <= t_pade;
+      }
+      if (take &&
           (size_t)ch.w * CHEB_CLUSTER * ch.R <= (size_t)n * ld && ch.push.size() <= (size_t)n * ld &&
           ch.rptr.size() <= (size_t)n * ld && ch.rent.size() <= (size_t)n * ld) {
         c->chost = std::move(ch);
@@ -1306,6 +1397,16 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
       lincomb(c->T1, n, ld, {}, {}, {}, {}, 1.0, st);
       c->stats.cheb_degree = cheb_action(c->cop, tau0, c->T1, ld, n, c->E_half, ld, 1.0, st);
       mirror_lower(c->E_half, n, ld, true, st);
+      {  // sanity of the Chebyshev-built E before it is sliced for every later step:
+         // finite, and ||E||_inf <= sqrt(n) ||E||_2 = sqrt(n) e^{tau lambda_max} <= sqrt(n) e^{tau b}
+        double en = 0;
+        rowabs_max(c->E_half, n, ld, c->red_scratch, c->norm_dev, st);
+        DME_CUDA(cudaMemcpyAsync(&en, c->norm_dev, 8, cudaMemcpyDeviceToHost, st));
+        sync(c);
+        const double bound = std::sqrt((double)n) * std::exp(tau0 * std::max(c->chost.b, 0.0)) * (1 + 1e-12);
+        DME_REQUIRE(std::isfinite(en) && en <= bound, DME_ERR_NUMERIC,
+                    "Chebyshev-built E_{h/2} failed its norm check (non-finite or too large)");
+      }
       matmul_sq(c, c->E_half, c->E_half, c->E_full);
       if (c->oz) {
         oz_slice_rows_tiled(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->exEh, c->ozpm, st);

@@ -396,13 +396,13 @@ void launch_fast(const SmallArgs& a, cudaStream_t st) {
   };
   size_t smem = bytes_for(a.k);
   if (smem < floor_b) smem = floor_b;
-  static bool attr = false;
-  if (!attr) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     const size_t need = bytes_for(FK);
     DME_CUDA(cudaFuncSetAttribute(eig_fast_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(need > floor_b ? need : floor_b)));
-    attr = true;
-  }
+  });
   eig_fast_kernel<FK><<<1, ENT, smem, st>>>(a);
   DME_KCHECK();
 }

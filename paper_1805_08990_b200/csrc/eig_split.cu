@@ -570,8 +570,9 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
   const size_t need_max = sizeof(double) * (size_t)FK * (FK | 1);
   size_t smem = sizeof(double) * (size_t)a.k * (a.k | 1);
   if (smem < floor_b) smem = floor_b;
-  static bool attr = false;
-  if (!attr) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     int mx = (int)(need_max > floor_b ? need_max : floor_b);
     if (FK <= 96) {  // the VEC (twisted-factorisation arrays) and FIN (W, U, F) extras at k = FK
       const int vec_x = (int)(sizeof(double) * 2 * ((FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1) * FK);
@@ -581,8 +582,7 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
     DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_vec_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_fin_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    attr = true;
-  }
+  });
   eig_tri_kernel<FK><<<1, ENT, smem, st>>>(a);
   DME_KCHECK();
   constexpr int MAXE = (FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1;

@@ -306,19 +306,18 @@ void lu_solve_right(double* Q, double* P, int64_t n, int64_t ld, double* QT, dou
   sl.crow_idx = reinterpret_cast<int*>(sl.rowk + 2 * NB);        // 2 G ints
   int* ipiv = sl.crow_idx + 2 * PANEL_MAX_CTAS;                   // n ints
   int* perm = ipiv + n;                                           // n ints
-  static int attr_dev = -1;
-  int dev = 0;
-  DME_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(diag_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   DIAG_SMEM));
     DME_CUDA(cudaFuncSetAttribute(panel_piv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   220 * 1024));
     DME_CUDA(cudaFuncSetAttribute(build_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   12288 * 4));
-    attr_dev = dev;
-  }
-  int nsm = 148;
+  });
+  int nsm = 148, dev = 0;
+  DME_CUDA(cudaGetDevice(&dev));
   DME_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   init_minpiv<<<1, 1, 0, st>>>(minpiv_dev);
   DME_KCHECK();

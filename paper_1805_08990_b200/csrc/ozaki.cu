@@ -499,11 +499,11 @@ void launch_oz(const OzGemmArgs& a, OzScratch& ws, cudaStream_t st) {
     tmA = make_tmap_3d_u8(a.A, a.K, a.M, OZ_S, a.lda, a.a_slice_stride, 128, 128, 1);
   const CUtensorMap tmB = make_tmap_3d_u8(a.B, a.K, listed ? a.N : NP, OZ_S, a.ldb, a.b_slice_stride,
                                           128, NP, OZ_S);
-  static bool attr = false;
-  if (!attr) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr = true;
-  }
+  });
   oz_gemm_kernel<NP><<<G, 224, C::SMEM, st>>>(tmA, tmB, a.eA, a.eB, a.out, a.out_rs, a.out_cs,
                                               (int)a.M, (int)a.N, nkc, ntiles, a.tiles,
                                               a.round_robin ? 1 : 0, a.alpha, ws.partial,

@@ -399,15 +399,13 @@ __global__ void __launch_bounds__(NT) tail_assemble_kernel(SmallArgs a, const do
 void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, int64_t ldu,
                       cudaStream_t st) {
   if (k > FAST_K_MAX || kb > k || kb < 0) throw std::runtime_error("complement_basis: bad size");
-  static int attr_dev = -1;
-  int dev = 0;
-  DME_CUDA(cudaGetDevice(&dev));
   const int mx = (int)(sizeof(double) * FAST_K_MAX * (FAST_K_MAX | 1));
-  if (attr_dev != dev) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(complement_basis_kernel<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(complement_basis_kernel<5, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    attr_dev = dev;
-  }
+  });
   const size_t smem = sizeof(double) * (size_t)(kb > 0 ? kb : 1) * (k | 1);
   if (k <= 96) complement_basis_kernel<3, 3><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   else complement_basis_kernel<5, 5><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
@@ -431,14 +429,12 @@ void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, c
     if (a.t3 && r > 0) t3_only(a, r, st);
     return;
   }
-  static int attr_dev = -1;
-  int dev = 0;
-  DME_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(tail_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SMALL_SMEM_MAX));
-    attr_dev = dev;
-  }
+  });
   tail_assemble_kernel<<<1, NT, need, st>>>(a, U, ldu, s, V, ldv, kb, ks);
   DME_KCHECK();
 }
@@ -460,12 +456,12 @@ void compress_t3(const SmallArgs& a, cudaStream_t st) {
   if (a.t3 && a.m > SMALL_M_MAX) throw std::runtime_error("compress_t3: m exceeds SMALL_M_MAX");
   size_t smem = a.compress ? sizeof(double) * (size_t)a.k * (a.k + 1) / 2 : 0;
   if (smem < sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX) smem = sizeof(double) * 2 * SMALL_K_MAX * SMALL_M_MAX;
-  static bool attr = false;
-  if (!attr) {
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(compress_t3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SMALL_SMEM_MAX));
-    attr = true;
-  }
+  });
   compress_t3_kernel<<<1, NT, smem, st>>>(a);
   DME_KCHECK();
 }

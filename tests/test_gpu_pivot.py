@@ -66,3 +66,39 @@ def test_pade_random_nonsymmetric_needs_pivoting(dme, n, seed):
         ref = sla.expm(t * A.T)
         assert np.abs(E - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max())
     s.close()
+
+
+def _biharmonic(nx):
+    from workloads import heat2d_matrix
+    L = heat2d_matrix(nx)
+    return -(L @ L)   # symmetric, 13 nonzeros per row, NOT diagonally dominant: Gershgorin b >> 0
+
+
+@pytest.mark.parametrize("h", [2e-4, 2e-5])
+def test_auto_expm_gate_non_diagonally_dominant(dme, h):
+    """AUTO may build E by Chebyshev actions only when the expansion is accurate: for -L^2 the
+    Gershgorin bound b >> lambda_max, the truncation error would be e^{tau (b - lambda_max)} times
+    the tail (relative error 1e14 at tau = 1e-4); the gate sends it to Padé-13."""
+    nx = 12
+    A = _biharmonic(nx)
+    n = A.shape[0]
+    rng = np.random.default_rng(3)
+    kw = dict(A=A, C=rng.uniform(size=(1, n)), B=rng.uniform(size=(n, 1)), R=np.eye(1))
+    s = dme.Solver(**kw, h=h)
+    for which, t in ((0, h / 2), (1, h)):
+        E = s.debug_get_exp(which)
+        ref = sla.expm(t * A.T)
+        assert np.abs(E - ref).max() <= 1e-13 * np.abs(ref).max(), (which, np.abs(E - ref).max())
+    s.close()
+    import scipy.sparse as sps
+    kw["A"] = sps.csr_matrix(A)
+    with pytest.raises(dme.DmeError):
+        dme.Solver(**kw, h=h)
+
+
+def test_auto_expm_gate_keeps_heat_on_chebyshev(dme):
+    from workloads import make_config
+    prob = make_config(5, nx=20)
+    s = dme.Solver(**dme.problem_kwargs(prob), h=0.005)
+    assert s.stats()["expm_chebyshev"] == 1
+    s.close()

@@ -166,9 +166,14 @@ def test_action_wide_rows_fallback_kernel(dme):
     shared memory, halo pushes in a separate phase): against expm."""
     rng = np.random.default_rng(11)
     n = 300
-    B = sps.random(n, n, density=3.0 / n, random_state=12, format="csr") + sps.eye(n)
-    A = -(B @ B.T) * 50.0  # symmetric negative semidefinite, a few dozen entries per row at most
-    A = sps.csr_matrix(A)
+    Wr = sps.random(n, n, density=4.0 / n, random_state=12, format="csr")
+    Wg = Wr + Wr.T                                   # symmetric nonnegative weights, ~8 per row
+    Wg.setdiag(0.0)
+    Wg.eliminate_zeros()
+    deg = np.asarray(Wg.sum(axis=1)).ravel()
+    # minus a weighted graph Laplacian: symmetric, negative semidefinite and diagonally dominant
+    # (Gershgorin b = 0: the Chebyshev accuracy gate of dme.cu accepts it)
+    A = sps.csr_matrix(-(sps.diags(deg) - Wg) * 50.0)
     assert np.diff(A.indptr).max() > 5
     h = 0.01
     s = dme.Solver(A=A, h=h)
