@@ -155,6 +155,11 @@ typedef struct {
                              reduced-SVD compression does.
                              DME_COMPRESS_GRAM: the single Gram pass, with the effective
                              tolerance max(trunc_tol, 1e-14)                                    */
+  int32_t virtual_world;  /* G > 1 with world_size == 1: run the row-sharded multi-GPU code on ONE
+                             GPU as G virtual shards: every E pass computes each shard's rows into
+                             its staging block, one ncclAllGather on a one-rank communicator and
+                             the unpack, exactly as a G-rank run does (test hook for the a13 path;
+                             results equal the unsharded run up to rounding). 0/1: off           */
 } dme_options;
 
 typedef enum { DME_COMPRESS_REFINED = 0, DME_COMPRESS_GRAM = 1 } dme_compression;

@@ -51,7 +51,7 @@ class _Options(ctypes.Structure):
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("big_inputs_on_device", ctypes.c_int32), ("no_fsal", ctypes.c_int32),
                 ("e_pass", ctypes.c_int32), ("expm", ctypes.c_int32),
-                ("compression", ctypes.c_int32)]
+                ("compression", ctypes.c_int32), ("virtual_world", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -182,7 +182,7 @@ class Solver:
                  trunc_tol=1e-16,
                  rank_cap=0, quad_nodes=14, quad_subpanels=1, device=None, stream=None,
                  world_size=1, world_rank=0, nccl_uid: Optional[bytes] = None, fsal=True,
-                 e_pass="auto", expm="auto", compression="refined", poison_workspace=False):
+                 e_pass="auto", expm="auto", compression="refined", virtual_world=0, poison_workspace=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1805_08990_b200.Solver needs a CUDA device (no CPU fallback)")
@@ -238,7 +238,7 @@ class Solver:
                        world_rank=world_rank, nccl_uid=ctypes.cast(uid, ctypes.c_void_p) if uid else None,
                        workspace=None, workspace_bytes=0, big_inputs_on_device=1 if on_dev else 0,
                        no_fsal=0 if fsal else 1, e_pass=E_PASS[e_pass], expm=EXPM[expm],
-                       compression=COMPRESSION[compression])
+                       compression=COMPRESSION[compression], virtual_world=virtual_world)
         nbytes = ctypes.c_size_t(0)
         _check(_lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(opt), ctypes.byref(nbytes)),
                "dme_workspace_size")

@@ -108,8 +108,14 @@ struct Planner {
 struct dme_ctx {
   int64_t n = 0, ldn = 0, p = 0, m = 0, r0 = 0;
   bool has_S = false, dre = false;
-  int world = 1, rank = 0;
+  int world = 1, rank = 0;  // logical shards of E's rows (= ranks, or virtual shards) and this rank
   int64_t nloc = 0, row0 = 0, rows_loc = 0;
+  // shards computed by this process: real multi-rank: {rank}; options.virtual_world = G on one GPU:
+  // all G (each through the same per-shard kernels, staging block, NCCL allgather on a one-rank
+  // communicator and unpack as a real G-rank run); rows of E held in memory: [erow0, erow0 + erows)
+  bool virt = false;
+  int nsh = 1, sh0 = 0;
+  int64_t erow0 = 0, erows = 0, img = 0;
   dme_options opt{};
   cudaStream_t st = nullptr;
   double h = 0;
@@ -194,9 +200,9 @@ namespace {
 void plan_buffers(dme_ctx* c, Planner& P) {
   const int64_t n = c->n, ld = c->ldn;
   const size_t nn = (size_t)n * ld, fk = (size_t)ld * KMAX;
-  if (!c->sparse) {
-    c->E_half = P.take<double>(nn);
-    c->E_full = P.take<double>(nn);
+  if (!c->sparse) {  // the rows of E this process holds (a real rank: its own rows only)
+    c->E_half = P.take<double>((size_t)std::max<int64_t>(c->erows, 1) * ld);
+    c->E_full = P.take<double>((size_t)std::max<int64_t>(c->erows, 1) * ld);
   } else {  // partitioned ELL of A^T (cheb.h); no n x n matrix in sparse mode
     const size_t ell = (size_t)c->chost.w * CHEB_CLUSTER * c->chost.R;
     c->cop.n = c->chost.n; c->cop.R = c->chost.R; c->cop.w = c->chost.w; c->cop.C = c->chost.C;
@@ -248,10 +254,11 @@ void plan_buffers(dme_ctx* c, Planner& P) {
     const int64_t rl = std::max<int64_t>(c->rows_loc, 1);
     // E-digit buffers: the local rows of E for the passes, and during the (replicated) init the
     // digits of both n x n operands of each product: n rows
-    const int64_t rb = c->oz_init ? std::max<int64_t>(rl, n) : rl;
-    // (the E passes read the tiled, pre-swizzled image of oz_slice_rows_tiled; the init products
-    // the row layout)
-    const size_t es = std::max<size_t>((size_t)OZ_S * rb * c->ozld, (size_t)oz_tiled_bytes(rl, n));
+    const int64_t rb = std::max<int64_t>(c->oz_init ? std::max<int64_t>(rl, n) : rl, (int64_t)c->nsh * c->nloc);
+    // (the E passes read the tiled, pre-swizzled image of oz_slice_rows_tiled, one image per shard
+    // computed here; the init products the row layout)
+    c->img = (oz_tiled_bytes(std::max<int64_t>(c->nloc, 1), n) + 255) / 256 * 256;
+    const size_t es = std::max<size_t>((size_t)OZ_S * rb * c->ozld, (size_t)c->nsh * c->img);
     const size_t ys = (size_t)OZ_S * OZ_NMAX * c->ozld;
     c->ozEh = P.take<int8_t>(es);
     c->ozEf = P.take<int8_t>(es);
@@ -278,7 +285,7 @@ void plan_buffers(dme_ctx* c, Planner& P) {
       o->counters = P.take<int>((size_t)o->max_tiles);
     }
   }
-  if (c->world > 1) c->stage = P.take<double>((size_t)c->world * c->nloc * KMAX);
+  if (c->world > 1) c->stage = P.take<double>((size_t)c->world * c->nloc * KMAX);  // (virtual too)
   // init-only
   if (!c->sparse) {
     c->Aup = P.take<double>(nn);
@@ -390,7 +397,14 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->opt = *o;
   c->world = o->world_size > 0 ? o->world_size : 1;
   c->rank = o->world_rank;
-  shard_rows(c->n, c->world, c->rank, &c->row0, &c->rows_loc, &c->nloc);
+  c->virt = c->world == 1 && o->virtual_world > 1;
+  if (c->virt) c->world = o->virtual_world;
+  c->nsh = c->virt ? c->world : 1;
+  c->sh0 = c->virt ? 0 : c->rank;
+  shard_rows(c->n, c->world, c->sh0, &c->row0, &c->rows_loc, &c->nloc);
+  // E rows held: a real rank keeps its own rows only; one process (single or virtual) all of them
+  c->erow0 = (c->world > 1 && !c->virt) ? c->row0 : 0;
+  c->erows = (c->world > 1 && !c->virt) ? c->rows_loc : c->n;
   c->qn = o->quad_nodes > 0 ? o->quad_nodes : 14;
   c->subpanels = o->quad_subpanels > 0 ? o->quad_subpanels : 1;
   int64_t cap = o->rank_cap > 0 ? o->rank_cap : c->n;
@@ -428,7 +442,8 @@ void validate(const dme_problem* pr, const dme_options* o, bool dre) {
               "n must be positive and A (dense) or A_rowptr (sparse) non-NULL");
   if (!pr->A) {
     DME_REQUIRE(!pr->M, DME_ERR_CONFIG, "a mass matrix M is not supported with a sparse A");
-    DME_REQUIRE(o->world_size <= 1, DME_ERR_CONFIG, "a sparse A runs on one GPU (world_size 1)");
+    DME_REQUIRE(o->world_size <= 1 && o->virtual_world <= 1, DME_ERR_CONFIG,
+                "a sparse A runs on one GPU (world_size 1, no virtual shards)");
   }
   DME_REQUIRE(std::isfinite(o->h) && o->h > 0, DME_ERR_INVALID, "h must be positive and finite");
   DME_REQUIRE(pr->p >= 0 && (pr->p == 0 || pr->C), DME_ERR_INVALID, "C must be non-NULL when p > 0");
@@ -447,6 +462,7 @@ void validate(const dme_problem* pr, const dme_options* o, bool dre) {
   const int sp = o->quad_subpanels > 0 ? o->quad_subpanels : 1;
   DME_REQUIRE((sp & (sp - 1)) == 0, DME_ERR_INVALID, "quad_subpanels must be a power of two");
   DME_REQUIRE(o->world_size <= 1 || o->nccl_uid, DME_ERR_INVALID, "nccl_uid required for world_size > 1");
+  DME_REQUIRE(o->virtual_world >= 0 && o->virtual_world <= 64, DME_ERR_INVALID, "virtual_world must be in [0, 64]");
   // input finiteness (host scan; inputs are host arrays)
   const size_t nn = (size_t)pr->n * pr->n;
   (void)nn;  // A and S (n x n) are checked on the device after the upload (init_all)
@@ -583,53 +599,72 @@ void drain_profile(dme_ctx* c) {
 
 // ------------------------------------------------------------------ building blocks
 // out (col-major, ldo) = alpha * E * X  (E: n x n row-major, X: n x k col-major), sharded over ranks
-// out (rows x k) = alpha * E[rows] * X on the int8 tensor cores; E = E_{h/2} or E_h (sliced)
-void oz_pass(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t out_cs,
-             double alpha, cudaStream_t st, bool second) {
-  // profiled as the E-pass kernel: the int8 product alone (the digit slicing of X, ~n k bytes, is
-  // its own pair of small kernels before it)
-  int8_t* yq = second ? c->ozY2 : c->ozY;
-  int* ye = second ? c->exY2 : c->exY;
-  oz_slice_rows(X, c->ldn, k, c->n, yq, c->ozld, (int64_t)OZ_NMAX * c->ozld, ye,
-                second ? c->ozpm2 : c->ozpm, st);
+// rows [row0, row0 + rows) of shard s (s-th block of nloc rows)
+void shard_range(const dme_ctx* c, int s, int64_t* r0, int64_t* rows) {
+  *r0 = std::min<int64_t>(c->n, (int64_t)s * c->nloc);
+  *rows = std::min<int64_t>(c->nloc, c->n - *r0);
+}
+
+// digit slices of the columns of X (one per pass; shared by the shards of this process)
+void oz_slice_operand(dme_ctx* c, const double* X, int64_t k, cudaStream_t st, bool second) {
+  oz_slice_rows(X, c->ldn, k, c->n, second ? c->ozY2 : c->ozY, c->ozld, (int64_t)OZ_NMAX * c->ozld,
+                second ? c->exY2 : c->exY, second ? c->ozpm2 : c->ozpm, st);
+}
+
+// out (rows_s x k) = alpha * E[rows of shard s] * X on the int8 tensor cores; E = E_{h/2} or E_h
+// (each shard's rows sliced once at init into their own tiled image); X already sliced
+void oz_pass(dme_ctx* c, const double* E, int s, int64_t k, double* out, int64_t out_cs, double alpha,
+             cudaStream_t st, bool second) {
+  int64_t r0, rows;
+  shard_range(c, s, &r0, &rows);
+  if (rows <= 0) return;
+  const int sl = s - c->sh0;  // local image index
   OzGemmArgs g;
-  g.A = E == c->E_full ? c->ozEf : c->ozEh;
-  g.eA = E == c->E_full ? c->exEf : c->exEh;
-  g.lda = c->ozld; g.a_slice_stride = c->rows_loc * c->ozld;
-  g.B = yq; g.eB = ye; g.ldb = c->ozld; g.b_slice_stride = (int64_t)OZ_NMAX * c->ozld;
-  g.M = c->rows_loc; g.N = k; g.K = c->n; g.alpha = alpha;
+  g.A = (E == c->E_full ? c->ozEf : c->ozEh) + (size_t)sl * c->img;
+  g.eA = (E == c->E_full ? c->exEf : c->exEh) + (size_t)sl * c->nloc;
+  g.lda = c->ozld; g.a_slice_stride = rows * c->ozld;
+  g.B = second ? c->ozY2 : c->ozY; g.eB = second ? c->exY2 : c->exY;
+  g.ldb = c->ozld; g.b_slice_stride = (int64_t)OZ_NMAX * c->ozld;
+  g.M = rows; g.N = k; g.K = c->n; g.alpha = alpha;
   g.out = out; g.out_rs = 1; g.out_cs = out_cs;
   g.A_tiled = g.A;  // E digits in the tiled image (oz_slice_rows_tiled at the end of init)
   {
+    // profiled as the E-pass kernel: the int8 product alone (the digit slicing of X, ~n k bytes,
+    // is its own pair of small kernels before it)
     ProfScope ps(c, PROF_EPASS, 2.0 * g.M * c->n * k, 1.0 * OZ_S * g.M * c->n, st);
     oz_gemm(g, second ? c->ozs2 : c->ozs, st);
   }
   c->stats.ozaki_passes++;
 }
 
+// tiled digit images of the shards this process computes, from E (its rows start at E's row erow0)
+void slice_shards(dme_ctx* c, const double* E, int8_t* img, int* ex, cudaStream_t st) {
+  for (int sl = 0; sl < c->nsh; ++sl) {
+    int64_t r0, rows;
+    shard_range(c, c->sh0 + sl, &r0, &rows);
+    if (rows > 0)
+      oz_slice_rows_tiled(E + (r0 - c->erow0) * c->ldn, c->ldn, rows, c->n, img + (size_t)sl * c->img,
+                          ex + (size_t)sl * c->nloc, c->ozpm, st);
+  }
+}
+
+// out (col-major, ldo) = alpha * E * X  (E: row-major, X: n x k col-major). E is E_{h/2} / E_h (the
+// rows this process holds) or a full n x n init buffer. Row-sharded (world > 1, real ranks or
+// virtual shards): every shard of this process computes its rows into its staging block
+// (nloc x k, col-major), one ncclAllGather replicates the blocks, a copy kernel unpacks them.
 void epass_on(dme_ctx* c, const double* E, const double* X, int64_t k, double* out, int64_t ldo,
               double alpha, cudaStream_t st, GemmScratch& gs) {
   if (k <= 0) return;
   c->stats.e_passes++;
   const bool second = &gs == &c->gs2;
-  const bool use_oz = c->oz && c->oz_ready && k <= OZ_NMAX && (E == c->E_half || E == c->E_full);
-  if (use_oz && c->world == 1) {
-    oz_pass(c, E, X, k, out, ldo, alpha, st, second);
-    return;
-  }
-  if (use_oz) {
-    double* mine = c->stage + (size_t)c->rank * c->nloc * k;
-    oz_pass(c, E, X, k, mine, c->nloc, alpha, st, second);
-    DME_NCCL(ncclAllGather(mine, c->stage, (size_t)c->nloc * k, ncclDouble, c->comm, st));
-    for (int gr = 0; gr < c->world; ++gr) {
-      const int64_t r0 = std::min<int64_t>(c->n, (int64_t)gr * c->nloc);
-      const int64_t rows = std::min<int64_t>(c->nloc, c->n - r0);
-      if (rows > 0)
-        copy_cols(out + r0, ldo, c->stage + (size_t)gr * c->nloc * k, c->nloc, rows, k, 1.0, st);
-    }
-    return;
-  }
+  const bool held = E == c->E_half || E == c->E_full;  // rows [erow0, erow0 + erows) only
+  const bool use_oz = c->oz && c->oz_ready && k <= OZ_NMAX && held;
+  if (use_oz) oz_slice_operand(c, X, k, st, second);
   if (c->world == 1) {
+    if (use_oz) {
+      oz_pass(c, E, 0, k, out, ldo, alpha, st, second);
+      return;
+    }
     GemmNTArgs g;
     g.A = E; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
     g.M = c->n; g.N = k; g.K = c->n; g.alpha = alpha;
@@ -638,20 +673,31 @@ void epass_on(dme_ctx* c, const double* E, const double* X, int64_t k, double* o
     gemm_nt(g, gs, st);
     return;
   }
-  // row shard: local rows into this rank's staging block (nloc x k, col-major), allgather, unpack
-  double* mine = c->stage + (size_t)c->rank * c->nloc * k;
-  if (c->rows_loc > 0) {
-    ProfScope ps(c, PROF_EPASS, 2.0 * c->rows_loc * c->n * k, 8.0 * c->rows_loc * c->n, st);
-    GemmNTArgs g;
-    g.A = E + c->row0 * c->ldn; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
-    g.M = c->rows_loc; g.N = k; g.K = c->n; g.alpha = alpha;
-    g.out = mine; g.out_rs = 1; g.out_cs = c->nloc;
-    gemm_nt(g, gs, st);
+  for (int sl = 0; sl < c->nsh; ++sl) {
+    const int s = c->sh0 + sl;
+    double* blk = c->stage + (size_t)s * c->nloc * k;
+    int64_t r0, rows;
+    shard_range(c, s, &r0, &rows);
+    if (rows <= 0) continue;
+    if (use_oz) {
+      oz_pass(c, E, s, k, blk, c->nloc, alpha, st, second);
+    } else {
+      ProfScope ps(c, PROF_EPASS, 2.0 * rows * c->n * k, 8.0 * rows * c->n, st);
+      GemmNTArgs g;
+      g.A = E + (held ? r0 - c->erow0 : r0) * c->ldn; g.lda = c->ldn; g.B = X; g.ldb = c->ldn;
+      g.M = rows; g.N = k; g.K = c->n; g.alpha = alpha;
+      g.out = blk; g.out_rs = 1; g.out_cs = c->nloc;
+      gemm_nt(g, gs, st);
+    }
   }
-  DME_NCCL(ncclAllGather(mine, c->stage, (size_t)c->nloc * k, ncclDouble, c->comm, st));
+  if (c->virt)  // one-rank communicator: all G blocks are "this rank's" contribution
+    DME_NCCL(ncclAllGather(c->stage, c->stage, (size_t)c->world * c->nloc * k, ncclDouble, c->comm, st));
+  else
+    DME_NCCL(ncclAllGather(c->stage + (size_t)c->rank * c->nloc * k, c->stage, (size_t)c->nloc * k,
+                           ncclDouble, c->comm, st));
   for (int gr = 0; gr < c->world; ++gr) {
-    const int64_t r0 = std::min<int64_t>(c->n, (int64_t)gr * c->nloc);
-    const int64_t rows = std::min<int64_t>(c->nloc, c->n - r0);
+    int64_t r0, rows;
+    shard_range(c, gr, &r0, &rows);
     if (rows > 0)
       copy_cols(out + r0, ldo, c->stage + (size_t)gr * c->nloc * k, c->nloc, rows, k, 1.0, st);
   }
@@ -1393,24 +1439,35 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     for (int j = 0; j < s_total; ++j) ladder_double(c, c->Zc12h, q_cur, nullptr, std::ldexp(delta, j));
     finish_ladder(q_cur, nullptr);
     if (c->cheb_e) {
-      // E_{h/2} = exp((h/2) A^T) I (columns = rows: A symmetric), exactly symmetrised; E_h = E_{h/2}^2
-      lincomb(c->T1, n, ld, {}, {}, {}, {}, 1.0, st);
-      c->stats.cheb_degree = cheb_action(c->cop, tau0, c->T1, ld, n, c->E_half, ld, 1.0, st);
-      mirror_lower(c->E_half, n, ld, true, st);
-      {  // sanity of the Chebyshev-built E before it is sliced for every later step:
-         // finite, and ||E||_inf <= sqrt(n) ||E||_2 = sqrt(n) e^{tau lambda_max} <= sqrt(n) e^{tau b}
+      const double bound = std::sqrt((double)n) * std::exp(tau0 * std::max(c->chost.b, 0.0)) * (1 + 1e-12);
+      auto check_norm = [&](const double* E, int64_t rows) {
+        // sanity of the Chebyshev-built E before it is sliced for every later step:
+        // finite, and ||E||_inf <= sqrt(n) ||E||_2 = sqrt(n) e^{tau lambda_max} <= sqrt(n) e^{tau b}
         double en = 0;
-        rowabs_max(c->E_half, n, ld, c->red_scratch, c->norm_dev, st);
+        rowabs_max(E, rows, ld, c->red_scratch, c->norm_dev, st);
         DME_CUDA(cudaMemcpyAsync(&en, c->norm_dev, 8, cudaMemcpyDeviceToHost, st));
         sync(c);
-        const double bound = std::sqrt((double)n) * std::exp(tau0 * std::max(c->chost.b, 0.0)) * (1 + 1e-12);
         DME_REQUIRE(std::isfinite(en) && en <= bound, DME_ERR_NUMERIC,
                     "Chebyshev-built E_{h/2} failed its norm check (non-finite or too large)");
+      };
+      lincomb(c->T1, n, ld, {}, {}, {}, {}, 1.0, st);  // identity (its columns e_j)
+      if (c->world == 1) {
+        // E_{h/2} = exp((h/2) A^T) I (columns = rows: A symmetric), exactly symmetrised; E_h = E_{h/2}^2
+        c->stats.cheb_degree = cheb_action(c->cop, tau0, c->T1, ld, n, c->E_half, ld, 1.0, st);
+        mirror_lower(c->E_half, n, ld, true, st);
+        check_norm(c->E_half, n);
+        matmul_sq(c, c->E_half, c->E_half, c->E_full);
+      } else {
+        // row-sharded: only the held rows, as columns of the symmetric E (E[rows, :] = (E I[:, rows])^T:
+        // a column-major n x rows block with leading dimension ldn IS the row-major rows x n block),
+        // E_h the same way with tau = h: no n x n matrix, no product, no collective
+        c->stats.cheb_degree = cheb_action(c->cop, tau0, c->T1 + c->erow0 * ld, ld, c->erows, c->E_half, ld, 1.0, st);
+        check_norm(c->E_half, c->erows);
+        cheb_action(c->cop, c->h, c->T1 + c->erow0 * ld, ld, c->erows, c->E_full, ld, 1.0, st);
       }
-      matmul_sq(c, c->E_half, c->E_half, c->E_full);
       if (c->oz) {
-        oz_slice_rows_tiled(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->exEh, c->ozpm, st);
-        oz_slice_rows_tiled(c->E_full + c->row0 * ld, ld, c->rows_loc, n, c->ozEf, c->exEf, c->ozpm, st);
+        slice_shards(c, c->E_half, c->ozEh, c->exEh, st);
+        slice_shards(c, c->E_full, c->ozEf, c->exEf, st);
         c->oz_ready = true;
       }
       c->cheb_e = false;  // the passes of the run use the dense E
@@ -1454,13 +1511,16 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     si ^= 1;
     Ecur = En;
   }
-  DME_CUDA(cudaMemcpyAsync(c->E_half, Ecur, (size_t)n * ld * 8, cudaMemcpyDeviceToDevice, st));
-  // L_I(h) = compress([L_I(h/2), E_{h/2} L_I(h/2)]),  E_h = E_{h/2}^2
-  finish_ladder(q_cur, c->E_half);
-  matmul_sq(c, c->E_half, c->E_half, c->E_full);
-  if (c->oz) {  // digit slices of the local rows of E_{h/2} and E_h (after the last product)
-    oz_slice_rows_tiled(c->E_half + c->row0 * ld, ld, c->rows_loc, n, c->ozEh, c->exEh, c->ozpm, st);
-    oz_slice_rows_tiled(c->E_full + c->row0 * ld, ld, c->rows_loc, n, c->ozEf, c->exEf, c->ozpm, st);
+  // L_I(h) = compress([L_I(h/2), E_{h/2} L_I(h/2)]),  E_h = E_{h/2}^2 (full n x n in init buffers);
+  // this process keeps the rows [erow0, erow0 + erows) of both (a real rank: its own rows)
+  finish_ladder(q_cur, Ecur);
+  double* Eh_full = spare[si];
+  matmul_sq(c, Ecur, Ecur, Eh_full);
+  DME_CUDA(cudaMemcpyAsync(c->E_half, Ecur + c->erow0 * ld, (size_t)c->erows * ld * 8, cudaMemcpyDeviceToDevice, st));
+  DME_CUDA(cudaMemcpyAsync(c->E_full, Eh_full + c->erow0 * ld, (size_t)c->erows * ld * 8, cudaMemcpyDeviceToDevice, st));
+  if (c->oz) {  // digit slices of the held rows of E_{h/2} and E_h (after the last product)
+    slice_shards(c, c->E_half, c->ozEh, c->exEh, st);
+    slice_shards(c, c->E_full, c->ozEf, c->exEf, st);
     c->oz_ready = true;
   }
   }  // dense E
@@ -1571,7 +1631,11 @@ dme_status init_common(const dme_problem* pr, const dme_options* o, dme_ctx** ou
     c->gs2.max_grid = la;
     c->ozs.max_grid = std::min(256, num_sms());
     c->ozs2.max_grid = la;
-    if (c->world > 1) {
+    if (c->virt) {  // one-rank communicator: the allgather of the virtual shards is a real NCCL call
+      ncclUniqueId uid;
+      DME_NCCL(ncclGetUniqueId(&uid));
+      DME_NCCL(ncclCommInitRank(&c->comm, 1, uid, 0));
+    } else if (c->world > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, o->nccl_uid, sizeof(uid));
       DME_NCCL(ncclCommInitRank(&c->comm, c->world, uid, c->rank));
@@ -1925,12 +1989,12 @@ dme_status dme_debug_set_exp(dme_ctx* c, int32_t which, const double* E) {
   return guarded(c, [&] {
     DME_REQUIRE(!c->sparse, DME_ERR_CONFIG, "no dense E with a sparse A");
     DME_REQUIRE(which == 0 || which == 1, DME_ERR_INVALID, "which must be 0 (E_{h/2}) or 1 (E_h)");
+    DME_REQUIRE(c->erows == c->n, DME_ERR_CONFIG, "this rank holds only its rows of E");
     double* dst = which ? c->E_full : c->E_half;
     DME_CUDA(cudaMemcpy2DAsync(dst, c->ldn * 8, E, c->n * 8, c->n * 8, c->n,
                                cudaMemcpyHostToDevice, c->st));
-    if (c->oz && c->oz_ready)  // the int8 E pass reads the digit image: re-slice the local rows
-      oz_slice_rows_tiled(dst + c->row0 * c->ldn, c->ldn, c->rows_loc, c->n, which ? c->ozEf : c->ozEh,
-                          which ? c->exEf : c->exEh, c->ozpm, c->st);
+    if (c->oz && c->oz_ready)  // the int8 E pass reads the digit images: re-slice them
+      slice_shards(c, dst, which ? c->ozEf : c->ozEh, which ? c->exEf : c->exEh, c->st);
     if (which == 1 && c->qf > 0)  // the look-ahead operand E_h L_I(h) of the pipelined body
       eact(c, true, c->Zc12f, c->qf, c->LA, c->ldn);
     if (which == 1 && c->m > 0 && 2 * c->qf + c->m <= KMAX)
@@ -1943,6 +2007,7 @@ dme_status dme_debug_get_exp(dme_ctx* c, int32_t which, double* E) {
   if (!c || !E) { g_last_error = "NULL argument"; return DME_ERR_INVALID; }
   return guarded(c, [&] {
     DME_REQUIRE(!c->sparse, DME_ERR_CONFIG, "no dense E with a sparse A");
+    DME_REQUIRE(c->erows == c->n, DME_ERR_CONFIG, "this rank holds only its rows of E");
     const double* src = which ? c->E_full : c->E_half;
     DME_CUDA(cudaMemcpy2DAsync(E, c->n * 8, src, c->ldn * 8, c->n * 8, c->n,
                                cudaMemcpyDeviceToHost, c->st));
