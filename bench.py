@@ -109,19 +109,46 @@ def _dist():
     return world, rank, local
 
 
-def cpu_baseline(prob, steps: int):
-    """The oracle (dense E_tau L products, SVD compression) timed on this host's cores."""
+def workload_label(config: int, prob) -> str:
+    """The workload string both arms print (BASELINE.json configs[4] for config 5)."""
+    if config == 5:
+        return (f"config5: DRE 2D heat n={prob.n} (n_x={int(round(prob.n ** 0.5))}), Strang F12F3, "
+                "rank cap 64, tol 1e-16 (refined compression), h=0.005 (T=0.5, N_t=100)")
+    return (f"config{config}: mass-matrix DRE (Example 4 structure, P1 FEM n={prob.n}), Strang F12F3, "
+            "rank cap 64, tol 1e-16 (refined compression), h=0.005 (T=0.5, N_t=100)")
+
+
+def cpu_baseline(prob, steps: int, one_thread_steps: int = 0):
+    """The oracle (dense E_tau L products, SVD compression) timed on this host's cores: its init
+    (closed-form heat exponential E_{h/2}, E_h; quadrature factor) timed separately, then `steps`
+    Strang F12F3 steps; optionally a second sample of `one_thread_steps` steps with BLAS limited
+    to one thread (threadpoolctl)."""
     from oracle.schemes import OracleOptions, OracleSolver
     cores = len(os.sched_getaffinity(0))
     t0 = time.perf_counter()
     orc = OracleSolver(prob, H, OracleOptions(rank_cap=RANK_CAP), dense_apply=True)
-    orc.step("strang", "F12F3", 1)          # builds E_{h/2}, L_I(h/2) (not timed)
+    orc.step("strang", "F12F3", 1)          # builds E_{h/2}, E_h and L_I(h/2), L_I(h): the init
     t1 = time.perf_counter()
     orc.step("strang", "F12F3", steps)
     t2 = time.perf_counter()
-    return {"value": steps / (t2 - t1), "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{steps} Strang F12F3 steps of {prob.name} (n={prob.n}) after a warm-up step; "
-                      f"oracle setup {t1 - t0:.1f}s untimed; NumPy/OpenBLAS threads = all cores"}
+    out = {"value": steps / (t2 - t1), "unit": UNIT, "cores": cores, "kind": "oracle",
+           "init_s": t1 - t0,
+           "time_to_T_s_est": (t1 - t0) + NT * (t2 - t1) / steps,
+           "sample": f"{steps} Strang F12F3 steps of {prob.name} (n={prob.n}) after the init step "
+                     f"(init incl. one step {t1 - t0:.1f}s, timed separately: closed-form heat "
+                     "exponential, not a general expm); NumPy/OpenBLAS threads = all cores"}
+    if one_thread_steps > 0:
+        try:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                t3 = time.perf_counter()
+                orc.step("strang", "F12F3", one_thread_steps)
+                t4 = time.perf_counter()
+            out["one_thread"] = {"value": one_thread_steps / (t4 - t3), "unit": UNIT, "cores": 1,
+                                 "sample": f"{one_thread_steps} more steps, BLAS limited to 1 thread"}
+        except Exception as ex:
+            out["one_thread"] = {"error": repr(ex)}
+    return out
 
 
 def run_reference(args):
@@ -135,7 +162,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config{args.config}: n={prob.n}, Strang F12F3, rank cap 64, h=0.005"},
+            "config": {"workload": workload_label(args.config, prob), "n": prob.n},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -222,6 +249,7 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = args.steps / (ms * 1e-3)
     rank_now = st["rank"]
+    q_full = st["q_full"]
     init_dev = st["init_seconds"]
     s.close()
     del s
@@ -341,6 +369,43 @@ def run_ours(args):
         del s3
         torch.cuda.empty_cache()
 
+    # ------------------------------------------------------------ Padé-13 init variant (a3-a5)
+    pade = None
+    if not args.no_pade and args.config == 5:
+        A_dev = torch.from_numpy(prob.A).cuda()
+        kw_p = dict(dme.problem_kwargs(prob), A=A_dev)
+        torch.cuda.synchronize()
+        t6 = time.perf_counter()
+        s6 = dme.Solver(**kw_p, **kw, expm="pade")
+        torch.cuda.synchronize()
+        init6 = time.perf_counter() - t6
+        del A_dev, kw_p
+        s6.split_step("strang", "F12F3", args.warmup)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(s6.stream)
+        s6.split_step("strang", "F12F3", args.steps)
+        v1.record(s6.stream)
+        torch.cuda.synchronize()
+        ms6 = v0.elapsed_time(v1)
+        if world > 1:
+            t = torch.tensor([ms6, init6], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms6, init6 = float(t[0].item()), float(t[1].item())
+        st6 = s6.stats()
+        pade = {"expm": "Padé-13 scaling and squaring (int8 digit-sliced products, pivoted LU solve) "
+                        "from HBM-resident A: SURVEY a3-a5",
+                "init_s": init6, "value": args.steps / (ms6 * 1e-3), "unit": UNIT,
+                "ms_per_step": ms6 / args.steps,
+                "time_to_T_s": init6 + NT * ms6 / args.steps * 1e-3,
+                "squarings": st6["squarings"], "pade_min_pivot": st6["pade_min_pivot"],
+                "expm_chebyshev": st6["expm_chebyshev"]}
+        s6.close()
+        del s6
+        torch.cuda.empty_cache()
+
     # ------------------------------------------------------------ sparse-A variant
     sparse = None
     if not args.no_sparse and args.config == 5 and world == 1:
@@ -404,7 +469,7 @@ def run_ours(args):
         cb = {"skipped": "cpu_baseline is reported for the headline workload (config 5) only"}
     elif rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cb = cpu_baseline(prob, 2)
+            cb = cpu_baseline(prob, 10, one_thread_steps=3)
         except Exception as ex:  # reported, never fatal
             cb = {"error": repr(ex)}
 
@@ -418,12 +483,10 @@ def run_ours(args):
                                  "int32 exact accumulation, FP64 assembly; per-entry error <= "
                                  "2^-54 max_l|E_il| sum_l|L_lj|, DESIGN.md 5b)"
                                  if st["ozaki_passes"] > 0 else "FP64 (DMMA + DFMA)"),
-                "config": {"workload": (f"config{args.config}: " + (
-                               "DRE 2D heat n=10000 (n_x=100), Strang F12F3, rank cap 64, tol 1e-16, "
-                               "h=0.005 (T=0.5, N_t=100)" if args.config == 5 else
-                               f"mass-matrix DRE (Example 4 structure, P1 FEM n={prob.n}), Strang "
-                               "F12F3, rank cap 64, tol 1e-16, h=0.005 (T=0.5, N_t=100)")),
+                "config": {"workload": workload_label(args.config, prob),
                            "n": prob.n, "rank_after_timed_steps": rank_now,
+                           "q_full": q_full, "compression": "refined: two eigen passes, the tail "
+                           "resolved from the explicit projected factor (trunc_tol 1e-16 honoured)",
                            "l2": f"inputs larger than L2 (E_h = {8 * prob.n ** 2 / 1e6:.0f} MB, 126 MB L2, "
                                  "streamed per pass)",
                            "parallelism": f"rows of E sharded over {world} GPU(s)"},
@@ -433,7 +496,7 @@ def run_ours(args):
                 "init_s": init_wall, "init_lib_s": init_dev,
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(),
-                "fp64_dmma_variant": variant, "sparse_variant": sparse}
+                "fp64_dmma_variant": variant, "pade_variant": pade, "sparse_variant": sparse}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -453,6 +516,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variant", action="store_true", help="skip the native-FP64 E-pass run")
     ap.add_argument("--no-sparse", action="store_true", help="skip the sparse-A (Chebyshev) run")
+    ap.add_argument("--no-pade", action="store_true", help="skip the Padé-13 init run")
     args = ap.parse_args()
     if args.nx is None:
         args.nx = 100 if args.config == 5 else 70

@@ -19,6 +19,10 @@ class Operator:
     method 'eigh'   : symmetric A = V diag(lam) V^T, exp(tA^T) X = V diag(e^{t lam}) V^T X
     method 'heat'   : the Dirichlet FD Laplacian's closed-form sine eigenbasis (pin P5),
                       for 1D (n = nx) or 2D (n = nx^2, index i*nx+j) problems
+    method 'action' : exp(t A^T) X by scipy.sparse.linalg.expm_multiply (Al-Mohy & Higham 2011,
+                      truncated Taylor with scaling, double-precision tolerance) on A^T in CSR, the
+                      a6 oracle form of SURVEY §8(c) for large nonsymmetric A (every quadrature
+                      node action without a dense exponential); dense E(t) by expm when asked
     """
 
     def __init__(self, A, method="auto", heat_nx=None, heat_dim=None, dense_apply=False):
@@ -36,6 +40,9 @@ class Operator:
                 method = "expm"
         self.method = method
         self._E = {}
+        if method == "action":
+            import scipy.sparse as sps
+            self.At = sps.csr_matrix(self.A.T)
         if method == "eigh":
             self.lam, self.V = np.linalg.eigh(self.A)
         elif method == "heat":
@@ -62,7 +69,7 @@ class Operator:
     def E(self, t):
         """Dense exp(t A^T)."""
         if t not in self._E:
-            if self.method == "expm":
+            if self.method in ("expm", "action"):
                 self._E[t] = sla.expm(t * self.A.T)
             else:
                 self._E[t] = self._from_eig(np.exp(t * self.lam)[:, None] * self._to_eig(
@@ -90,6 +97,9 @@ class Operator:
         """exp(t A^T) X."""
         if X.shape[1] == 0:
             return X.copy()
+        if self.method == "action":
+            from scipy.sparse.linalg import expm_multiply
+            return expm_multiply(t * self.At, X)
         if self.method == "expm":
             return self.E(t) @ X
         return self._from_eig(np.exp(t * self.lam)[:, None] * self._to_eig(X))

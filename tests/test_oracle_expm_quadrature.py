@@ -128,3 +128,17 @@ def test_two_node_single_panel_is_inaccurate():
     LI, DI = flows.build_integral(op, tau, tau, 2, C.T, np.eye(1), 1e-16)
     ref = exact.dle_vanloan(A, C.T @ C, np.zeros((25, 25)), tau)
     assert np.linalg.norm(lowrank.to_dense(LI, DI) - ref) > 1e-8 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("dim,nx,t", [(1, 60, 1e-3), (2, 14, 5e-3), (2, 20, 2.5e-3)])
+def test_operator_action_method_vs_closed_form(dim, nx, t):
+    """The 'action' method (expm_multiply on the sparse A^T) against the DST closed form of the
+    heat exponential (pin P5): the oracle's route for large nonsymmetric A is pinned on an
+    operator whose exponential is known exactly."""
+    from workloads import heat1d_matrix, heat2d_matrix
+    A = heat1d_matrix(nx) if dim == 1 else heat2d_matrix(nx)
+    op = flows.Operator(A, "action")
+    X = np.random.default_rng(nx).random((A.shape[0], 3))
+    ref = exact.heat_expm_closed_form(nx, t, dim) @ X
+    Y = op.apply(t, X)
+    assert np.abs(Y - ref).max() <= 1e-13 * np.abs(ref).max()

@@ -4,7 +4,7 @@ O=gpurun_out
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { tail -20 $O/build.log; exit 1; }
 timeout 1200 python -m pytest -x -q -m gpu "${@:-tests}" 2>&1 | tail -25
-timeout 300 python bench.py --no-cpu --no-variant --no-e2e --no-sparse > $O/bench_q.json 2> $O/bench_q.err; tail -3 $O/bench_q.err
+timeout 300 python bench.py --no-cpu --no-variant --no-e2e --no-sparse --no-pade > $O/bench_q.json 2> $O/bench_q.err; tail -3 $O/bench_q.err
 python - <<'PY'
 import json
 try:
