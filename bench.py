@@ -29,6 +29,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "split steps/sec & time-to-T, n=10000 DRE FP64"
 UNIT = "steps/s"
+# per-config run parameters (BASELINE.json configs, workloads.CONFIGS): step size,
+# the composition timed, quadrature rule, and the oracle's exponential route for cpu_baseline
+RUNS = {
+    1: dict(h=1e-3, scheme="lie", comp="F1F2", q=14, sp=1, method="auto"),
+    2: dict(h=0.005, scheme="strang", comp="F12", q=5, sp=4, method="auto"),
+    3: dict(h=0.005, scheme="strang", comp="F12F3", q=14, sp=1, method="action"),
+    4: dict(h=0.005, scheme="strang", comp="F12F3F4", q=14, sp=1, method="eigh"),
+    5: dict(h=0.005, scheme="strang", comp="F12F3", q=14, sp=1, method="auto"),
+    6: dict(h=0.005, scheme="strang", comp="F12F3", q=14, sp=1, method="auto"),
+}
 OZ_PAIRS = 36           # digit-slice pairs a + b <= 7 of the int8 E pass (ozaki.h, OZ_S = 8)
 FP64_PEAK_TFLOPS = 36.6   # measured DMMA microbenchmark on this pool's B200 (profiles/r01_peaks_fp64.json)
 H, NT, RANK_CAP = 0.005, 100, 64
@@ -111,38 +121,45 @@ def _dist():
 
 def workload_label(config: int, prob) -> str:
     """The workload string both arms print (BASELINE.json configs[4] for config 5)."""
+    r = RUNS[config]
     if config == 5:
         return (f"config5: DRE 2D heat n={prob.n} (n_x={int(round(prob.n ** 0.5))}), Strang F12F3, "
                 "rank cap 64, tol 1e-16 (refined compression), h=0.005 (T=0.5, N_t=100)")
-    return (f"config{config}: mass-matrix DRE (Example 4 structure, P1 FEM n={prob.n}), Strang F12F3, "
-            "rank cap 64, tol 1e-16 (refined compression), h=0.005 (T=0.5, N_t=100)")
+    if config == 6:
+        return (f"config6: mass-matrix DRE (Example 4 structure, P1 FEM n={prob.n}), Strang F12F3, "
+                "rank cap 64, tol 1e-16 (refined compression), h=0.005 (T=0.5, N_t=100)")
+    return (f"config{config}: {prob.meta['desc']} (n={prob.n}), {r['scheme']} {r['comp']}, "
+            f"rank cap 64, tol 1e-16, h={r['h']} (N_t=100), {r['q']}-node Gauss x {r['sp']} subpanels")
 
 
-def cpu_baseline(prob, steps: int, one_thread_steps: int = 0):
+def cpu_baseline(prob, steps: int, one_thread_steps: int = 0, config: int = 5):
     """The oracle (dense E_tau L products, SVD compression) timed on this host's cores: its init
     (closed-form heat exponential E_{h/2}, E_h; quadrature factor) timed separately, then `steps`
     Strang F12F3 steps; optionally a second sample of `one_thread_steps` steps with BLAS limited
     to one thread (threadpoolctl)."""
     from oracle.schemes import OracleOptions, OracleSolver
     cores = len(os.sched_getaffinity(0))
+    r = RUNS[config]
     t0 = time.perf_counter()
-    orc = OracleSolver(prob, H, OracleOptions(rank_cap=RANK_CAP), dense_apply=True)
-    orc.step("strang", "F12F3", 1)          # builds E_{h/2}, E_h and L_I(h/2), L_I(h): the init
+    orc = OracleSolver(prob, r["h"], OracleOptions(rank_cap=RANK_CAP, quad_nodes=r["q"],
+                                                   quad_subpanels=r["sp"]),
+                       method=r["method"], dense_apply=config == 5)
+    orc.step(r["scheme"], r["comp"], 1)     # builds E_{h/2}, E_h and L_I(h/2), L_I(h): the init
     t1 = time.perf_counter()
-    orc.step("strang", "F12F3", steps)
+    orc.step(r["scheme"], r["comp"], steps)
     t2 = time.perf_counter()
     out = {"value": steps / (t2 - t1), "unit": UNIT, "cores": cores, "kind": "oracle",
            "init_s": t1 - t0,
            "time_to_T_s_est": (t1 - t0) + NT * (t2 - t1) / steps,
-           "sample": f"{steps} Strang F12F3 steps of {prob.name} (n={prob.n}) after the init step "
-                     f"(init incl. one step {t1 - t0:.1f}s, timed separately: closed-form heat "
-                     "exponential, not a general expm); NumPy/OpenBLAS threads = all cores"}
+           "sample": f"{steps} {r['scheme']} {r['comp']} steps of {prob.name} (n={prob.n}) after the "
+                     f"init step (init incl. one step {t1 - t0:.1f}s, timed separately; oracle "
+                     f"exponential route '{r['method']}'); NumPy/OpenBLAS threads = all cores"}
     if one_thread_steps > 0:
         try:
             from threadpoolctl import threadpool_limits
             with threadpool_limits(limits=1):
                 t3 = time.perf_counter()
-                orc.step("strang", "F12F3", one_thread_steps)
+                orc.step(r["scheme"], r["comp"], one_thread_steps)
                 t4 = time.perf_counter()
             out["one_thread"] = {"value": one_thread_steps / (t4 - t3), "unit": UNIT, "cores": 1,
                                  "sample": f"{one_thread_steps} more steps, BLAS limited to 1 thread"}
@@ -151,13 +168,18 @@ def cpu_baseline(prob, steps: int, one_thread_steps: int = 0):
     return out
 
 
+def _problem(args):
+    from workloads import make_config
+    return make_config(args.config, nx=args.nx) if args.config != 1 else make_config(1)
+
+
 def run_reference(args):
     world, rank, _ = _dist()
     if rank != 0:
         return
     from workloads import make_config
-    prob = make_config(args.config, nx=args.nx)
-    cb = cpu_baseline(prob, max(1, args.steps))
+    prob = _problem(args)
+    cb = cpu_baseline(prob, max(1, args.steps), config=args.config)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "strong",
@@ -181,7 +203,8 @@ def run_ours(args):
     import paper_1805_08990_b200 as dme
     from workloads import make_config
 
-    prob = make_config(args.config, nx=args.nx)
+    prob = _problem(args)
+    R = RUNS[args.config]
     uid = None
     if world > 1:
         buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
@@ -189,7 +212,8 @@ def run_ours(args):
             buf.copy_(torch.frombuffer(bytearray(dme.unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, 0)
         uid = bytes(buf.cpu().numpy().tobytes())
-    kw = dict(h=H, rank_cap=RANK_CAP, world_size=world, world_rank=rank, nccl_uid=uid)
+    kw = dict(h=R["h"], rank_cap=RANK_CAP, world_size=world, world_rank=rank, nccl_uid=uid,
+              quad_nodes=R["q"], quad_subpanels=R["sp"])
 
     # ------------------------------------------------------------ device-resident timed region
     # A (800 MB) resident in HBM before the clock starts (options.big_inputs_on_device); the init
@@ -197,22 +221,25 @@ def run_ours(args):
     # P0 compression) is timed as part of time-to-T.
     # one tiny solve first: loads the library's kernels into the context (lazy module loading is a
     # once-per-process cost, not part of solving) and allocates the pinned rank record
-    tiny = make_config(args.config, nx=8)
-    _w = dme.Solver(**dme.problem_kwargs(tiny), h=H, rank_cap=RANK_CAP, world_size=1, world_rank=0)
-    _w.split_step("strang", "F12F3", 3)
+    tiny = make_config(args.config, nx=8) if args.config != 1 else make_config(1, n=64)
+    _w = dme.Solver(**dme.problem_kwargs(tiny), h=R["h"], rank_cap=RANK_CAP, world_size=1, world_rank=0,
+                    quad_nodes=R["q"], quad_subpanels=R["sp"])
+    _w.split_step(R["scheme"], R["comp"], 3)
     _w.close()
     del _w
     A_dev = torch.from_numpy(prob.A).cuda()
     kw_dev = dict(dme.problem_kwargs(prob), A=A_dev)
     if prob.M is not None:  # the mass matrix lives with A (device-resident too)
         kw_dev["M"] = torch.from_numpy(prob.M).cuda()
+    if prob.S is not None:  # so does S (config 4)
+        kw_dev["S"] = torch.from_numpy(prob.S).cuda()
     torch.cuda.synchronize()
     t_init0 = time.perf_counter()
     s = dme.Solver(**kw_dev, **kw)
     torch.cuda.synchronize()
     init_wall = time.perf_counter() - t_init0
     del A_dev, kw_dev
-    s.split_step("strang", "F12F3", args.warmup)
+    s.split_step(R["scheme"], R["comp"], args.warmup)
     torch.cuda.synchronize()
     launches0 = s.stats()["kernel_launches"]
     stream = s.stream
@@ -224,7 +251,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        s.split_step("strang", "F12F3", args.steps)
+        s.split_step(R["scheme"], R["comp"], args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -241,7 +268,7 @@ def run_ours(args):
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     p0.record(stream)
-    s.split_step("strang", "F12F3", args.steps)
+    s.split_step(R["scheme"], R["comp"], args.steps)
     p1.record(stream)
     torch.cuda.synchronize()
     ms_prof = p0.elapsed_time(p1)
@@ -323,7 +350,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s2 = dme.Solver(**kw_host, **kw)                            # H2D of A, C, B, R, L0
-        s2.split_step("strang", "F12F3", NT)
+        s2.split_step(R["scheme"], R["comp"], NT)
         L, D = s2.get_factor()                                      # D2H of the factor
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
@@ -341,19 +368,19 @@ def run_ours(args):
 
     # ------------------------------------------------------------ native-FP64 (DMMA) variant
     variant = None
-    if not args.no_variant:
+    if not args.no_variant and args.config == 5:
         torch.cuda.synchronize()
         t3 = time.perf_counter()
         s3 = dme.Solver(**dme.problem_kwargs(prob), **kw, e_pass="dmma")
         torch.cuda.synchronize()
         init3 = time.perf_counter() - t3
-        s3.split_step("strang", "F12F3", args.warmup)
+        s3.split_step(R["scheme"], R["comp"], args.warmup)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         v0.record(s3.stream)
-        s3.split_step("strang", "F12F3", args.steps)
+        s3.split_step(R["scheme"], R["comp"], args.steps)
         v1.record(s3.stream)
         torch.cuda.synchronize()
         ms3 = v0.elapsed_time(v1)
@@ -380,13 +407,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         init6 = time.perf_counter() - t6
         del A_dev, kw_p
-        s6.split_step("strang", "F12F3", args.warmup)
+        s6.split_step(R["scheme"], R["comp"], args.warmup)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         v0.record(s6.stream)
-        s6.split_step("strang", "F12F3", args.steps)
+        s6.split_step(R["scheme"], R["comp"], args.steps)
         v1.record(s6.stream)
         torch.cuda.synchronize()
         ms6 = v0.elapsed_time(v1)
@@ -413,7 +440,7 @@ def run_ours(args):
         A_csr = sps.csr_matrix(prob.A)  # host CSR (the caller's sparse matrix)
         kw_sp = dict(dme.problem_kwargs(prob), A=A_csr)
         # tiny sparse solve first (kernel modules of this path loaded, as for the dense line)
-        _w = dme.Solver(**dict(dme.problem_kwargs(tiny), A=sps.csr_matrix(tiny.A)), h=H,
+        _w = dme.Solver(**dict(dme.problem_kwargs(tiny), A=sps.csr_matrix(tiny.A)), h=R["h"],
                         rank_cap=RANK_CAP)
         _w.split_step("strang", "F12F3", 3)
         _w.close()
@@ -465,11 +492,11 @@ def run_ours(args):
                          "d2h_bytes_per_step": (L5.nbytes + D5.nbytes) / NT}
 
     cb = None
-    if args.config != 5:  # the oracle's dense E for a nonsymmetric A M^-1 takes minutes: not a bounded sample
-        cb = {"skipped": "cpu_baseline is reported for the headline workload (config 5) only"}
+    if args.config in (4, 6):  # oracle init: dense eigh / expm of n = 4900: not a bounded sample
+        cb = {"skipped": "cpu_baseline: the oracle's init at this config takes minutes"}
     elif rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cb = cpu_baseline(prob, 10, one_thread_steps=3)
+            cb = cpu_baseline(prob, 10, one_thread_steps=3, config=args.config)
         except Exception as ex:  # reported, never fatal
             cb = {"error": repr(ex)}
 
@@ -509,17 +536,18 @@ def main():
     ap.add_argument("--steps", type=int, default=100)  # = N_t of config 5
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=5, choices=[5, 6],
-                    help="5 (default, BASELINE.json's headline) or 6 (mass-matrix DRE, SURVEY f3)")
-    ap.add_argument("--nx", type=int, default=None, help="grid size (default: 100 for 5, 70 for 6)")
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5, 6],
+                    help="5 (default, BASELINE.json's headline), 1-4 (BASELINE.json's other configs) "
+                         "or 6 (mass-matrix DRE, SURVEY f3)")
+    ap.add_argument("--nx", type=int, default=None, help="grid size (default: the config's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variant", action="store_true", help="skip the native-FP64 E-pass run")
     ap.add_argument("--no-sparse", action="store_true", help="skip the sparse-A (Chebyshev) run")
     ap.add_argument("--no-pade", action="store_true", help="skip the Padé-13 init run")
     args = ap.parse_args()
-    if args.nx is None:
-        args.nx = 100 if args.config == 5 else 70
+    if args.nx is None and args.config == 6:
+        args.nx = 70
     if args.impl == "reference":
         run_reference(args)
     else:
