@@ -433,6 +433,31 @@ def run_ours(args):
         del s6
         torch.cuda.empty_cache()
 
+    # ------------------------------------------------------------ CSR S variant (config 4: T4 products)
+    sparse_s = None
+    if args.config == 4 and prob.S is not None:
+        import scipy.sparse as sps
+        kw_s = dict(dme.problem_kwargs(prob), S=sps.csr_matrix(prob.S))
+        torch.cuda.synchronize()
+        t7 = time.perf_counter()
+        s7 = dme.Solver(**kw_s, **kw)
+        torch.cuda.synchronize()
+        init7 = time.perf_counter() - t7
+        s7.split_step(R["scheme"], R["comp"], args.warmup)
+        torch.cuda.synchronize()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(s7.stream)
+        s7.split_step(R["scheme"], R["comp"], args.steps)
+        v1.record(s7.stream)
+        torch.cuda.synchronize()
+        ms7 = v0.elapsed_time(v1)
+        sparse_s = {"S": f"CSR ({sps.csr_matrix(prob.S).nnz} nonzeros: the diagonal Robin-edge S of "
+                         "reading G18) instead of the dense n x n S",
+                    "value": args.steps / (ms7 * 1e-3), "unit": UNIT, "ms_per_step": ms7 / args.steps,
+                    "init_s_from_host": init7, "time_to_T_s": init7 + NT * ms7 / args.steps * 1e-3}
+        s7.close()
+        del s7
+
     # ------------------------------------------------------------ sparse-A variant
     sparse = None
     if not args.no_sparse and args.config == 5 and world == 1:
@@ -523,7 +548,8 @@ def run_ours(args):
                 "init_s": init_wall, "init_lib_s": init_dev,
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(),
-                "fp64_dmma_variant": variant, "pade_variant": pade, "sparse_variant": sparse}
+                "fp64_dmma_variant": variant, "pade_variant": pade, "sparse_variant": sparse,
+                "sparse_S_variant": sparse_s}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

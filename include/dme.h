@@ -108,6 +108,15 @@ typedef struct {
   const int64_t* A_rowptr; /* n + 1 */
   const int32_t* A_colind; /* A_nnz */
   const double* A_values;  /* A_nnz */
+  /* Sparse S (SURVEY / VERDICT r1 item 10; "S sparse"): used when S == NULL and
+     S_rowptr != NULL. S in CSR form (host arrays, 0-based, row-major; duplicates summed), finite
+     values. The T4 flow's S L and S (S L) products are then CSR x skinny products on the GPU
+     (replicated on every rank, no collective) instead of two 8 n^2-byte streams of a dense S.
+     Callers that zero-initialise the struct get S_rowptr = NULL.                           */
+  int64_t S_nnz;
+  const int64_t* S_rowptr; /* n + 1 */
+  const int32_t* S_colind; /* S_nnz */
+  const double* S_values;  /* S_nnz */
 } dme_problem;
 
 typedef struct {

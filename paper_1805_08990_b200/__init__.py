@@ -39,7 +39,9 @@ class _Problem(ctypes.Structure):
                 ("m", ctypes.c_int64), ("B", _dp), ("R", _dp), ("S", _dp),
                 ("r0", ctypes.c_int64), ("L0", _dp), ("D0", _dp), ("M", _dp),
                 ("A_nnz", ctypes.c_int64), ("A_rowptr", ctypes.POINTER(ctypes.c_int64)),
-                ("A_colind", ctypes.POINTER(ctypes.c_int32)), ("A_values", _dp)]
+                ("A_colind", ctypes.POINTER(ctypes.c_int32)), ("A_values", _dp),
+                ("S_nnz", ctypes.c_int64), ("S_rowptr", ctypes.POINTER(ctypes.c_int64)),
+                ("S_colind", ctypes.POINTER(ctypes.c_int32)), ("S_values", _dp)]
 
 
 class _Options(ctypes.Structure):
@@ -192,6 +194,13 @@ class Solver:
         # A and S may be CUDA tensors (float64, contiguous): then they are read device-to-device
         on_dev = isinstance(A, torch.Tensor) and A.is_cuda
         sparse = _is_sparse(A)
+        self._csrS = None
+        if _is_sparse(S):  # CSR S (T4 by sparse x skinny products); host arrays
+            cs = S.tocsr()
+            self._csrS = (np.ascontiguousarray(cs.indptr, dtype=np.int64),
+                          np.ascontiguousarray(cs.indices, dtype=np.int32),
+                          np.ascontiguousarray(cs.data, dtype=np.float64))
+            S = None
         if sparse:  # CSR host arrays; the library builds its device layout from them
             csr = A.tocsr()
             self._csr = (np.ascontiguousarray(csr.indptr, dtype=np.int64),
@@ -222,6 +231,12 @@ class Solver:
         pr = _Problem(n=n, A=pA, p=0 if C_ is None else C_.shape[0], C=_ptr(C_),
                       m=0 if B_ is None else B_.shape[1], B=_ptr(B_), R=_ptr(R_), S=pS,
                       r0=0 if L0_ is None else L0_.shape[1], L0=_ptr(L0_), D0=_ptr(D0_), M=pM)
+        if self._csrS is not None:
+            rp, ci, vv = self._csrS
+            pr.S_nnz = vv.size
+            pr.S_rowptr = rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+            pr.S_colind = ci.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            pr.S_values = _ptr(vv)
         if sparse:
             rp, ci, vv = self._csr
             pr.A_nnz = vv.size

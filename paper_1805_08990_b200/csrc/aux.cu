@@ -573,4 +573,32 @@ void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, doub
   DME_KCHECK();
 }
 
+namespace {
+// thread per (row, column): consecutive threads take consecutive rows of one column (coalesced
+// stores; the gathers of a banded / diagonal S stay within a few sectors)
+__global__ void spmm_csr_kernel(const int* __restrict__ rp, const int* __restrict__ ci,
+                                const double* __restrict__ v, int64_t n, const double* __restrict__ X,
+                                int64_t ldx, int64_t k, double* __restrict__ out, int64_t ldo,
+                                double alpha) {
+  const int64_t total = n * k;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / n, i = t - j * n;
+    const double* xj = X + j * ldx;
+    double acc = 0.0;
+    for (int e = rp[i]; e < rp[i + 1]; ++e) acc = fma(v[e], xj[ci[e]], acc);
+    out[i + j * ldo] = alpha * acc;
+  }
+}
+}  // namespace
+
+void spmm_csr(const int* rp, const int* ci, const double* v, int64_t n, const double* X, int64_t ldx,
+              int64_t k, double* out, int64_t ldo, double alpha, cudaStream_t st) {
+  if (n <= 0 || k <= 0) return;
+  const int64_t total = n * k;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+  spmm_csr_kernel<<<blocks, 256, 0, st>>>(rp, ci, v, n, X, ldx, k, out, ldo, alpha);
+  DME_KCHECK();
+}
+
 }  // namespace dme

@@ -27,6 +27,10 @@ void copy_cols(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t
 // dst (rows x cols column-major) <- src (rows x cols row-major)
 void rowmajor_to_colmajor(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
                           int64_t cols, cudaStream_t st);
+// out[:, j] = alpha * S X[:, j] (j < k) for a CSR S (n rows, int32 row pointers / column indices);
+// X, out column-major with leading dimensions ldx / ldo (out != X)
+void spmm_csr(const int* rp, const int* ci, const double* v, int64_t n, const double* X, int64_t ldx,
+              int64_t k, double* out, int64_t ldo, double alpha, cudaStream_t st);
 // C = A * B, A: M x K column-major, B: K x N column-major (small K, N), C: column-major
 void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                 int64_t M, int64_t N, int64_t K, cudaStream_t st);

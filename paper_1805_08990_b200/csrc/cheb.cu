@@ -108,6 +108,9 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_THRE
     }
   };
   const double alpha = p.alpha, beta = p.beta;
+  // every CTA of the cluster has started (and initialised its shared memory) before any peer
+  // pushes into it (compute-sanitizer racecheck: DSMEM store into a block not yet entered)
+  cluster_sync_all();
   for (int sub = 0; sub < p.substeps; ++sub) {
     if (sub > 0) {  // v_0 of the next substep = y (own rows)
       for (int e = tid; e < C * R; e += CHEB_THREADS) {
@@ -252,6 +255,7 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
       e[u][q] = in ? idx_s[q * R + i] : 0u;
     }
   }
+  cluster_sync_all();  // all CTAs of the cluster running before the first DSMEM push (racecheck)
   for (int sub = 0; sub < p.substeps; ++sub) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {

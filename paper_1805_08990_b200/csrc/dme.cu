@@ -108,6 +108,10 @@ struct Planner {
 struct dme_ctx {
   int64_t n = 0, ldn = 0, p = 0, m = 0, r0 = 0;
   bool has_S = false, dre = false;
+  bool sparse_S = false;   // S given in CSR form: T4 products by spmm_csr (aux.h)
+  int64_t S_nnz = 0;
+  int *S_rp = nullptr, *S_ci = nullptr;
+  double* S_v = nullptr;
   int world = 1, rank = 0;  // logical shards of E's rows (= ranks, or virtual shards) and this rank
   int64_t nloc = 0, row0 = 0, rows_loc = 0;
   // shards computed by this process: real multi-rank: {rank}; options.virtual_world = G on one GPU:
@@ -214,7 +218,12 @@ void plan_buffers(dme_ctx* c, Planner& P) {
     c->cop.rptr = P.take<uint32_t>(std::max<size_t>(c->chost.rptr.size(), 1));
     c->cop.rent = P.take<uint32_t>(std::max<size_t>(c->chost.rent.size(), 1));
   }
-  if (c->has_S) c->S = P.take<double>(nn);
+  if (c->has_S && !c->sparse_S) c->S = P.take<double>(nn);
+  if (c->sparse_S) {
+    c->S_rp = P.take<int>((size_t)n + 1);
+    c->S_ci = P.take<int>((size_t)std::max<int64_t>(c->S_nnz, 1));
+    c->S_v = P.take<double>((size_t)std::max<int64_t>(c->S_nnz, 1));
+  }
   c->Bcol = P.take<double>((size_t)ld * std::max<int64_t>(c->m, 1));
   c->LQ = P.take<double>((size_t)ld * std::max<int64_t>(c->p, 1));
   c->Zc12h = P.take<double>(fk);
@@ -393,7 +402,9 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->p = pr->p;
   c->m = pr->m;
   c->r0 = pr->r0;
-  c->has_S = pr->S != nullptr;
+  c->sparse_S = pr->S == nullptr && pr->S_rowptr != nullptr;
+  c->has_S = pr->S != nullptr || c->sparse_S;
+  c->S_nnz = c->sparse_S ? pr->S_nnz : 0;
   c->opt = *o;
   c->world = o->world_size > 0 ? o->world_size : 1;
   c->rank = o->world_rank;
@@ -466,8 +477,21 @@ void validate(const dme_problem* pr, const dme_options* o, bool dre) {
   // input finiteness (host scan; inputs are host arrays)
   const size_t nn = (size_t)pr->n * pr->n;
   (void)nn;  // A and S (n x n) are checked on the device after the upload (init_all)
-  DME_REQUIRE(!(pr->M && pr->S), DME_ERR_CONFIG,
+  DME_REQUIRE(!(pr->M && (pr->S || pr->S_rowptr)), DME_ERR_CONFIG,
               "a mass matrix M together with the bilinear term S is not supported");
+  if (!pr->S && pr->S_rowptr) {  // CSR S: structure and values on the host
+    const int64_t n = pr->n;
+    DME_REQUIRE(pr->S_nnz >= 0 && pr->S_nnz < (int64_t)1 << 31 && (pr->S_nnz == 0 || (pr->S_colind && pr->S_values)),
+                DME_ERR_INVALID, "CSR S: bad nnz or NULL arrays");
+    DME_REQUIRE(pr->S_rowptr[0] == 0 && pr->S_rowptr[n] == pr->S_nnz, DME_ERR_INVALID,
+                "CSR S: row pointers must start at 0 and end at S_nnz");
+    for (int64_t i = 0; i < n; ++i)
+      DME_REQUIRE(pr->S_rowptr[i + 1] >= pr->S_rowptr[i], DME_ERR_INVALID, "CSR S: decreasing row pointers");
+    for (int64_t e = 0; e < pr->S_nnz; ++e) {
+      DME_REQUIRE(pr->S_colind[e] >= 0 && pr->S_colind[e] < n, DME_ERR_INVALID, "CSR S: column index out of range");
+      DME_REQUIRE(std::isfinite(pr->S_values[e]), DME_ERR_INVALID, "CSR S: non-finite value");
+    }
+  }
   if (pr->p) DME_REQUIRE(all_finite(pr->C, (size_t)pr->p * pr->n), DME_ERR_INVALID, "C non-finite");
   if (pr->r0) DME_REQUIRE(all_finite(pr->L0, (size_t)pr->n * pr->r0), DME_ERR_INVALID, "L0 non-finite");
   if (pr->m) {
@@ -985,14 +1009,26 @@ void flow_T3(dme_ctx* c, double tau) {
   swapZ(c);
 }
 
+// out = alpha S X for the bilinear flow: the dense S through the E-pass GEMM (row-sharded like E),
+// or the CSR S by a sparse x skinny product (every rank all rows: n nnz-sized work, no collective)
+void s_pass(dme_ctx* c, const double* X, int64_t k, double* out, int64_t ldo, double alpha) {
+  if (k <= 0) return;
+  if (!c->sparse_S) {
+    epass(c, c->S, X, k, out, ldo, alpha);
+    return;
+  }
+  ProfScope ps(c, PROF_EPASS, 2.0 * c->S_nnz * k, 12.0 * c->S_nnz + 16.0 * c->n * k, c->st);
+  spmm_csr(c->S_rp, c->S_ci, c->S_v, c->n, X, c->ldn, k, out, ldo, alpha, c->st);
+}
+
 void flow_T4(dme_ctx* c, double tau, int order, bool t3, double tau3) {
   if (c->r == 0) return;
   const int64_t r = c->r, ld = c->ldn;
   copy_cols(c->Zc2, ld, c->Z, ld, c->n, r, 1.0, c->st);
-  epass(c, c->S, c->Z, r, c->Zc2 + r * ld, ld, std::sqrt(tau));                  // sqrt(tau) S L
+  s_pass(c, c->Z, r, c->Zc2 + r * ld, ld, std::sqrt(tau));                         // sqrt(tau) S L
   int64_t k = 2 * r;
   if (order == 2) {                                                                 // tau/sqrt2 S^2 L
-    epass(c, c->S, c->Zc2 + r * ld, r, c->Zc2 + 2 * r * ld, ld, std::sqrt(tau) / std::sqrt(2.0));
+    s_pass(c, c->Zc2 + r * ld, r, c->Zc2 + 2 * r * ld, ld, std::sqrt(tau) / std::sqrt(2.0));
     k = 3 * r;
   }
   finish_compress(c, c->Zc2, k, t3, tau3);
@@ -1237,8 +1273,19 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   } else {
     DME_CUDA(cudaMemcpy2DAsync(c->Aup, ld * 8, pr->A, n * 8, n * 8, n, kbig, st));
   }
-  if (c->has_S)
+  if (c->has_S && !c->sparse_S)
     DME_CUDA(cudaMemcpy2DAsync(c->S, ld * 8, pr->S, n * 8, n * 8, n, kbig, st));
+  if (c->sparse_S) {  // (validated on the host: indices in range, finite values)
+    std::vector<int> rp32(n + 1), ci32(std::max<int64_t>(c->S_nnz, 1));
+    for (int64_t i = 0; i <= n; ++i) rp32[i] = (int)pr->S_rowptr[i];
+    for (int64_t e = 0; e < c->S_nnz; ++e) ci32[e] = pr->S_colind[e];
+    DME_CUDA(cudaMemcpyAsync(c->S_rp, rp32.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (c->S_nnz > 0) {
+      DME_CUDA(cudaMemcpyAsync(c->S_ci, ci32.data(), c->S_nnz * sizeof(int), cudaMemcpyHostToDevice, st));
+      DME_CUDA(cudaMemcpyAsync(c->S_v, pr->S_values, c->S_nnz * 8, cudaMemcpyHostToDevice, st));
+    }
+    sync(c);  // (the pageable staging vectors die here)
+  }
   // mass matrix (Example 4): A <- A M^-1, C <- C M^-1 by a dense LU of M
   const bool mass = pr->M != nullptr;
   if (mass) {
@@ -1268,7 +1315,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
     DME_CUDA(cudaMemsetAsync(c->r_dev, 0, 4 * sizeof(int), st));
     if (!c->sparse)  // (a sparse A was validated on the host by cheb_prepare)
       check_square(c->Aup, n, ld, c->r_dev, st);         // r_dev[0]: non-finite, r_dev[1]: asymmetric
-    if (c->has_S) check_square(c->S, n, ld, c->r_dev + 2, st);
+    if (c->has_S && !c->sparse_S) check_square(c->S, n, ld, c->r_dev + 2, st);
     DME_CUDA(cudaMemcpyAsync(flags_host, c->r_dev, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     sync(c);
     DME_REQUIRE(flags_host[0] == 0, DME_ERR_INVALID, "A has non-finite entries");

@@ -124,8 +124,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
         cnt_s[tid] = sturm_count(d, e2, k, a0 + (b0 - a0) * (t + 1) / (P + 1.0));
       }
       __syncthreads();
+      double a0 = 0.0, b0 = 0.0;
+      if (act) { a0 = lo_s[grp]; b0 = hi_s[grp]; }
+      __syncthreads();  // every thread has read the bracket before the transition thread moves it
       if (act) {  // transition between probe t and t+1 (counts are monotone in the probe position)
-        const double a0 = lo_s[grp], b0 = hi_s[grp];
         const bool le = cnt_s[tid] <= jj;
         const bool nxt = (t + 1 < P) ? (cnt_s[tid + 1] <= jj) : false;
         if (le && !nxt) {

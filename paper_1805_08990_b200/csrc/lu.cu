@@ -418,7 +418,7 @@ void lu_solve_right(double* Q, double* P, int64_t n, int64_t ld, double* QT, dou
   col_scatter_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 64), (unsigned)n), 256, 0, st>>>(
       P, QT, n, ld, perm);
   DME_KCHECK();
-  DME_CUDA(cudaMemcpyAsync(P, QT, (size_t)n * ld * 8, cudaMemcpyDeviceToDevice, st));
+  DME_CUDA(cudaMemcpy2DAsync(P, ld * 8, QT, ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, st));
 }
 
 }  // namespace dme

@@ -369,8 +369,9 @@ __global__ void __launch_bounds__(NT) tail_assemble_kernel(SmallArgs a, const do
   constexpr int NWP = NT / 32;
   for (int c = warp; c < kb; c += NWP)
     for (int i = lane; i < k; i += 32) Ts[i + c * k] = a.Tm[i + (size_t)c * a.ldt];
-  for (int c = warp; c < m; c += NWP)
-    for (int i = lane; i < k; i += 32) Hs[i + c * k] = a.H[i + (size_t)c * a.ldh];
+  if (a.t3)  // (H = Zc^T B is only formed when T3 is fused)
+    for (int c = warp; c < m; c += NWP)
+      for (int i = lane; i < k; i += 32) Hs[i + c * k] = a.H[i + (size_t)c * a.ldh];
   for (int c = warp; c < s; c += NWP)
     for (int i = lane; i < k; i += 32) Us[i + c * k] = U[i + (size_t)c * ldu];
   for (int c = warp; c < ks; c += NWP)
