@@ -97,9 +97,11 @@ typedef struct {
      polynomial in the sparse A, no dense matrix exponential). Used when A == NULL and
      A_rowptr != NULL: A in CSR form (host arrays, 0-based, row-major: row i holds entries
      A_colind[e], A_values[e] for e in [A_rowptr[i], A_rowptr[i+1]); duplicates are summed).
-     A must be exactly symmetric (DME_ERR_CONFIG otherwise). Every E_tau L action is then a
-     Chebyshev expansion of exp on the Gershgorin interval of tau A^T (truncation tail <= 2^-56,
-     degree fixed at init), the quadrature rule is unchanged (its panel count
+     Every E_tau L action is then, for an exactly symmetric A, a Chebyshev expansion of exp on the
+     Gershgorin interval of tau A^T (truncation tail <= 2^-56, degree fixed at init; DME_ERR_CONFIG
+     when the Gershgorin bound is too loose for it), and for a nonsymmetric A the
+     truncated Taylor series with scaling of Al-Mohy & Higham (cheb.h; degree m <= 55 and s substeps
+     from ||tau (A^T - mu I)||), evaluated by the same cluster kernels; the quadrature rule is unchanged (its panel count
      still comes from ||(h/2) A^T||_1), and init builds no n x n matrix. n x (row width) must fit
      the shared memory of one 8-CTA cluster (DME_ERR_DIM otherwise; n = 10^4 with a 5-point
      stencil fits). Not combinable with M or with world_size > 1 (DME_ERR_CONFIG).

@@ -26,6 +26,16 @@ namespace dme {
 
 namespace {
 
+constexpr int TAYLOR_MMAX = 55;
+// theta_m of Al-Mohy & Higham (2011), Table 3.1 / Higham (2008) Table A.3, unit roundoff 2^-53
+constexpr int TAYLOR_NM = 35;
+const int TAYLOR_M[TAYLOR_NM] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
+                                 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 35, 40, 45, 50, 55};
+const double TAYLOR_THETA[TAYLOR_NM] = {
+    2.29e-16, 2.58e-8, 1.39e-5, 3.40e-4, 2.40e-3, 9.07e-3, 2.38e-2, 5.00e-2, 8.96e-2, 1.44e-1,
+    2.14e-1, 3.00e-1, 4.00e-1, 5.14e-1, 6.41e-1, 7.81e-1, 9.31e-1, 1.09, 1.26, 1.44,
+    1.62, 1.82, 2.01, 2.22, 2.43, 2.64, 2.86, 3.08, 3.31, 3.54, 4.7, 6.0, 7.2, 8.5, 9.9};
+
 struct ChebParams {
   const double* val;
   const uint32_t* idx;
@@ -38,6 +48,9 @@ struct ChebParams {
   int R, w, H, P, k, K, substeps;
   double alpha, beta, out_scale;
   double coef[CHEB_KMAX + 1];  // coef_k = e^{c + gamma} chat_k (k ? 2 : 1), one substep
+  // Taylor mode (nonsymmetric A): v_k = (alpha A^T v_{k-1} - beta v_{k-1}) / k, y += coef_k v_k
+  int taylor;
+  double rk[TAYLOR_MMAX + 1];  // 1 / k
 };
 
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
@@ -156,7 +169,7 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_THRE
 #pragma unroll
         for (int j = 0; j < C; ++j) {
           const double t = alpha * acc[j] - beta * bc[j * LD + i];
-          const double vn = kd == 1 ? t : 2.0 * t - bp[j * LD + i];
+          const double vn = p.taylor ? t * p.rk[kd] : (kd == 1 ? t : 2.0 * t - bp[j * LD + i]);
           bp[j * LD + i] = vn;
           y_s[j * R + i] = fma(ck, vn, y_s[j * R + i]);
         }
@@ -303,7 +316,7 @@ __global__ void __cluster_dims__(CHEB_CLUSTER, 1, 1) __launch_bounds__(CHEB_REG_
 #pragma unroll
           for (int q = 0; q < W; ++q) acc = fma(am[q], bc[j * LD + em[q]], acc);
           const double t = alpha * acc - beta * vc[u][j];
-          const double vn = kd == 1 ? t : 2.0 * t - vp[u][j];
+          const double vn = p.taylor ? t * p.rk[kd] : (kd == 1 ? t : 2.0 * t - vp[u][j]);
           vp[u][j] = vc[u][j];
           vc[u][j] = vn;
           y[u][j] = fma(ck, vn, y[u][j]);
@@ -535,15 +548,17 @@ int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* c
   std::vector<std::vector<std::pair<int32_t, double>>> rowsT(n);
   std::vector<std::pair<int32_t, double>> ra;
   int w = 1;
-  double a = INFINITY, b = -INFINITY, norm1 = 0.0;
+  double a = INFINITY, b = -INFINITY, norm1 = 0.0, trace = 0.0;
+  out.sym = true;
   for (int64_t i = 0; i < n; ++i) {
     canon(tp.data(), tc.data(), tv.data(), i, rowsT[i]);
     canon(rowptr, colind, values, i, ra);
-    if (ra.size() != rowsT[i].size())
-      return fail(DME_ERR_CONFIG, "sparse A must be symmetric (Chebyshev on the Gershgorin interval)");
-    for (size_t e = 0; e < ra.size(); ++e)
-      if (ra[e].first != rowsT[i][e].first || ra[e].second != rowsT[i][e].second)
-        return fail(DME_ERR_CONFIG, "sparse A must be symmetric (Chebyshev on the Gershgorin interval)");
+    bool same = ra.size() == rowsT[i].size();
+    for (size_t e = 0; same && e < ra.size(); ++e)
+      same = ra[e].first == rowsT[i][e].first && ra[e].second == rowsT[i][e].second;
+    if (!same) out.sym = false;
+    for (auto& x : ra)
+      if (x.first == i) trace += x.second;
     double diag = 0.0, off = 0.0, rs = 0.0;
     for (auto& x : rowsT[i]) {
       if (x.first == i) diag += x.second;
@@ -583,6 +598,27 @@ int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* c
   for (auto& r : rowsT) out.nnz += (int64_t)r.size();
   out.n = n; out.R = R; out.w = w; out.H = H; out.P = P; out.C = C;
   out.a = a; out.b = b; out.norm1 = norm1;
+  // shifted norms for the Taylor route: max(||A^T - mu I||_1, ||A^T - mu I||_inf), mu = trace / n
+  out.mu = trace / n;
+  {
+    double rmax = 0.0;  // rows of A^T
+    std::vector<double> csum(n, 0.0);  // columns of A^T = rows of A
+    for (int64_t i = 0; i < n; ++i) {
+      double rs = 0.0;
+      bool dg = false;
+      for (auto& x : rowsT[i]) {
+        const double v = x.second - (x.first == i ? out.mu : 0.0);
+        dg = dg || x.first == i;
+        rs += std::fabs(v);
+        csum[x.first] += std::fabs(v);
+      }
+      if (!dg) { rs += std::fabs(out.mu); csum[i] += std::fabs(out.mu); }
+      rmax = std::max(rmax, rs);
+    }
+    double cmax = 0.0;
+    for (double v : csum) cmax = std::max(cmax, v);
+    out.tnorm = std::max(rmax, cmax);
+  }
   const int64_t ldm = (int64_t)CHEB_CLUSTER * R;
   out.val.assign((size_t)w * ldm, 0.0);
   out.idx.assign((size_t)w * ldm, 0u);
@@ -650,27 +686,49 @@ int cheb_action(const ChebOp& op, double tau, const double* X, int64_t ldx, int6
   preload_all();
   ChebParams prm;
   std::memset(&prm, 0, sizeof(prm));
-  // interval of tau A^T (tau > 0): [tau a, tau b]; substeps keep the degree within CHEB_KMAX
-  std::vector<double> chat;
   int substeps = 1, K = 0;
   double c = 0, gamma = 0;
-  for (;;) {
-    const double ts = tau / substeps;
-    c = ts * (op.a + op.b) / 2;
-    gamma = ts * (op.b - op.a) / 2;
-    K = cheb_coeffs(gamma, 0x1p-56, chat);
-    if (K <= CHEB_KMAX) break;
-    substeps *= 2;
+  if (op.sym) {
+    // interval of tau A^T (tau > 0): [tau a, tau b]; substeps keep the degree within CHEB_KMAX
+    std::vector<double> chat;
+    for (;;) {
+      const double ts = tau / substeps;
+      c = ts * (op.a + op.b) / 2;
+      gamma = ts * (op.b - op.a) / 2;
+      K = cheb_coeffs(gamma, 0x1p-56, chat);
+      if (K <= CHEB_KMAX) break;
+      substeps *= 2;
+    }
+    const double scale = std::exp(c + gamma);
+    for (int j = 0; j <= K; ++j) prm.coef[j] = scale * chat[j] * (j ? 2.0 : 1.0);
+  } else {
+    // truncated Taylor with scaling (Al-Mohy & Higham 2011): the cheapest m s with
+    // s >= tau ||A^T - mu I|| / theta_m
+    const double tn = tau * op.tnorm;
+    int64_t best = INT64_MAX;
+    for (int q = 0; q < TAYLOR_NM; ++q) {
+      const int m = TAYLOR_M[q];
+      const int64_t s = std::max<int64_t>(1, (int64_t)std::ceil(tn / TAYLOR_THETA[q]));
+      if ((int64_t)m * s < best) { best = (int64_t)m * s; K = m; substeps = (int)s; }
+    }
+    const double ts = tau / substeps, eta = std::exp(ts * op.mu);
+    for (int j = 0; j <= K; ++j) {
+      prm.coef[j] = eta;
+      prm.rk[j] = j ? 1.0 / j : 1.0;
+    }
+    prm.taylor = 1;
+    prm.alpha = ts;
+    prm.beta = ts * op.mu;
   }
-  const double scale = std::exp(c + gamma);
-  for (int j = 0; j <= K; ++j) prm.coef[j] = scale * chat[j] * (j ? 2.0 : 1.0);
   prm.val = op.val; prm.idx = op.idx; prm.push = op.push; prm.rptr = op.rptr; prm.rent = op.rent;
   prm.X = X; prm.out = out;
   prm.ldx = ldx; prm.ldo = ldo; prm.n = op.n;
   prm.R = (int)op.R; prm.w = op.w; prm.H = op.H; prm.P = op.P;
   prm.k = (int)k; prm.K = K; prm.substeps = substeps;
-  prm.alpha = gamma > 0 ? (tau / substeps) / gamma : 0.0;
-  prm.beta = gamma > 0 ? c / gamma : 0.0;
+  if (op.sym) {
+    prm.alpha = gamma > 0 ? (tau / substeps) / gamma : 0.0;
+    prm.beta = gamma > 0 ? c / gamma : 0.0;
+  }
   prm.out_scale = alpha;
   // columns per cluster: the smallest C whose ceil(k / C) clusters are co-resident in one wave
   // (cudaOccupancyMaxActiveClusters: clusters are placed within a GPC, 15 x 8 CTAs on a B200 at

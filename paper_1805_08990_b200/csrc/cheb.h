@@ -39,6 +39,8 @@ struct ChebOp {
   int C = 0;              // max columns per cluster (shared-memory budget)
   double a = 0, b = 0;    // Gershgorin interval of A^T
   double norm1 = 0;       // ||A^T||_1
+  bool sym = true;        // A == A^T: Chebyshev on [a, b]; otherwise truncated Taylor (below)
+  double mu = 0, tnorm = 0;  // trace(A)/n and max(||A^T - mu I||_1, ||A^T - mu I||_inf)
   double* val = nullptr;    // [w][CHEB_CLUSTER * R] (device)
   uint32_t* idx = nullptr;  // [w][CHEB_CLUSTER * R]: local index into [0, R + H) (own row or halo slot)
   uint32_t* push = nullptr; // [CHEB_CLUSTER][P][2]: (own row, (dest CTA << 24) | dest slot), ~0 = none
@@ -53,6 +55,8 @@ struct ChebHost {
   int64_t n = 0, R = 0, nnz = 0;  // nnz: stored entries of A^T (duplicates merged)
   int w = 0, H = 0, P = 0, C = 0;
   double a = 0, b = 0, norm1 = 0;
+  bool sym = true;
+  double mu = 0, tnorm = 0;
   std::vector<double> val;
   std::vector<uint32_t> idx, push, rptr, rent;
 };
@@ -72,6 +76,11 @@ int cheb_csr_from_dense(const double* A, int64_t n, int64_t ld, int64_t max_nnz,
 // normalised by e^{gamma} = I_0 + 2 sum I_k (all terms positive).
 int cheb_coeffs(double gamma, double tol, std::vector<double>& chat);
 
+// Nonsymmetric A (op.sym == false, the paper's advection operators P:L343-348):
+// the same kernels evaluate the truncated Taylor series with scaling of Al-Mohy & Higham (2011),
+//   exp(tau A^T) = (e^{tau mu / s} T_m((tau / s)(A^T - mu I)))^s,  mu = trace(A) / n,
+// with (m, s) minimising m s subject to s >= tau ||A^T - mu I||_1 / theta_m (theta_m: their backward-
+// error bounds for unit roundoff 2^-53, m <= 55): accurate for any A, no spectrum information.
 // out[:, j] = alpha * exp(tau A^T) X[:, j], j < k (column-major, leading dims ldx / ldo; out != X).
 // Returns the total polynomial degree applied (sum over substeps).
 int cheb_action(const ChebOp& op, double tau, const double* X, int64_t ldx, int64_t k, double* out,

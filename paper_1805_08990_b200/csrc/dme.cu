@@ -212,6 +212,7 @@ void plan_buffers(dme_ctx* c, Planner& P) {
     c->cop.n = c->chost.n; c->cop.R = c->chost.R; c->cop.w = c->chost.w; c->cop.C = c->chost.C;
     c->cop.H = c->chost.H; c->cop.P = c->chost.P;
     c->cop.a = c->chost.a; c->cop.b = c->chost.b; c->cop.norm1 = c->chost.norm1;
+    c->cop.sym = c->chost.sym; c->cop.mu = c->chost.mu; c->cop.tnorm = c->chost.tnorm;
     c->cop.val = P.take<double>(ell);
     c->cop.idx = P.take<uint32_t>(ell);
     c->cop.push = P.take<uint32_t>(std::max<size_t>(c->chost.push.size(), 1));
@@ -429,7 +430,9 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
     const int code = cheb_prepare(pr->n, pr->A_nnz, pr->A_rowptr, pr->A_colind, pr->A_values, c->chost, &err);
     if (code) throw DmeError((dme_status)code, err);
     double lm = 0;
-    DME_REQUIRE(cheb_accurate(o->h, c->chost.b, pr->n, pr->A_rowptr, pr->A_colind, pr->A_values, &lm),
+    // (a nonsymmetric A takes the Taylor route of cheb.h, accurate by its backward-error bound)
+    DME_REQUIRE(!c->chost.sym ||
+                    cheb_accurate(o->h, c->chost.b, pr->n, pr->A_rowptr, pr->A_colind, pr->A_values, &lm),
                 DME_ERR_CONFIG,
                 "sparse A: the Gershgorin bound of A is too loose for an accurate Chebyshev action "
                 "(h (b - lambda_max) > ln 4); pass A dense (Padé-13)");
@@ -1401,6 +1404,7 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
         op.n = c->chost.n; op.R = c->chost.R; op.w = c->chost.w; op.C = c->chost.C;
         op.H = c->chost.H; op.P = c->chost.P;
         op.a = c->chost.a; op.b = c->chost.b; op.norm1 = c->chost.norm1;
+        op.sym = c->chost.sym; op.mu = c->chost.mu; op.tnorm = c->chost.tnorm;
         op.val = c->X4;
         op.idx = reinterpret_cast<uint32_t*>(c->X6);
         op.push = reinterpret_cast<uint32_t*>(c->U);
@@ -1563,8 +1567,10 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
   finish_ladder(q_cur, Ecur);
   double* Eh_full = spare[si];
   matmul_sq(c, Ecur, Ecur, Eh_full);
-  DME_CUDA(cudaMemcpyAsync(c->E_half, Ecur + c->erow0 * ld, (size_t)c->erows * ld * 8, cudaMemcpyDeviceToDevice, st));
-  DME_CUDA(cudaMemcpyAsync(c->E_full, Eh_full + c->erow0 * ld, (size_t)c->erows * ld * 8, cudaMemcpyDeviceToDevice, st));
+  DME_CUDA(cudaMemcpy2DAsync(c->E_half, ld * 8, Ecur + c->erow0 * ld, ld * 8, n * 8, c->erows,
+                             cudaMemcpyDeviceToDevice, st));
+  DME_CUDA(cudaMemcpy2DAsync(c->E_full, ld * 8, Eh_full + c->erow0 * ld, ld * 8, n * 8, c->erows,
+                             cudaMemcpyDeviceToDevice, st));
   if (c->oz) {  // digit slices of the held rows of E_{h/2} and E_h (after the last product)
     slice_shards(c, c->E_half, c->ozEh, c->exEh, st);
     slice_shards(c, c->E_full, c->ozEf, c->exEf, st);

@@ -71,6 +71,8 @@ def _workspace(A_dense=None, csr=None, n=None, **kw):
     opt = _Options()
     _lib.dme_default_options(ctypes.byref(opt))
     opt.rank_cap = 64
+    for key, val in kw.items():
+        setattr(opt, key, val)
     nbytes = ctypes.c_size_t(0)
     code = _lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(opt), ctypes.byref(nbytes))
     return code, nbytes.value
@@ -92,8 +94,12 @@ def test_sparse_workspace_has_no_dense_matrices():
 def test_sparse_plan_errors():
     import scipy.sparse as sps
     from workloads import make_config
-    prob = make_config(3, nx=8)  # nonsymmetric convection-diffusion
-    assert _workspace(csr=sps.csr_matrix(prob.A), n=prob.n)[0] == 3
+    prob = make_config(3, nx=8)  # nonsymmetric convection-diffusion: the Taylor route (accepted)
+    assert _workspace(csr=sps.csr_matrix(prob.A), n=prob.n)[0] == 0
+    # symmetric but not diagonally dominant (-L^2): the Chebyshev accuracy gate rejects it
+    from workloads import heat2d_matrix
+    L = heat2d_matrix(12)
+    assert _workspace(csr=sps.csr_matrix(-(L @ L)), n=L.shape[0], h=2e-4)[0] == 3
     A = sps.csr_matrix(make_config(5, nx=8).A)
     bad = A.copy()
     bad.indices = bad.indices.copy()

@@ -98,3 +98,21 @@ def test_config4_full_size(dme, eig4, scheme, comp):
     o._LI = {}
     Lo, Do = _orc(o, scheme, comp, N)
     assert lowrank.rel_diff(Lg, Dg, Lo, Do) <= TOL_P
+
+
+def test_config3_full_size_sparse_csr(dme, orc3):
+    """Config 3 (nonsymmetric convection-diffusion, n = 2500) with A passed as CSR: the cluster
+    kernels' Taylor route, no dense exponential; against the oracle at 1e-10."""
+    import scipy.sparse as sps
+    prob, _ = orc3
+    h, N = 0.005, 4
+    kw = dme.problem_kwargs(prob)
+    kw["A"] = sps.csr_matrix(prob.A)
+    s = dme.Solver(**kw, h=h, rank_cap=64)
+    s.split_step("strang", "F12F3", N)
+    Lg, Dg = s.get_factor()
+    s.close()
+    o = OracleSolver(prob, h, OracleOptions(rank_cap=64), method="action")
+    o.step("strang", "F12F3", N)
+    Lo, Do = o.factor()
+    assert lowrank.rel_diff(Lg, Dg, Lo, Do) <= TOL_P

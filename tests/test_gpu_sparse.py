@@ -5,7 +5,8 @@ built. The result it approximates has a plain definition, exp(tau A^T) L, so the
   * whole schemes against the oracle (dense exponential, same quadrature rule) at 1e-10 (P-level)
     and against the dense GPU path;
   * invariants: A = 0 (empty CSR) gives exp(0) = I, so Strang F1F2 yields P0 + T Q exactly (P13);
-  * the configuration errors of the boundary (nonsymmetric A, M with a sparse A, bad CSR).
+  * the configuration errors of the boundary (a loose Gershgorin bound, M with a sparse A, bad CSR);
+  * a nonsymmetric sparse A through the Taylor route of the same kernels.
 """
 import numpy as np
 import pytest
@@ -123,9 +124,10 @@ def test_zero_A_strang_F1F2_exact(dme):
 
 
 def test_sparse_errors(dme):
-    prob = make_config(3, nx=8)  # convection-diffusion: nonsymmetric
+    from workloads import heat2d_matrix
+    L = heat2d_matrix(10)  # -L^2: symmetric, Gershgorin bound far above lambda_max (accuracy gate)
     with pytest.raises(dme.DmeError) as e:
-        dme.Solver(**_kw(dme, prob), h=0.01)
+        dme.Solver(A=sps.csr_matrix(-(L @ L)), h=2e-4)
     assert e.value.code == 3
     prob = make_config(5, nx=8)
     A = sps.csr_matrix(prob.A)
@@ -224,3 +226,38 @@ def test_dense_A_chebyshev_E_matches_pade(dme, nx):
             assert np.array_equal(E, E.T)
     sa.close()
     sp.close()
+
+
+@pytest.mark.parametrize("nx,comp", [(10, "F12F3"), (16, "F1F2F3")])
+def test_nonsymmetric_sparse_taylor(dme, nx, comp):
+    """Nonsymmetric sparse A (config 3's convection-diffusion operator, the paper's advection
+    setting P:L343-348): the cluster kernels evaluate the truncated Taylor series with scaling
+    (Al-Mohy & Higham); against the oracle at 1e-10."""
+    prob = make_config(3, nx=nx)
+    h, N = 0.005, 5
+    kw = dme.problem_kwargs(prob)
+    kw["A"] = sps.csr_matrix(prob.A)
+    s = dme.Solver(**kw, h=h, rank_cap=64)
+    s.split_step("strang", comp, N)
+    Lg, Dg = s.get_factor()
+    s.close()
+    o = OracleSolver(prob, h, OracleOptions(rank_cap=64))
+    o.step("strang", comp, N)
+    Lo, Do = o.factor()
+    assert lowrank.rel_diff(Lg, Dg, Lo, Do) <= 1e-10
+
+
+def test_nonsymmetric_action_vs_expm(dme):
+    n = 300
+    rng = np.random.default_rng(7)
+    R = sps.random(n, n, density=4.0 / n, random_state=8, format="csr")
+    A = sps.csr_matrix(R * 30.0 - sps.eye(n) * 60.0)          # nonsymmetric, non-normal
+    h = 0.02
+    s = dme.Solver(A=A, h=h)
+    L = rng.random((n, 7))
+    s.debug_set_factor(L)
+    s.debug_apply("T1", h)
+    Y, _ = s.get_factor()
+    s.close()
+    ref = sla.expm(h * A.toarray().T) @ L
+    assert np.abs(Y - ref).max() <= 1e-12 * np.abs(ref).max()
