@@ -185,7 +185,9 @@ typedef struct {
   int64_t rank;             /* current rank of the factor                                      */
   int64_t max_rank;         /* largest rank seen after a compression                           */
   int64_t q_half, q_full;   /* ranks of L_I(h/2), L_I(h)                                       */
-  int32_t squarings;        /* s: Padé-13 scaling exponent of (h/2) A^T                        */
+  int32_t squarings;        /* s: Padé-13 scaling exponent of (h/2) A^T; it fixes the quadrature
+                               panel count (reading G6) also when E_{h/2} is built by Chebyshev
+                               actions (then no squarings beyond E_h = E_{h/2}^2 are performed) */
   int32_t quad_panels;      /* panels of the composite rule on [0, h/2]                        */
   double panel_width;       /* delta = (h/2) / panels                                          */
   double pade_min_pivot;    /* smallest |u_ii| of the Padé denominator factorisation           */
