@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -916,6 +917,7 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
   const int64_t k = cp.k;
   const int cap = cp.a.cap;
   int64_t ks = 0, s = 0;
+  bool tail_done = false;
   if (kb < k && tmax > 0.0 && kb < cap) {
     // U (k x s): orthonormal basis of the complement of span(W_b); Zs = Zc U (n x s), Gs = Zs^T Zs
     s = k - kb;
@@ -947,11 +949,29 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
     if (b.map) b.map_seq = ++c->map_seq;
     bool fast2 = false;
     launch_eig(c, b, fast2);
+    // the tail assembly (+ T3) is queued right behind the eigen pass and reads ks on the device,
+    // so the critical stream does not idle through this host round trip; a Jacobi fallback of the
+    // pass (ks < 0 published) turns it into a no-op and it is queued again below
+    const int ks_bound = std::min<int>(b.cap, (int)s);
+    const bool dev_ks = fast2 && tail_assemble_smem((int)k, (int)c->m, (int)s, (int)kb, ks_bound) <=
+                                     (size_t)SMALL_SMEM_MAX;
+    if (dev_ks) {
+      SmallArgs t = cp.a;
+      t.k = (int)k;
+      t.t3 = cp.t3 ? 1 : 0;
+      ProfScope ps(c, PROF_SMALL);
+      tail_assemble_t3(t, c->Us, KMAX, (int)s, c->Ts, KMAX, (int)kb, ks_bound, c->st, c->r_dev);
+    }
+    const int64_t pubs = c->stats.eig_fallbacks;
     ks = eig_finish(c, b, fast2);
     r = kb + ks;
     drop = c->last_st[2];
+    tail_done = dev_ks && c->stats.eig_fallbacks == pubs;
+    if (std::getenv("DME_DEBUG_REFINE"))
+      std::fprintf(stderr, "refine: k %lld kb %lld s %lld ks %lld\n", (long long)k, (long long)kb,
+                   (long long)s, (long long)ks);
   }
-  if (ks > 0 || (cp.t3 && r > 0)) {  // Tm[:, kb:r] = U V_s, then T3 on Tm
+  if (!tail_done && (ks > 0 || (cp.t3 && r > 0))) {  // Tm[:, kb:r] = U V_s, then T3 on Tm
     SmallArgs t = cp.a;
     t.k = (int)k;
     t.t3 = cp.t3 ? 1 : 0;

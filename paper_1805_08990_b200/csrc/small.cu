@@ -355,8 +355,12 @@ __global__ void tail_product_kernel(double* Tm, int64_t ldt, const double* __res
 // the Riccati flow T3 on the whole Tm (k x (kb + ks)) when a.t3 is set.
 __global__ void __launch_bounds__(NT) tail_assemble_kernel(SmallArgs a, const double* __restrict__ U,
                                                            int64_t ldu, int s, const double* __restrict__ V,
-                                                           int64_t ldv, int kb, int ks) {
+                                                           int64_t ldv, int kb, int ks, const int* ks_dev) {
   extern __shared__ double S[];
+  if (ks_dev) {  // the tail rank published by the preceding eigen pass (< 0: it fell back to Jacobi)
+    ks = *ks_dev;
+    if (ks < 0) return;
+  }
   __shared__ double Gam[SMALL_M_MAX * SMALL_M_MAX];
   __shared__ double Phi[SMALL_M_MAX * SMALL_M_MAX];
   const int k = a.k, r = kb + ks, m = a.m, tid = threadIdx.x;
@@ -415,14 +419,22 @@ void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, in
 
 void t3_only(const SmallArgs& a, int r, cudaStream_t st);
 
+size_t tail_assemble_smem(int k, int m, int s, int kb, int ks) {
+  const int r = kb + ks;
+  size_t need = sizeof(double) * ((size_t)k * r + (size_t)k * m + (size_t)k * s + (size_t)s * ks);
+  const size_t t3s = sizeof(double) * ((size_t)k * r + (size_t)k * m + 2 * SMALL_K_MAX * SMALL_M_MAX);
+  return need < t3s ? t3s : need;
+}
+
 void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, const double* V,
-                      int64_t ldv, int kb, int ks, cudaStream_t st) {
+                      int64_t ldv, int kb, int ks, cudaStream_t st, const int* ks_dev) {
   if (a.m > SMALL_M_MAX) throw std::runtime_error("tail_assemble_t3: m exceeds SMALL_M_MAX");
   const int k = a.k, r = kb + ks;
   size_t need = sizeof(double) * ((size_t)k * r + (size_t)k * a.m + (size_t)k * s + (size_t)s * ks);
   const size_t t3s = sizeof(double) * ((size_t)k * r + (size_t)k * a.m + 2 * SMALL_K_MAX * SMALL_M_MAX);
   if (need < t3s) need = t3s;
   if (need > (size_t)SMALL_SMEM_MAX) {  // wide systems: the product in global memory, then T3 alone
+    if (ks_dev) throw std::runtime_error("tail_assemble_t3: device rank needs the shared-memory path");
     if (ks > 0) {
       tail_product_kernel<<<(k * ks + 255) / 256, 256, 0, st>>>(a.Tm, a.ldt, U, ldu, s, V, ldv, k, kb, ks);
       DME_KCHECK();
@@ -436,7 +448,7 @@ void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, c
     DME_CUDA(cudaFuncSetAttribute(tail_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SMALL_SMEM_MAX));
   });
-  tail_assemble_kernel<<<1, NT, need, st>>>(a, U, ldu, s, V, ldv, kb, ks);
+  tail_assemble_kernel<<<1, NT, need, st>>>(a, U, ldu, s, V, ldv, kb, ks, ks_dev);
   DME_KCHECK();
 }
 

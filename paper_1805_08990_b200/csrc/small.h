@@ -57,9 +57,12 @@ void t3_only(const SmallArgs& a, int r, cudaStream_t st);  // T3 on Tm (k x r) a
 // U (k x (k - kb), ldu): orthonormal basis of the complement of span(W), W = k x kb orthonormal
 void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, int64_t ldu,
                       cudaStream_t st);
-// a.Tm[:, kb:kb+ks] = U V (U: k x s, V: s x ks), then T3 on a.Tm (k x (kb + ks)) if a.t3
+// a.Tm[:, kb:kb+ks] = U V (U: k x s, V: s x ks), then T3 on a.Tm (k x (kb + ks)) if a.t3.
+// ks_dev != nullptr: ks is read on the device (the rank the preceding eigen pass published; a
+// negative value -- Jacobi fallback pending -- makes the kernel a no-op); ks is then an upper bound
+size_t tail_assemble_smem(int k, int m, int s, int kb, int ks);
 void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, const double* V,
-                      int64_t ldv, int kb, int ks, cudaStream_t st);
+                      int64_t ldv, int kb, int ks, cudaStream_t st, const int* ks_dev = nullptr);
 // Pp = I - W W^T (k x k), W: k x kb (the kept leading eigenvectors of the first pass)
 void complement_projector(const double* W, int64_t ldw, int k, int kb, double* Pp, int64_t ldp,
                           cudaStream_t st);
