@@ -60,7 +60,7 @@ constexpr double SPLIT_TOL = 1e-11;     // refined compression: first pass keeps
 // rung, so the rungs below the final L_I(h/2), L_I(h) keep 64x finer directions and only the final
 // factors are truncated at trunc_tol (their ranks then match a one-shot truncation)
 constexpr double LADDER_TOL = 1.0 / 64;
-constexpr int LOOKAHEAD_RESERVE = EIG_SPLIT_CTAS;  // SMs the look-ahead stream leaves free
+constexpr int LOOKAHEAD_RESERVE = 8;  // SMs the look-ahead stream leaves free (tools/la_ab.sh: 116-140 equal step rate)
 
 // Gauss-Legendre nodes/weights on [0,1] by Newton on P_q (Golub-Welsch-free; own implementation)
 void gauss_legendre01(int q, std::vector<double>& c, std::vector<double>& w) {
