@@ -258,9 +258,22 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const Params p) {
     const int tid = (int)(e % NUM_CONSUMERS);
     const int i = (int)((e / NUM_CONSUMERS) % ACC);
     const int tile = (int)(e / ((long long)NUM_CONSUMERS * ACC));
-    double acc = 0.0;
-    for (int sl = 0; sl < p.slices; ++sl)
-      acc += __ldcg(p.partial + (size_t)(sl * T + tile) * (BM * BN) + i * NUM_CONSUMERS + tid);
+    // fixed association (deterministic): 8 interleaved partial sums over the slices, combined in
+    // a fixed tree; the 8 independent loads of a round are in flight together (the reduction was
+    // bound by one L2 round trip per slice)
+    const double* src = p.partial + (size_t)tile * (BM * BN) + i * NUM_CONSUMERS + tid;
+    const size_t sstride = (size_t)T * (BM * BN);
+    double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int sl = 0;
+    for (; sl + 8 <= p.slices; sl += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + (size_t)(sl + u) * sstride);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s8[u] += x[u];
+    }
+    for (int u = 0; sl < p.slices; ++sl, ++u) s8[u] += __ldcg(src + (size_t)sl * sstride);
+    const double acc = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int wm = warp % WM, wn = warp / WM;
     const int el = i & 1, mn = i >> 1, mi = mn / NTW, ni = mn % NTW;
