@@ -102,9 +102,11 @@ typedef struct {
      when the Gershgorin bound is too loose for it), and for a nonsymmetric A the
      truncated Taylor series with scaling of Al-Mohy & Higham (cheb.h; degree m <= 55 and s substeps
      from ||tau (A^T - mu I)||), evaluated by the same cluster kernels; the quadrature rule is unchanged (its panel count
-     still comes from ||(h/2) A^T||_1), and init builds no n x n matrix. n x (row width) must fit
-     the shared memory of one 8-CTA cluster (DME_ERR_DIM otherwise; n = 10^4 with a 5-point
-     stencil fits). Not combinable with M or with world_size > 1 (DME_ERR_CONFIG).
+     still comes from ||(h/2) A^T||_1), and init builds no n x n matrix. While n x (row width) fits
+     the shared memory of one 8-CTA cluster (n ~ 1.2e4 rows of a 5-point stencil) the actions run
+     on chip in cluster kernels; beyond, in a grid-wide cooperative kernel with the vectors in
+     global memory (any n with n x 224 < 2^31). Not combinable with M or with world_size > 1
+     (DME_ERR_CONFIG).
      Callers that zero-initialise the struct get the dense path.                          */
   int64_t A_nnz;
   const int64_t* A_rowptr; /* n + 1 */

@@ -18,6 +18,9 @@
 #include <cstdlib>
 
 #include "cheb.h"
+
+#include <cooperative_groups.h>
+#include <memory>
 #include "common.cuh"
 #include "dme.h"
 #include "small.h"
@@ -505,7 +508,7 @@ int cheb_coeffs(double gamma, double tol, std::vector<double>& chat) {
 }
 
 int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* colind,
-                 const double* values, ChebHost& out, std::string* err) {
+                 const double* values, ChebHost& out, std::string* err, bool force_global) {
   auto fail = [&](int code, const char* m) {
     if (err) *err = m;
     return code;
@@ -593,7 +596,12 @@ int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* c
   int C = 0;
   for (int c = CHEB_CMAX; c >= 1; --c)
     if (cheb_smem_bytes(R, w, H, P, c) <= 225 * 1024) { C = c; break; }
-  if (C == 0) return fail(DME_ERR_DIM, "sparse A: rows x (ELL width + halo) too large for one cluster's shared memory");
+  out.global = force_global || C == 0 || std::getenv("DME_CHEB_GLOBAL") != nullptr;
+  if (out.global) {  // rows beyond one cluster's shared memory: the grid-wide kernel
+    C = CHEB_CMAX;
+    H = P = 0;
+    for (auto& pl : pushes) pl.clear();
+  }
   out.nnz = 0;
   for (auto& r : rowsT) out.nnz += (int64_t)r.size();
   out.n = n; out.R = R; out.w = w; out.H = H; out.P = P; out.C = C;
@@ -622,6 +630,22 @@ int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* c
   const int64_t ldm = (int64_t)CHEB_CLUSTER * R;
   out.val.assign((size_t)w * ldm, 0.0);
   out.idx.assign((size_t)w * ldm, 0u);
+  if (out.global) {  // ELL with global column indices (padding: 0 x own row)
+    for (int64_t i = 0; i < ldm; ++i) {
+      for (int q = 0; q < w; ++q) out.idx[q * ldm + i] = (uint32_t)std::min<int64_t>(i, n - 1);
+      if (i >= n) continue;
+      int q = 0;
+      for (auto& x : rowsT[i]) {
+        out.val[q * ldm + i] = x.second;
+        out.idx[q * ldm + i] = (uint32_t)x.first;
+        ++q;
+      }
+    }
+    out.push.clear();
+    out.rptr.assign(1, 0u);
+    out.rent.clear();
+    return 0;
+  }
   for (int64_t i = 0; i < ldm; ++i) {
     const int r = (int)(i / R);
     for (int q = 0; q < w; ++q) out.idx[q * ldm + i] = (uint32_t)(i % R);  // padding: 0 x own row
@@ -678,6 +702,125 @@ void preload_all() {
     preload_c<5>(); preload_c<6>(); preload_c<7>(); preload_c<8>();
   });
 }
+
+// ---------------------------------------------------------------- global mode (large n)
+// The same recurrences (Chebyshev, or Taylor for a nonsymmetric A) over all rows with one
+// cooperative grid: thread (row i, column j) pairs strided over the grid, v_{k-1} gathered from
+// global memory (L2-resident: n x k doubles), v_k written over v_{k-2}, y in global memory; one
+// grid barrier per degree. Used when n x (ELL width + halo) exceeds one cluster's shared memory.
+struct GParams {
+  const double* val;
+  const uint32_t* idx;
+  int64_t ldm;
+  const double* X;
+  double* out;
+  double *v0, *v1, *y;
+  int64_t ldx, ldo, ldv, n;
+  int w, k, K, substeps, taylor;
+  double alpha, beta, out_scale;
+  double coef[CHEB_KMAX + 1];
+  double rk[TAYLOR_MMAX + 1];
+};
+
+constexpr int GTHREADS = 512;
+
+__global__ void __launch_bounds__(GTHREADS) cheb_global_kernel(GParams p) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t n = p.n, ldv = p.ldv;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < p.k; ++j)
+    for (int64_t i = t0; i < n; i += stride) {
+      const double x = p.X[i + j * p.ldx];
+      p.v0[i + j * ldv] = x;
+      p.y[i + j * ldv] = p.coef[0] * x;
+    }
+  grid.sync();
+  double* cur = p.v0;
+  double* prv = p.v1;
+  for (int sub = 0; sub < p.substeps; ++sub) {
+    if (sub > 0) {  // v_0 of the next substep = y
+      for (int j = 0; j < p.k; ++j)
+        for (int64_t i = t0; i < n; i += stride) {
+          const double v = p.y[i + j * ldv];
+          cur[i + j * ldv] = v;
+          p.y[i + j * ldv] = p.coef[0] * v;
+        }
+      grid.sync();
+    }
+    const int nn = (int)n, total4 = (int)n * ((p.k + 3) / 4);  // (n k <= 2^31: checked on the host)
+    for (int kd = 1; kd <= p.K; ++kd) {
+      const double ck = p.coef[kd], rk = p.rk[kd < TAYLOR_MMAX ? kd : TAYLOR_MMAX];
+      // (row, 4-column block) pairs flattened over the whole grid: consecutive threads take
+      // consecutive rows (coalesced); a thread loads its row's ELL entries once for 4 columns
+      // and issues their gathers together (the loop is bound by L2 traffic and latency)
+      const double* __restrict__ cr_ = cur;
+      double* __restrict__ pr_ = prv;
+      double* __restrict__ yr_ = p.y;
+      for (int e = (int)t0; e < total4; e += (int)stride) {
+        const int jb = e / nn, i = e - jb * nn;
+        const int j0 = 4 * jb;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < p.w; ++q) {
+          const double a = p.val[q * p.ldm + i];
+          const int64_t col = p.idx[q * p.ldm + i];
+          double g[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) g[u] = j0 + u < p.k ? __ldcg(cr_ + col + (int64_t)(j0 + u) * ldv) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u] = fma(a, g[u], acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (j0 + u >= p.k) break;
+          const int64_t o = i + (int64_t)(j0 + u) * ldv;
+          const double t = p.alpha * acc[u] - p.beta * cr_[o];
+          const double vn = p.taylor ? t * rk : (kd == 1 ? t : 2.0 * t - pr_[o]);
+          pr_[o] = vn;
+          yr_[o] = fma(ck, vn, yr_[o]);
+        }
+      }
+      grid.sync();
+      double* tmp = cur;
+      cur = prv;
+      prv = tmp;
+    }
+  }
+  for (int j = 0; j < p.k; ++j)
+    for (int64_t i = t0; i < n; i += stride) p.out[i + j * p.ldo] = p.out_scale * p.y[i + j * ldv];
+}
+
+int cheb_action_global(const ChebOp& op, const ChebParams& prm, cudaStream_t st) {
+  GParams* g = new GParams;  // (large: built on the heap, passed by value to the launch)
+  std::unique_ptr<GParams> own(g);
+  std::memset(g, 0, sizeof(GParams));
+  g->val = op.val; g->idx = op.idx; g->ldm = (int64_t)CHEB_CLUSTER * op.R;
+  g->X = prm.X; g->out = prm.out; g->v0 = op.gv0; g->v1 = op.gv1; g->y = op.gy;
+  g->ldx = prm.ldx; g->ldo = prm.ldo; g->ldv = (int64_t)CHEB_CLUSTER * op.R; g->n = op.n;
+  g->w = op.w; g->k = prm.k; g->K = prm.K; g->substeps = prm.substeps; g->taylor = prm.taylor;
+  g->alpha = prm.alpha; g->beta = prm.beta; g->out_scale = prm.out_scale;
+  std::memcpy(g->coef, prm.coef, sizeof(g->coef));
+  std::memcpy(g->rk, prm.rk, sizeof(g->rk));
+  static std::mutex mu;
+  static uint64_t mask = 0;
+  static int per_sm = 1;
+  per_device_once(mu, mask, [&] {
+    DME_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cheb_global_kernel, GTHREADS, 0));
+  });
+  int dev = 0, sms = 148;
+  DME_CUDA(cudaGetDevice(&dev));
+  DME_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // few CTAs per SM: each grid barrier costs more with more CTAs
+  int bps = 2;  // (measured at n = 1e4 and 3.6e4: 2 CTAs per SM beat 1 and 4)
+  if (const char* e = std::getenv("DME_CHEB_GLOBAL_BPS")) bps = std::atoi(e);
+  const int grid_n = std::max(1, std::min(std::max(per_sm, 1), std::max(bps, 1)) * sms);
+  void* args[] = {g};
+  DME_CUDA(cudaLaunchCooperativeKernel((void*)cheb_global_kernel, dim3(grid_n), dim3(GTHREADS), args, 0, st));
+  DME_KCHECK();
+  return prm.K * prm.substeps;
+}
+
 }  // namespace
 
 int cheb_action(const ChebOp& op, double tau, const double* X, int64_t ldx, int64_t k, double* out,
@@ -730,6 +873,11 @@ int cheb_action(const ChebOp& op, double tau, const double* X, int64_t ldx, int6
     prm.beta = gamma > 0 ? c / gamma : 0.0;
   }
   prm.out_scale = alpha;
+  if (op.global) {
+    if (k > SMALL_K_MAX || (int64_t)op.n * k >= ((int64_t)1 << 31))
+      throw std::runtime_error("cheb_action (global): too many columns");
+    return cheb_action_global(op, prm, st);
+  }
   // columns per cluster: the smallest C whose ceil(k / C) clusters are co-resident in one wave
   // (cudaOccupancyMaxActiveClusters: clusters are placed within a GPC, 15 x 8 CTAs on a B200 at
   // this shared-memory size), less one cluster's SMs for the eigen kernels that run concurrently

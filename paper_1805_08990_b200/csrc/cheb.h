@@ -41,6 +41,10 @@ struct ChebOp {
   double norm1 = 0;       // ||A^T||_1
   bool sym = true;        // A == A^T: Chebyshev on [a, b]; otherwise truncated Taylor (below)
   double mu = 0, tnorm = 0;  // trace(A)/n and max(||A^T - mu I||_1, ||A^T - mu I||_inf)
+  // global mode (n beyond one cluster's shared memory): ELL of A^T with global column indices,
+  // one cooperative grid over all SMs, vectors in global memory (L2), one grid barrier per degree
+  bool global = false;
+  double *gv0 = nullptr, *gv1 = nullptr, *gy = nullptr;  // [CHEB_CLUSTER * R][KMAX] each (device)
   double* val = nullptr;    // [w][CHEB_CLUSTER * R] (device)
   uint32_t* idx = nullptr;  // [w][CHEB_CLUSTER * R]: local index into [0, R + H) (own row or halo slot)
   uint32_t* push = nullptr; // [CHEB_CLUSTER][P][2]: (own row, (dest CTA << 24) | dest slot), ~0 = none
@@ -57,11 +61,12 @@ struct ChebHost {
   double a = 0, b = 0, norm1 = 0;
   bool sym = true;
   double mu = 0, tnorm = 0;
+  bool global = false;
   std::vector<double> val;
   std::vector<uint32_t> idx, push, rptr, rent;
 };
 int cheb_prepare(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* colind,
-                 const double* values, ChebHost& out, std::string* err);
+                 const double* values, ChebHost& out, std::string* err, bool force_global = false);
 size_t cheb_smem_bytes(int64_t R, int w, int H, int P, int C);
 
 // CSR of a dense row-major device matrix (nonzero pattern, exact values), if it has at most max_nnz

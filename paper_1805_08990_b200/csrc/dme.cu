@@ -214,6 +214,13 @@ void plan_buffers(dme_ctx* c, Planner& P) {
     c->cop.H = c->chost.H; c->cop.P = c->chost.P;
     c->cop.a = c->chost.a; c->cop.b = c->chost.b; c->cop.norm1 = c->chost.norm1;
     c->cop.sym = c->chost.sym; c->cop.mu = c->chost.mu; c->cop.tnorm = c->chost.tnorm;
+    c->cop.global = c->chost.global;
+    if (c->cop.global) {  // vectors of the grid-wide action (cheb.h)
+      const size_t gv = (size_t)CHEB_CLUSTER * c->chost.R * KMAX;
+      c->cop.gv0 = P.take<double>(gv);
+      c->cop.gv1 = P.take<double>(gv);
+      c->cop.gy = P.take<double>(gv);
+    }
     c->cop.val = P.take<double>(ell);
     c->cop.idx = P.take<uint32_t>(ell);
     c->cop.push = P.take<uint32_t>(std::max<size_t>(c->chost.push.size(), 1));
@@ -1407,7 +1414,8 @@ void init_all(dme_ctx* c, const dme_problem* pr) {
       // (accuracy gate: ADVICE r1; cost model: the Chebyshev-built E costs ~K ceil(n/60) cluster
       // waves of ~2.1 us per degree (measured, §9c), Padé-13 with int8 products ~0.33 s (n/1e4)^3)
       const bool ok_prep = cheb_prepare(n, (int64_t)vv.size(), rp.data(), ci.data(), vv.data(), ch, &err) == 0;
-      bool take = ok_prep && cheb_accurate(c->h, ch.b, n, rp.data(), ci.data(), vv.data(), &lm_est);
+      bool take = ok_prep && !ch.global &&
+                  cheb_accurate(c->h, ch.b, n, rp.data(), ci.data(), vv.data(), &lm_est);
       if (take) {
         std::vector<double> chat;
         const double gamma = 0.5 * tau0 * (ch.b - ch.a);

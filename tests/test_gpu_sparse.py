@@ -261,3 +261,63 @@ def test_nonsymmetric_action_vs_expm(dme):
     s.close()
     ref = sla.expm(h * A.toarray().T) @ L
     assert np.abs(Y - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def _with_env(key, fn):
+    import os
+    old = os.environ.get(key)
+    os.environ[key] = "1"
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[key]
+        else:
+            os.environ[key] = old
+
+
+@pytest.mark.parametrize("cfg,nx,comp", [(5, 14, "F12F3"), (3, 12, "F12F3"), (5, 10, "F1F2F3")])
+def test_global_mode_forced_small(dme, cfg, nx, comp):
+    """The grid-wide action (large-n layout) forced at small n (DME_CHEB_GLOBAL): Chebyshev for the
+    symmetric heat operator, Taylor for convection-diffusion; against the oracle at 1e-10."""
+    prob = make_config(cfg, nx=nx)
+    h, N = 0.005, 4
+    kw = dme.problem_kwargs(prob)
+    kw["A"] = sps.csr_matrix(prob.A)
+    s = _with_env("DME_CHEB_GLOBAL", lambda: dme.Solver(**kw, h=h, rank_cap=64))
+    s.split_step("strang", comp, N)
+    Lg, Dg = s.get_factor()
+    s.close()
+    o = OracleSolver(prob, h, OracleOptions(rank_cap=64))
+    o.step("strang", comp, N)
+    Lo, Do = o.factor()
+    assert lowrank.rel_diff(Lg, Dg, Lo, Do) <= 1e-10
+
+
+@pytest.mark.slow
+def test_large_n_beyond_one_cluster(dme):
+    """n = 190^2 = 36100 (> 3e4; one 8-CTA cluster's shared memory holds ~1.2e4 rows): the sparse
+    action runs grid-wide. One T1 action against the closed-form heat eigenbasis (pin P5), and
+    three Strang F1F2F3 DRE steps against the oracle (1e-10)."""
+    from oracle import flows
+    nx, h = 190, 0.005
+    prob = make_config(5, nx=nx)
+    kw = dme.problem_kwargs(prob)
+    kw["A"] = sps.csr_matrix(prob.A)
+    s = dme.Solver(**kw, h=h, rank_cap=64)
+    L = np.random.default_rng(9).random((prob.n, 11))
+    s.debug_set_factor(L)
+    s.debug_apply("T1", h)
+    Y, _ = s.get_factor()
+    s.close()
+    op = flows.Operator(prob.A, "heat", nx, 2)
+    ref = op.apply(h, L)
+    assert np.abs(Y - ref).max() <= 1e-13 * np.abs(L).max()
+    s = dme.Solver(**kw, h=h, rank_cap=64)
+    s.split_step("strang", "F1F2F3", 3)
+    Lg, Dg = s.get_factor()
+    s.close()
+    o = OracleSolver(prob, h, OracleOptions(rank_cap=64))
+    o.step("strang", "F1F2F3", 3)
+    Lo, Do = o.factor()
+    assert lowrank.rel_diff(Lg, Dg, Lo, Do) <= 1e-10
