@@ -78,3 +78,71 @@ def test_init_rejects_bad_input_without_device():
     assert b"positive definite" in dme._lib.dme_last_error()
     assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
     assert dme._lib.dme_split_step(None, 0, 0, 1) == 1
+
+
+def _host_problem(n):
+    import numpy as np
+    import paper_1805_08990_b200 as dme
+    A = -2.0 * np.eye(n)
+    keep = [A]
+    pr = dme._Problem(n=n, A=A.ctypes.data_as(dme._dp), p=0, C=None, m=0, B=None, R=None, S=None,
+                      r0=0, L0=None, D0=None)
+    o = dme._Options()
+    dme._lib.dme_default_options(ctypes.byref(o))
+    return pr, o, keep
+
+
+def test_csr_s_validation_host_only():
+    """The CSR form of S (T4 by sparse products) is validated on the host before any device work."""
+    import numpy as np
+    import paper_1805_08990_b200 as dme
+    n = 6
+    pr, o, keep = _host_problem(n)
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = np.arange(n, dtype=np.int32)
+    vv = np.full(n, 0.5)
+    keep += [rp, ci, vv]
+    pr.S_nnz = n
+    pr.S_rowptr = rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    pr.S_colind = ci.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    pr.S_values = vv.ctypes.data_as(dme._dp)
+    nb = ctypes.c_size_t(0)
+    assert dme._lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(nb)) == 0
+    assert nb.value > 0
+    # (the init validates the host inputs before any device call: DME_ERR_INVALID here, no GPU)
+    o.h = 0.01
+    ctx = ctypes.c_void_p()
+    ci[2] = n + 3                      # column index out of range
+    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+    assert b"CSR S" in dme._lib.dme_last_error()
+    ci[2] = 2
+    vv[1] = np.inf                     # non-finite value
+    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+    vv[1] = 0.5
+    rp[3] = 1                          # decreasing row pointers
+    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+
+
+def test_virtual_world_plan_host_only():
+    """options.virtual_world = G plans the G-shard staging blocks and digit images on one GPU;
+    out-of-range values are rejected."""
+    import paper_1805_08990_b200 as dme
+    n = 200
+    pr, o, keep = _host_problem(n)
+    nb1, nbg = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    assert dme._lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(nb1)) == 0
+    o.virtual_world = 4
+    assert dme._lib.dme_workspace_size(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(nbg)) == 0
+    assert nbg.value > nb1.value       # + the 4 x n_loc x 224 staging blocks
+    o.virtual_world = 65
+    o.h = 0.01
+    ctx = ctypes.c_void_p()
+    assert dme._lib.dme_dle_init(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(ctx)) == 1
+    assert b"virtual_world" in dme._lib.dme_last_error()
+
+
+def test_compression_option_values():
+    import paper_1805_08990_b200 as dme
+    o = dme._Options()
+    dme._lib.dme_default_options(ctypes.byref(o))
+    assert o.compression == 0 and o.virtual_world == 0      # refined compression, no virtual shards
