@@ -144,3 +144,28 @@ def test_poisoned_workspace(dme, e_pass):
         s.close()
     (L1, D1), (L2, D2) = out
     assert L1.shape == L2.shape and np.array_equal(L1, L2) and np.array_equal(D1, D2)
+
+
+@pytest.mark.parametrize("a,q,beta,p0", [(-1.0, 1.0, 1.0, 1.0), (-3.0, 0.5, 2.0, 0.2), (0.4, 2.0, 0.5, 1.5)])
+def test_scalar_dre_scheme_closed_form(dme, a, q, beta, p0):
+    """n = 1 through the whole GPU path against the paper's scalar recursions written out here
+    (pin P3 of SURVEY §8(c), independent of the oracle): Strang F12F3 is
+    p <- T12(h/2) T3(h) T12(h/2) p with T12(t) p = e^{2at} p + q (e^{2at} - 1) / (2a) (eq:full,
+    P:L129) and T3(t) p = p / (1 + t beta p); Lie F1F2F3 is T1 T2 T3 with
+    T1(t) p = e^{2at} p, T2(t) p = p + t q."""
+    h, N = 0.01, 40
+    prob = Problem(A=np.array([[a]]), C=np.array([[np.sqrt(q)]]), L0=np.array([[np.sqrt(p0)]]),
+                   D0=np.eye(1), B=np.array([[1.0]]), R=np.array([[1.0 / beta]]), T=h * N)
+    t12 = lambda p, t: np.exp(2 * a * t) * p + q * np.expm1(2 * a * t) / (2 * a)
+    t3 = lambda p, t: p / (1 + t * beta * p)
+    for scheme, comp, step in (("strang", "F12F3", lambda p: t12(t3(t12(p, h / 2), h), h / 2)),
+                               ("lie", "F1F2F3", lambda p: t3(np.exp(2 * a * h) * p + h * q, h))):
+        s = dme.Solver(**dme.problem_kwargs(prob), h=h)
+        s.split_step(scheme, comp, N)
+        L, D = s.get_factor()
+        s.close()
+        pg = float((L @ D @ L.T)[0, 0])
+        p = p0
+        for _ in range(N):
+            p = step(p)
+        assert abs(pg - p) <= 1e-12 * abs(p), (scheme, pg, p)
