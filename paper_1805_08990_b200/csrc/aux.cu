@@ -2,7 +2,9 @@
 #include "aux.h"
 
 #include <algorithm>
+#include <mutex>
 #include "common.cuh"
+#include <cooperative_groups.h>
 #include "gemm_nt.h"
 
 namespace dme {
@@ -232,6 +234,188 @@ inline int grid_for(int64_t total, int threads = 256) {
   int64_t b = (total + threads - 1) / threads;
   const int64_t cap = (int64_t)num_sms() * 8;
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+
+// ---------------------------------------------------------------- projected Gram (refined compression)
+// G = (Z U)^T (Z U) without materialising W = Z U (n x s). One cooperative wave: every CTA takes one
+// block of rb rows of Z (rb = n / #SMs rounded up to 8), forms its W rows in shared memory (DMMA,
+// K = k) and accumulates the upper tiles of W^T W (DMMA, K = rb) in registers; after a grid barrier
+// each warp sums the per-CTA partials of some elements in a fixed order (lane-strided, then a fixed
+// butterfly: deterministic). Operands are staged with cp.async (8-byte, zero-filled outside Z / U),
+// all in flight at once. Phase-1 work units are (n-tile, m-group) pairs, NT * MG = 16 * UPW of
+// them: every warp owns UPW units and the m-tiles mt = mg (mod MG) of each (one B fragment per unit
+// and k-step, one A fragment per m-tile).
+constexpr int PG_KMAX = 160;   // k bound (the refined compression runs for k <= FAST_K_MAX = 160)
+constexpr int PG_RMAX = 128;   // rows per block
+constexpr int PG_WARPS = 16;
+constexpr size_t PG_SMEM = 220 * 1024;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(ok ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__host__ __device__ constexpr int pg_kpad(int k) { return (k + 15) & ~15; }
+__host__ __device__ constexpr int pg_ldz(int rb) { return ((rb + 15) & ~15) + 8; }
+template <int NT>
+struct PgShape {
+  static constexpr int SP = NT * 8, LDW = SP + 8;
+  static constexpr int MG = NT == 8 ? 2 : 4;                  // NT * MG = 16 * UPW units
+  static constexpr int UPW = NT * MG / PG_WARPS;              // units per warp
+  static constexpr int MTG = (PG_RMAX / 8 + MG - 1) / MG;     // m-tiles per unit (max)
+  static constexpr int T = NT * (NT + 1) / 2, Q = (T + PG_WARPS - 1) / PG_WARPS;  // phase-2 tiles
+};
+
+template <int NT>
+__global__ void __launch_bounds__(PG_WARPS * 32, 1)
+    proj_gram_kernel(const double* __restrict__ Z, int64_t ldz, int64_t n, int k,
+                     const double* __restrict__ U, int64_t ldu, int s, int rb, double* part,
+                     double* G, int64_t ldg) {
+  using S = PgShape<NT>;
+  constexpr int SP = S::SP, LDW = S::LDW, MG = S::MG, UPW = S::UPW, MTG = S::MTG, T = S::T,
+                Q = S::Q;
+  extern __shared__ __align__(16) double pg_sm[];
+  const int kp = pg_kpad(k), ldu_s = kp + 4, k4 = (k + 3) & ~3, ldz_s = pg_ldz(rb);
+  const int mt_n = rb >> 3;
+  double* sU = pg_sm;             // [SP][ldu_s]: sU[j][kk] = U[kk, j]
+  double* sZ = sU + SP * ldu_s;   // [kp][ldz_s]: sZ[kk][m] = Z[m0 + m, kk]; reused as sW
+  double* sW = sZ;                // [rb][LDW]:   sW[m][j] = W[m0 + m, j]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  for (int j = warp; j < SP; j += PG_WARPS)
+    for (int kk = lane; kk < kp; kk += 32) {
+      const bool ok = j < s && kk < k;
+      cp_async8(sU + j * ldu_s + kk, ok ? U + kk + (int64_t)j * ldu : U, ok);
+    }
+  int tI[Q], tJ[Q];
+  double gacc[Q][2];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    int rem = warp + PG_WARPS * q, jt = 0;
+    while (rem > jt) rem -= ++jt;
+    tI[q] = rem;
+    tJ[q] = jt;
+    gacc[q][0] = gacc[q][1] = 0.0;
+  }
+  for (int64_t m0 = (int64_t)blockIdx.x * rb; m0 < n; m0 += (int64_t)gridDim.x * rb) {
+    for (int kk = warp; kk < kp; kk += PG_WARPS)
+      for (int m = lane; m < rb; m += 32) {
+        const bool ok = kk < k && m0 + m < n;
+        cp_async8(sZ + kk * ldz_s + m, ok ? Z + (m0 + m) + (int64_t)kk * ldz : Z, ok);
+      }
+    cp_async_wait_all();
+    __syncthreads();
+    double w[UPW][MTG][2];
+#pragma unroll
+    for (int u = 0; u < UPW; ++u)
+#pragma unroll
+      for (int i = 0; i < MTG; ++i) w[u][i][0] = w[u][i][1] = 0.0;
+    for (int ks = 0; ks < k4; ks += 4) {
+      const double* zrow = sZ + (ks + t) * ldz_s + g;
+#pragma unroll
+      for (int u = 0; u < UPW; ++u) {
+        const int unit = warp + PG_WARPS * u, nt = unit % NT, mg = unit / NT;
+        const double b = sU[(nt * 8 + g) * ldu_s + ks + t];
+#pragma unroll
+        for (int i = 0; i < MTG; ++i) {
+          const int mt = mg + MG * i;
+          if (mt < mt_n) dmma_8x8x4(w[u][i][0], w[u][i][1], zrow[mt * 8], b);
+        }
+      }
+    }
+    __syncthreads();  // every read of sZ precedes the sW stores
+#pragma unroll
+    for (int u = 0; u < UPW; ++u) {
+      const int unit = warp + PG_WARPS * u, nt = unit % NT, mg = unit / NT;
+#pragma unroll
+      for (int i = 0; i < MTG; ++i) {
+        const int mt = mg + MG * i;
+        if (mt < mt_n) {
+          double* d = sW + (mt * 8 + g) * LDW + nt * 8 + 2 * t;
+          d[0] = w[u][i][0];
+          d[1] = w[u][i][1];
+        }
+      }
+    }
+    __syncthreads();
+    // upper tiles (it <= jt) of W^T W over the block's rb rows (rows past n are zero)
+    for (int ks = 0; ks < rb; ks += 4) {
+      const double* wrow = sW + (ks + t) * LDW + g;
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (warp + PG_WARPS * q < T)
+          dmma_8x8x4(gacc[q][0], gacc[q][1], wrow[tI[q] * 8], wrow[tJ[q] * 8]);
+    }
+    __syncthreads();  // sW is overwritten by the next block's Z
+  }
+  // partial of this CTA: element (i, j) at part[(i + j * SP) * gridDim.x + blockIdx.x]
+  const int P = gridDim.x;
+#pragma unroll
+  for (int q = 0; q < Q; ++q)
+    if (warp + PG_WARPS * q < T) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = tI[q] * 8 + g, j = tJ[q] * 8 + 2 * t + e;
+        part[(size_t)(i + j * SP) * P + blockIdx.x] = gacc[q][e];
+      }
+    }
+  cooperative_groups::this_grid().sync();
+  // G[i, j] = G[j, i] = sum over CTAs, i <= j < s: one warp per element
+  const int64_t ne = (int64_t)s * (s + 1) / 2;
+  for (int64_t e = (int64_t)blockIdx.x * PG_WARPS + warp; e < ne; e += (int64_t)P * PG_WARPS) {
+    int j = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(j + 1) * (j + 2) / 2 <= e) ++j;
+    while ((int64_t)j * (j + 1) / 2 > e) --j;
+    const int i = (int)(e - (int64_t)j * (j + 1) / 2);
+    const double* src = part + (size_t)(i + j * SP) * P;
+    double acc = 0.0;
+    for (int p = lane; p < P; p += 32) acc += __ldcg(src + p);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) {
+      G[i + (int64_t)j * ldg] = acc;
+      G[j + (int64_t)i * ldg] = acc;
+    }
+  }
+}
+
+template <int NT>
+size_t proj_gram_smem(int k, int rb) {
+  const int kp = pg_kpad(k);
+  return sizeof(double) * ((size_t)NT * 8 * (kp + 4) +
+                           std::max<size_t>((size_t)kp * pg_ldz(rb), (size_t)rb * PgShape<NT>::LDW));
+}
+
+template <int NT>
+bool proj_gram_launch(const double* Z, int64_t ldz, int64_t n, int k, const double* U, int64_t ldu,
+                      int s, double* G, int64_t ldg, double* part, size_t part_doubles,
+                      cudaStream_t st) {
+  const int sms = num_sms();
+  int rb = (int)std::min<int64_t>(PG_RMAX, (ceil_div(n, sms) + 7) / 8 * 8);
+  while (rb > 8 && proj_gram_smem<NT>(k, rb) > PG_SMEM) rb -= 8;
+  const size_t smem = proj_gram_smem<NT>(k, rb);
+  if (smem > PG_SMEM) return false;
+  int P = (int)std::min<int64_t>(ceil_div(n, rb), sms);
+  if ((size_t)P * NT * 8 * NT * 8 > part_doubles) return false;
+  static std::mutex attr_mu;
+  static uint64_t attr_mask = 0;
+  per_device_once(attr_mu, attr_mask, [&] {
+    DME_CUDA(cudaFuncSetAttribute(proj_gram_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)PG_SMEM));
+  });
+  int per_sm = 0;
+  DME_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, proj_gram_kernel<NT>,
+                                                         PG_WARPS * 32, smem));
+  if (per_sm < 1) return false;
+  P = std::min(P, per_sm * sms);
+  void* args[] = {(void*)&Z, (void*)&ldz, (void*)&n, (void*)&k, (void*)&U, (void*)&ldu,
+                  (void*)&s, (void*)&rb, (void*)&part, (void*)&G, (void*)&ldg};
+  DME_CUDA(cudaLaunchCooperativeKernel((void*)proj_gram_kernel<NT>, dim3(P), dim3(PG_WARPS * 32), args,
+                                       smem, st));
+  DME_KCHECK();
+  return true;
 }
 
 }  // namespace
@@ -591,6 +775,15 @@ __global__ void spmm_csr_kernel(const int* __restrict__ rp, const int* __restric
   }
 }
 }  // namespace
+
+bool proj_gram(const double* Z, int64_t ldz, int64_t n, int k, const double* U, int64_t ldu, int s,
+               double* G, int64_t ldg, double* part, size_t part_doubles, cudaStream_t st) {
+  if (n <= 0 || s <= 0) return true;
+  if (k > PG_KMAX || s > 96 || s > k) return false;
+  if (s <= 32) return proj_gram_launch<4>(Z, ldz, n, k, U, ldu, s, G, ldg, part, part_doubles, st);
+  if (s <= 64) return proj_gram_launch<8>(Z, ldz, n, k, U, ldu, s, G, ldg, part, part_doubles, st);
+  return proj_gram_launch<12>(Z, ldz, n, k, U, ldu, s, G, ldg, part, part_doubles, st);
+}
 
 void spmm_csr(const int* rp, const int* ci, const double* v, int64_t n, const double* X, int64_t ldx,
               int64_t k, double* out, int64_t ldo, double alpha, cudaStream_t st) {

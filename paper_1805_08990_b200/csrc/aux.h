@@ -35,6 +35,12 @@ void spmm_csr(const int* rp, const int* ci, const double* v, int64_t n, const do
 void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                 int64_t M, int64_t N, int64_t K, cudaStream_t st);
 
+// G = (Z U)^T (Z U) (s x s, both triangles, ld ldg) for Z: n x k column-major, U: k x s (ld ldu),
+// without storing Z U; part: scratch of >= min(ceil(n/64), #SMs) * 96^2 doubles. Deterministic.
+// Returns false (nothing launched) when k > 160, s > 96 or the scratch is too small.
+bool proj_gram(const double* Z, int64_t ldz, int64_t n, int k, const double* U, int64_t ldu, int s,
+               double* G, int64_t ldg, double* part, size_t part_doubles, cudaStream_t st);
+
 // Gram matrix of Zc' = [L_I | LA Tm] (and H = Zc'^T B) from the Gram Gh of GB = [L_I | B | LA]
 // (q, m, kp columns; ld ldh) and Tm (kp x r, ld ldt), without touching the n-row factors:
 //   G = [[Gh_II, Gh_I,LA Tm], [Tm^T Gh_LA,I, Tm^T Gh_LA,LA Tm]]  (k = q + r, column-major, ld ldg)

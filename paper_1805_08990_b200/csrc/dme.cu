@@ -131,6 +131,7 @@ struct dme_ctx {
   double *norm_dev = nullptr, *red_scratch = nullptr, *stage = nullptr;
   double *Zs = nullptr, *Gs = nullptr, *Us = nullptr, *Ts = nullptr;  // refined compression: Zc U, its Gram, U, tail eigenvectors
   bool refine = true;      // options.compression == DME_COMPRESS_REFINED
+  bool no_proj_gram = false;  // DME_NO_PROJ_GRAM: unfused Zs = Zc U + Gram (A/B measurement knob)
   double tol_scale = 1.0;  // intermediate quadrature-ladder compressions run at trunc_tol * LADDER_TOL
   double last_st[5] = {0, 0, 0, 0, 0};  // stats of the last small-kernel pass read by the host
   cudaEvent_t ev_zc = nullptr, ev_tm = nullptr;
@@ -432,6 +433,7 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->h = o->h;
   c->fsal = o->no_fsal == 0;
   c->refine = o->compression == DME_COMPRESS_REFINED;
+  c->no_proj_gram = std::getenv("DME_NO_PROJ_GRAM") != nullptr;
   c->sparse = pr->A == nullptr && pr->A_rowptr != nullptr;
   if (c->sparse) {
     std::string err;
@@ -933,11 +935,19 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
       complement_basis(cp.a.Tm, KMAX, (int)k, (int)kb, c->Us, KMAX, c->st);
     }
     if (zc_ready) DME_CUDA(cudaStreamWaitEvent(c->st, zc_ready, 0));
+    // fused: Zs rows are formed chunk by chunk in shared memory, never stored
+    bool fused;
     {
-      ProfScope ps(c, PROF_APPLY);
-      tall_small(cp.Zc, c->ldn, c->Us, KMAX, c->Zs, c->ldn, c->n, s, k, c->st);
+      ProfScope ps(c, PROF_GRAM);
+      fused = !c->no_proj_gram &&
+              proj_gram(cp.Zc, c->ldn, c->n, (int)k, c->Us, KMAX, (int)s, c->Gs, KMAX, c->gs.partial,
+                        GemmScratch::partial_doubles(c->gs.max_grid), c->st);
     }
-    {
+    if (!fused) {
+      {
+        ProfScope ps(c, PROF_APPLY);
+        tall_small(cp.Zc, c->ldn, c->Us, KMAX, c->Zs, c->ldn, c->n, s, k, c->st);
+      }
       ProfScope ps(c, PROF_GRAM);
       GemmNTArgs g;
       g.A = c->Zs; g.lda = c->ldn; g.B = c->Zs; g.ldb = c->ldn;
