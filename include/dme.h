@@ -294,6 +294,10 @@ dme_status dme_debug_matmul(int64_t M, int64_t N, int64_t K, const double* A, co
 /* The same product through the int8 digit-slicing kernel of the E pass (N <= 64, K <= 32768). */
 dme_status dme_debug_matmul_ozaki(int64_t M, int64_t N, int64_t K, const double* A, const double* B,
                                   double* C);
+/* Orthonormal basis U (k x (k - kb), row-major host array) of the complement of span(W), W (k x kb,
+ * row-major host array, orthonormal columns), through the refined compression's complement-basis
+ * kernel (P:L245-246 tail pass, reading G7'); 0 <= kb < k <= 160. Test hook. */
+dme_status dme_debug_complement(int64_t k, int64_t kb, const double* W, double* U);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdme.so")
+# DME_LIB: another in-tree build of the same library (A/B measurements in tools/); no fallback
+LIB_PATH = os.environ.get("DME_LIB") or os.path.join(_HERE, "libdme.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -98,6 +99,7 @@ for _name, _args in {
                                ctypes.c_int64],
     "dme_debug_matmul": [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp],
     "dme_debug_matmul_ozaki": [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp],
+    "dme_debug_complement": [ctypes.c_int64, ctypes.c_int64, _dp, _dp],
     "dme_debug_small_stats": [_ctx_p, _dp],
     "dme_cheb_coeffs": [ctypes.c_double, ctypes.c_double, _dp, ctypes.c_int64,
                         ctypes.POINTER(ctypes.c_int32)],
@@ -109,7 +111,8 @@ EXPORTED = ["dme_default_options", "dme_status_string", "dme_last_error", "dme_w
             "dme_get_unique_id", "dme_shard_rows", "dme_dle_init", "dme_dre_init", "dme_split_step",
             "dme_get_factor", "dme_extrapolate", "dme_get_stats", "dme_set_profiling", "dme_destroy", "dme_debug_apply",
             "dme_debug_set_factor", "dme_debug_get_exp", "dme_debug_set_exp", "dme_debug_get_integral",
-            "dme_debug_small_stats", "dme_debug_matmul", "dme_debug_matmul_ozaki", "dme_cheb_coeffs"]
+            "dme_debug_small_stats", "dme_debug_matmul", "dme_debug_matmul_ozaki", "dme_cheb_coeffs",
+            "dme_debug_complement"]
 
 
 class DmeError(RuntimeError):
@@ -353,6 +356,16 @@ def matmul_ozaki(A, B):
     _check(_lib.dme_debug_matmul_ozaki(A.shape[0], B.shape[1], A.shape[1], _ptr(A), _ptr(B),
                                        _ptr(C)), "dme_debug_matmul_ozaki")
     return C
+
+
+def complement_basis(W):
+    """Orthonormal basis (k x (k - kb)) of the complement of span(W) (W: k x kb, orthonormal
+    columns) through the refined compression's complement-basis kernel (test hook)."""
+    W = _f64(W)
+    k, kb = W.shape
+    U = np.zeros((k, k - kb))
+    _check(_lib.dme_debug_complement(k, kb, _ptr(W), _ptr(U)), "dme_debug_complement")
+    return U
 
 
 def matmul(A, B):

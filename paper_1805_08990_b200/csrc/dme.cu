@@ -2131,6 +2131,27 @@ dme_status dme_debug_small_stats(dme_ctx* c, double* out16) {
   });
 }
 
+dme_status dme_debug_complement(int64_t k, int64_t kb, const double* W, double* U) {
+  return guarded(nullptr, [&] {
+    DME_REQUIRE(W && U && kb >= 0 && kb < k && k <= FAST_K_MAX, DME_ERR_INVALID, "bad complement args");
+    const int64_t s = k - kb;
+    std::vector<double> wc((size_t)k * (kb > 0 ? kb : 1)), uc((size_t)k * s);
+    for (int64_t i = 0; i < k; ++i)
+      for (int64_t j = 0; j < kb; ++j) wc[j * k + i] = W[i * kb + j];  // column-major, ld k
+    double *dW, *dU;
+    DME_CUDA(cudaMalloc(&dW, wc.size() * 8));
+    DME_CUDA(cudaMalloc(&dU, uc.size() * 8));
+    DME_CUDA(cudaMemcpy(dW, wc.data(), wc.size() * 8, cudaMemcpyHostToDevice));
+    complement_basis(dW, k, (int)k, (int)kb, dU, k, nullptr);
+    DME_CUDA(cudaDeviceSynchronize());
+    DME_CUDA(cudaMemcpy(uc.data(), dU, uc.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dW);
+    cudaFree(dU);
+    for (int64_t i = 0; i < k; ++i)
+      for (int64_t j = 0; j < s; ++j) U[i * s + j] = uc[j * k + i];
+  });
+}
+
 dme_status dme_debug_matmul(int64_t M, int64_t N, int64_t K, const double* A, const double* B,
                             double* C) {
   return guarded(nullptr, [&] {

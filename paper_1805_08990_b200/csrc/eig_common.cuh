@@ -65,6 +65,15 @@ __device__ __forceinline__ double frcp(double x) {
   return fma(r, t, r);
 }
 
+// x / d for 0 <= x < 2^20, 0 < d < 2^12 without the integer-division sequence (float reciprocal
+// estimate, corrected by one step either way)
+__device__ __forceinline__ int udiv_small(int x, int d) {
+  int q = __float2int_rz(__fmul_rz((float)x, __frcp_rn((float)d)));
+  if ((q + 1) * d <= x) ++q;
+  if (q * d > x) --q;
+  return q;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -163,14 +172,31 @@ __device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, d
       } else {
         // rows 1..m-1 of the trailing block by the other warps: thread per column l, rows strided
         const int t2 = tid - 32, nt2 = ENT - 32;
-        const int rg = nt2 / m;  // row groups
-        const int l = t2 % m, grp = t2 / m;
+        const int rg = udiv_small(nt2, m);  // row groups
+        const int grp = udiv_small(t2, m), l = t2 - grp * m;
         if (grp < rg) {
           const double vl = vj[l], wl = pv[l] - K * vl;
-          for (int i = 1 + grp; i < m; i += rg) {
+          double* col = A + (j + 1) * ld + (j + 1 + l);
+          int i = 1 + grp;
+          // four rows per round with the loads first (in-order issue: the stores then do not hold
+          // back the next row's shared-memory loads)
+          for (; i + 3 * rg < m; i += 4 * rg) {
+            double av[4], vi[4], pi[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              vi[u] = vj[i + u * rg];
+              pi[u] = pv[i + u * rg];
+              av[u] = col[(i + u * rg) * ld];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double wi = pi[u] - K * vi[u];
+              col[(i + u * rg) * ld] = av[u] - (vi[u] * wl + wi * vl);
+            }
+          }
+          for (; i < m; i += rg) {
             const double vi = vj[i], wi = pv[i] - K * vi;
-            double* a_ = A + (j + 1 + i) * ld + (j + 1 + l);
-            *a_ -= vi * wl + wi * vl;
+            col[i * ld] -= vi * wl + wi * vl;
           }
         }
       }

@@ -47,12 +47,36 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
   const int tid = threadIdx.x;
   const int k = a.k, ld = k | 1;
   const EsLayout es{a.Es, SMALL_K_MAX};
-  for (int e_ = tid; e_ < k * k; e_ += ENT) {
-    const int i = e_ % k, j = e_ / k;
-    A[i * ld + j] = 0.5 * (a.G[i + (size_t)j * a.ldg] + a.G[j + (size_t)i * a.ldg]);
+  const long long t_in = clock64();
+  {
+    // column j of G into row j of A (coalesced, 8 loads in flight per thread), then the exact
+    // symmetrisation A = (G + G^T) / 2 in shared memory
+    constexpr int B = 8;
+    for (int e0 = tid; e0 < k * k; e0 += B * ENT) {
+      double v[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int e_ = e0 + u * ENT;
+        v[u] = e_ < k * k ? a.G[(e_ % k) + (size_t)(e_ / k) * a.ldg] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int e_ = e0 + u * ENT;
+        if (e_ < k * k) A[(e_ / k) * ld + (e_ % k)] = v[u];
+      }
+    }
+    __syncthreads();
+    for (int e_ = tid; e_ < k * k; e_ += ENT) {
+      const int i = e_ % k, j = e_ / k;
+      if (i < j) {
+        const double v = 0.5 * (A[i * ld + j] + A[j * ld + i]);
+        A[i * ld + j] = v;
+        A[j * ld + i] = v;
+      }
+    }
   }
-  const long long t0 = clock64();
   __syncthreads();
+  const long long t0 = clock64();
   tridiagonalise<FK>(A, k, ld, d, e, tau, vec, pv, pv2);
   const long long t1 = clock64();
   {
@@ -137,6 +161,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
     h[3] = tmax;
     h[4] = (double)r;
     if (a.stats) {  // phase cycles (tools/eig_split_probe.py)
+      a.stats[6] = (double)(t0 - t_in);
       a.stats[8] = (double)(t1 - t0);
       a.stats[9] = (double)(clock64() - t1);
     }
@@ -149,6 +174,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
   }
   double* R = es.refl();
   for (int e_ = tid; e_ < k * ld; e_ += ENT) R[e_] = A[e_];
+  if (a.stats) {  // whole-kernel cycles (entry to last store issued)
+    __syncthreads();
+    if (tid == 0) a.stats[7] = (double)(clock64() - t_in);
+  }
 }
 
 template <int FK>
@@ -173,14 +202,26 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   const int nb = c1 - c0;
   if (nb <= 0) return;
   const double scale = h[0], glo = h[1], ghi = h[2];
+  // the reflectors (k x ld doubles, contiguous) by one bulk async copy (rounded up to 16 bytes: the
+  // scratch and the shared buffer both have room), the tridiagonal by the threads meanwhile
+  __shared__ uint64_t rbar;
+  const uint32_t rbytes = ((uint32_t)(k * ld) * 8u + 15u) & ~15u;
+  if (tid == 0) {
+    mbar_init(&rbar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&rbar, rbytes);
+    for (uint32_t off = 0; off < rbytes; off += 32768u)
+      bulk_load(reinterpret_cast<char*>(R) + off, reinterpret_cast<const char*>(es.refl()) + off,
+                rbytes - off < 32768u ? rbytes - off : 32768u, &rbar);
+  }
   for (int i = tid; i < k; i += ENT) {
     d[i] = es.d()[i];
     e[i] = es.e()[i];
     e2[i] = es.e2()[i];
     tau[i] = es.tau()[i];
   }
-  for (int e_ = tid; e_ < k * ld; e_ += ENT) R[e_] = es.refl()[e_];
-  __syncthreads();
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  mbar_wait(&rbar, 0);
 
   // ------------------------------------------------------------ multisection on this slice
   t_ph[1] = clock64();
@@ -581,6 +622,7 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
       const int fin_x = (int)(sizeof(double) * 3 * (size_t)FK * SMALL_M_MAX);
       mx += vec_x > fin_x ? vec_x : fin_x;
     }
+    mx += 2 * (int)sizeof(double);  // VEC's rounded-up reflector copy
     DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_vec_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_fin_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -588,7 +630,9 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
   eig_tri_kernel<FK><<<1, ENT, smem, st>>>(a);
   DME_KCHECK();
   constexpr int MAXE = (FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1;
-  const size_t vsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * MAXE * FK) : smem;
+  // (+ 2 doubles: the bulk copy of the reflectors is rounded up to 16 bytes)
+  const size_t vsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * MAXE * FK + 2)
+                                : smem + 2 * sizeof(double);
   eig_vec_kernel<FK><<<EIG_SPLIT_CTAS, ENT, vsmem > smem ? vsmem : smem, st>>>(a);
   DME_KCHECK();
   const size_t fsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * (size_t)a.k * SMALL_M_MAX +

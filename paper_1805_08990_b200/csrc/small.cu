@@ -19,6 +19,7 @@
 #include "small_common.cuh"
 
 #include <cmath>
+#include <cstdlib>
 
 namespace dme {
 
@@ -274,8 +275,10 @@ __global__ void __launch_bounds__(NT) complement_basis_kernel(const double* __re
     double t = 0.0, scal = 0.0;
     if (n2 > 0.0) {
       const double beta = -copysign(sqrt(fma(alpha, alpha, n2)), alpha);
-      scal = 1.0 / (alpha - beta);
-      t = (beta - alpha) / beta;
+      const double amb = alpha - beta;
+      const double inv = 1.0 / (amb * beta);  // one division for both quotients
+      scal = beta * inv;                      // 1 / (alpha - beta)
+      t = -amb * amb * inv;                   // (beta - alpha) / beta
     }
 #pragma unroll
     for (int u = 0; u < RPL; ++u) {
@@ -318,27 +321,162 @@ __global__ void __launch_bounds__(NT) complement_basis_kernel(const double* __re
     }
   }
   __syncthreads();
-  // U = H_0 ... H_{kb-1} [0; I_s]: column t of U starts as e_{kb + t}
+  // U = H_0 ... H_{kb-1} [0; I_s]: column t of U starts as e_{kb + t}. Eight lanes per column
+  // (rows sub + 8u), so a reflector costs each column a 3-level shuffle reduction (instead of a
+  // 5-level one per column and per warp slot): the phase is bound by the SM's shuffle throughput.
+  // (k > 96: a whole warp per column, as in phase 1, to stay within 64 registers)
+  constexpr int LPC = RPL * CPW <= 9 ? 8 : 32;      // lanes per column
+  constexpr int NG = NT / LPC;                      // column groups
+  constexpr int R8 = (32 * RPL + LPC - 1) / LPC;    // rows per lane
+  constexpr int CPG = (32 * CPW + NG - 1) / NG;     // columns per group
+  const int sub = lane & (LPC - 1), grp = tid / LPC;
+  double y[CPG][R8];
 #pragma unroll
-  for (int q = 0; q < CPW; ++q) {
-    const int t = warp + 32 * q;
+  for (int q = 0; q < CPG; ++q)
 #pragma unroll
-    for (int u = 0; u < RPL; ++u) x[q][u] = (lane + 32 * u == kb + t) ? 1.0 : 0.0;
+    for (int u = 0; u < R8; ++u) y[q][u] = (sub + LPC * u == kb + grp + NG * q) ? 1.0 : 0.0;
+  for (int j = kb - 1; j >= 0; --j) {
+    const double t = tau_s[j];
+    if (t == 0.0) continue;
+    double vv[R8];
+#pragma unroll
+    for (int u = 0; u < R8; ++u) {
+      const int i = sub + LPC * u;
+      vv[u] = i < k ? Vh[j * ld + i] : 0.0;
+    }
+    double d[CPG];
+#pragma unroll
+    for (int q = 0; q < CPG; ++q) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int u = 0; u < R8; u += 2) {
+        d0 = fma(vv[u], y[q][u], d0);
+        if (u + 1 < R8) d1 = fma(vv[u + 1], y[q][u + 1], d1);
+      }
+      d[q] = d0 + d1;
+    }
+#pragma unroll
+    for (int o = 1; o < LPC; o <<= 1)
+#pragma unroll
+      for (int q = 0; q < CPG; ++q) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+#pragma unroll
+    for (int q = 0; q < CPG; ++q) {
+      const double dq = t * d[q];
+#pragma unroll
+      for (int u = 0; u < R8; ++u) y[q][u] = fma(-dq, vv[u], y[q][u]);
+    }
   }
-  for (int j = kb - 1; j >= 0; --j)
 #pragma unroll
-    for (int q = 0; q < CPW; ++q)
-      if (warp + 32 * q < s) apply(j, q);
-#pragma unroll
-  for (int q = 0; q < CPW; ++q) {
-    const int t = warp + 32 * q;
+  for (int q = 0; q < CPG; ++q) {
+    const int t = grp + NG * q;
     if (t < s)
 #pragma unroll
-      for (int u = 0; u < RPL; ++u) {
-        const int i = lane + 32 * u;
-        if (i < k) U[i + (size_t)t * ldu] = x[q][u];
+      for (int u = 0; u < R8; ++u) {
+        const int i = sub + LPC * u;
+        if (i < k) U[i + (size_t)t * ldu] = y[q][u];
       }
   }
+}
+
+// Complement basis for k <= 96 by Householder reconstruction from an LU factorisation (Ballard,
+// Demmel, Grigori, Jacquelin, Nguyen, Solomonik 2014: "Reconstructing Householder vectors from
+// tall-skinny QR"). W (k x kb) has orthonormal columns, so its Householder QR is W = Q [S; 0] with
+// S = diag(+-1) and Q = I - Y T Y^T; then W - [S; 0] = Y (-T Y1^T S) is an LU factorisation
+// (Y unit lower trapezoidal, Y1 its leading kb x kb block) that needs no pivoting when s_j is taken
+// as -sign of the current diagonal entry (|u_jj| >= 1). The trailing columns of Q are
+//   U = Q [0; I_s] = [0; I_s] - Y T Y2^T = [0; I_s] + Y (U_lu S Z^T),   Z = Y2 Y1^{-1}  (s x kb).
+// Same U as the column-by-column kernel below in exact arithmetic; its kb sequential steps are plain
+// rank-1 updates (one division, no norms or reductions, one barrier), and the rest is small
+// products that all 1024 threads share.
+__device__ __forceinline__ int cdiv_small(int x, int d) {  // x / d, 0 <= x < 2^20, 0 < d < 2^12
+  int q = __float2int_rz(__fmul_rz((float)x, __frcp_rn((float)d)));
+  if ((q + 1) * d <= x) ++q;
+  if (q * d > x) --q;
+  return q;
+}
+
+constexpr int CLU_KMAX = 96;
+
+__global__ void __launch_bounds__(NT) complement_lu_kernel(const double* __restrict__ W, int64_t ldw, int k,
+                                                           int kb, double* __restrict__ U, int64_t ldu) {
+  extern __shared__ double sm[];
+  __shared__ double sg[CLU_KMAX], ud[CLU_KMAX];
+  const int tid = threadIdx.x, s = k - kb;
+  double* Ms = sm;                         // k x kb (ld k): W, reduced in place; rows < kb end as U_lu
+  double* Ls = Ms + (size_t)k * kb;        // k x kb (ld k): Y below the diagonal
+  double* Zs = Ls + (size_t)k * kb;        // s x kb (ld s): Z = Y2 Y1^{-1}
+  double* M2 = Zs + (size_t)s * kb;        // kb x s (ld kb): U_lu S Z^T
+  {
+    constexpr int B = 4;
+    for (int e0 = tid; e0 < k * kb; e0 += B * NT) {
+      double v[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int e = e0 + u * NT;
+        if (e < k * kb) {
+          const int c = cdiv_small(e, k);
+          v[u] = W[(e - c * k) + (size_t)c * ldw];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (e0 + u * NT < k * kb) Ms[e0 + u * NT] = v[u];
+    }
+  }
+  __syncthreads();
+  // LU of W - [S; 0], right-looking, one barrier per step (column j of L goes to Ls, so the
+  // step's reads of column j and row j of Ms never race with its writes)
+  for (int j = 0; j < kb; ++j) {
+    const double mjj = Ms[j + j * k];
+    const double sj = mjj >= 0.0 ? -1.0 : 1.0;
+    const double ujj = mjj - sj;  // |u_jj| >= 1
+    const double rj = 1.0 / ujj;
+    const int rows = k - j - 1, cols = kb - j;
+    for (int e = tid; e < rows * cols; e += NT) {
+      const int cc = cdiv_small(e, rows);
+      const int i = j + 1 + (e - cc * rows), c = j + cc;
+      const double lij = Ms[i + j * k] * rj;
+      if (c == j) Ls[i + j * k] = lij;
+      else Ms[i + c * k] -= lij * Ms[j + c * k];
+    }
+    if (tid == 0) {
+      sg[j] = sj;
+      ud[j] = ujj;
+    }
+    __syncthreads();
+  }
+  // Z = Y2 Y1^{-1}: row r solves z Y1 = y2 (Y1 unit lower triangular), one thread per row
+  if (tid < s) {
+    const int r = tid;
+    for (int i = 0; i < kb; ++i) Zs[r + i * s] = Ls[kb + r + i * k];
+    for (int l = kb - 1; l > 0; --l) {
+      const double zl = Zs[r + l * s];
+      for (int i = 0; i < l; ++i) Zs[r + i * s] = fma(-zl, Ls[l + i * k], Zs[r + i * s]);
+    }
+  }
+  __syncthreads();
+  // M2 = U_lu S Z^T  (kb x s): M2[i][r] = sum_{l >= i} U[i][l] s_l Z[r][l]
+  for (int e = tid; e < kb * s; e += NT) {
+    const int r = cdiv_small(e, kb), i = e - r * kb;
+    double acc = ud[i] * sg[i] * Zs[r + i * s];
+    for (int l = i + 1; l < kb; ++l) acc = fma(Ms[i + l * k] * sg[l], Zs[r + l * s], acc);
+    M2[i + r * kb] = acc;
+  }
+  __syncthreads();
+  // U = [0; I_s] + Y M2  (k x s): Y[row][i] = 1 (row == i), Ls[row + i k] (row > i), 0 (row < i)
+  for (int e = tid; e < k * s; e += NT) {
+    const int r = cdiv_small(e, k), row = e - r * k;
+    double acc = (row == kb + r) ? 1.0 : 0.0;
+    const int imax = row < kb ? row : kb;  // i < imax: Y[row][i] = Ls
+    for (int i = 0; i < imax; ++i) acc = fma(Ls[row + i * k], M2[i + r * kb], acc);
+    if (row < kb) acc += M2[row + r * kb];
+    U[row + (size_t)r * ldu] = acc;
+  }
+}
+
+size_t complement_lu_smem(int k, int kb) {
+  const int s = k - kb;
+  return sizeof(double) * (2 * (size_t)k * kb + 2 * (size_t)s * kb + 2);
 }
 
 __global__ void tail_product_kernel(double* Tm, int64_t ldt, const double* __restrict__ U, int64_t ldu,
@@ -410,9 +548,14 @@ void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, in
   per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(complement_basis_kernel<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(complement_basis_kernel<5, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DME_CUDA(cudaFuncSetAttribute(complement_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)complement_lu_smem(CLU_KMAX, CLU_KMAX)));
   });
   const size_t smem = sizeof(double) * (size_t)(kb > 0 ? kb : 1) * (k | 1);
-  if (k <= 96) complement_basis_kernel<3, 3><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
+  static const bool old_cb = std::getenv("DME_CB_HOUSEHOLDER") != nullptr;  // A/B knob
+  if (k <= CLU_KMAX && !old_cb)
+    complement_lu_kernel<<<1, NT, complement_lu_smem(k, kb), st>>>(W, ldw, k, kb, U, ldu);
+  else if (k <= 96) complement_basis_kernel<3, 3><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   else complement_basis_kernel<5, 5><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   DME_KCHECK();
 }

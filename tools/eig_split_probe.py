@@ -13,6 +13,6 @@ for k in (64, 90, 96):
         s.debug_set_factor(L); s.debug_apply("compress", 0.0)
     torch.cuda.synchronize()
     ss = s.debug_small_stats()
-    print(k, "rank", s.get_factor()[0].shape[1], "kcycles: tri %.1f tmax %.1f | vec load %.1f msec %.1f twist %.1f backtr %.1f"
+    print(k, "rank", s.get_factor()[0].shape[1], "tri-load %.1f" % (ss[6] / 1e3), "kcycles: tri %.1f tmax %.1f | vec load %.1f msec %.1f twist %.1f backtr %.1f"
           % tuple(ss[8:14] / 1e3))
     print("    fin kcycles: load %.1f check %.1f t3 %.1f" % (ss[14] / 1e3, ss[15] / 1e3, ss[5] / 1e3))
