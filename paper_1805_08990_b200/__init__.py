@@ -104,6 +104,8 @@ for _name, _args in {
     "dme_cheb_coeffs": [ctypes.c_double, ctypes.c_double, _dp, ctypes.c_int64,
                         ctypes.POINTER(ctypes.c_int32)],
 }.items():
+    if os.environ.get("DME_LIB") and not hasattr(_lib, _name):
+        continue  # an older build under A/B measurement may lack newer test hooks
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = ctypes.c_int
 

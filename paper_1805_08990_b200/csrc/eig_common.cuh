@@ -11,6 +11,20 @@ namespace eigk {
 constexpr int ENT = 512;  // threads of the eigen kernels (16 warps, up to 128 registers each)
 constexpr int NW = ENT / 32;
 
+// Exact power-of-two rescaling of a pair of consecutive minors to ~1 when they leave [2^-64, 2^64]
+// (the ratios and signs the callers need are unchanged; a block of 8 recurrence steps then cannot
+// overflow for ||T|| <= 1 nor underflow unless the pivots fall below ~2^-120 each)
+__device__ __forceinline__ void rescale_pair(double& p1, double& p2) {
+  const double m1 = fmax(fabs(p1), fabs(p2));
+  if (m1 > 0x1p64 || (m1 < 0x1p-64 && m1 > 0.0)) {
+    int ex;
+    frexp(m1, &ex);
+    const double sc = ldexp(1.0, -ex);
+    p1 *= sc;
+    p2 *= sc;
+  }
+}
+
 // number of eigenvalues of T (d, e2 = e^2, normalised to ||T|| <= 1) smaller than x:
 // sign changes of the leading principal minors p_i of T - xI (an exact zero counts as negative,
 // a measure-zero event that only moves a bisection probe by one count)
@@ -21,8 +35,9 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
   int cnt = neg_prev;
   int i = 1;
   // blocks of 8: the loads are independent of the recurrence and issue ahead of it; the exact
-  // power-of-two rescaling is checked once per block (|p| grows <= 3^8 per block for ||T|| <= 1,
-  // and a block cannot underflow from 2^-300 to below the normal range)
+  // power-of-two rescaling to ~1 is checked once per block (|p| grows <= 3^8 per block for
+  // ||T|| <= 1; a fixed 2^300 step could not keep up with strongly graded T, whose minors then
+  // underflowed to zero and stopped counting)
   for (; i + 7 < k; i += 8) {
     double dd[8], ff[8];
 #pragma unroll
@@ -39,9 +54,7 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
       p2 = p1;
       p1 = p;
     }
-    const double m1 = fmax(fabs(p1), fabs(p2));
-    if (m1 > 0x1p300) { p1 *= 0x1p-300; p2 *= 0x1p-300; }
-    else if (m1 < 0x1p-300) { p1 *= 0x1p300; p2 *= 0x1p300; }
+    rescale_pair(p1, p2);
   }
   for (; i < k; ++i) {
     const double p = fma(d[i] - x, p1, -e2[i - 1] * p2);
@@ -74,6 +87,44 @@ __device__ __forceinline__ int udiv_small(int x, int d) {
   return q;
 }
 
+// Pivots of the twisted factorisation of T - lm I (d, e2 = e^2 of the normalised T): forward
+// (fwd: D+_i = p_i / p_{i-1}, p_i the leading principal minors) or backward (D-_i from the trailing
+// minors). The minors follow the division-free three-term recurrence (one FMA per row on the
+// dependency chain, rescaled per block of 8); the ratios are formed off the chain. Same pivots as
+// the ratio recurrence D_i = (d_i - lm) - e2 / D_{i-1} up to rounding; |D_i| < pivmin (or a
+// 0/0 ratio) becomes -pivmin as there.
+__device__ inline void twisted_pivots(const double* __restrict__ d, const double* __restrict__ e2, int k,
+                                      double lm, bool fwd, double* __restrict__ D) {
+  constexpr double pivmin = 1e-290;
+  auto row = [&](int t) { return fwd ? t : k - 1 - t; };
+  auto cpl = [&](int t) { return fwd ? t - 1 : k - 1 - t; };  // e2 index coupling rows t-1, t
+  auto clampd = [&](double x) { return fabs(x) >= pivmin ? x : -pivmin; };
+  double p2 = 1.0, p1 = d[row(0)] - lm;
+  D[row(0)] = clampd(p1);
+  int t = 1;
+  for (; t + 7 < k; t += 8) {
+    double pb[8];
+    const double prev = p1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double p = fma(d[row(t + u)] - lm, p1, -e2[cpl(t + u)] * p2);
+      p2 = p1;
+      p1 = p;
+      pb[u] = p;
+    }
+    D[row(t)] = clampd(pb[0] * frcp(prev));
+#pragma unroll
+    for (int u = 1; u < 8; ++u) D[row(t + u)] = clampd(pb[u] * frcp(pb[u - 1]));
+    rescale_pair(p1, p2);
+  }
+  for (; t < k; ++t) {
+    const double p = fma(d[row(t)] - lm, p1, -e2[cpl(t)] * p2);
+    D[row(t)] = clampd(p * frcp(p1));
+    p2 = p1;
+    p1 = p;
+  }
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -83,7 +134,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Householder tridiagonalisation of the symmetric k x k matrix in A (row stride ld, shared
 // memory), in place: d, e (unnormalised) and tau; reflector j kept in row j (v_0 = 1 implicit).
-template <int FK>
+template <int FK, int NTH = ENT>
 __device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, double* tau,
                                double* vec, double* pv, double* pv2) {
   constexpr int RCH = (FK + 31) / 32;
@@ -135,7 +186,7 @@ __device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, d
     const double tj = tau[j];
     // p = tau A22 v by columns (A symmetric): thread i sums A[l][i] v_l over the trailing rows l
     if (tj != 0.0) {
-      for (int i = tid; i < m; i += ENT) {
+      for (int i = tid; i < m; i += NTH) {
         const double* col = A + (j + 1) * ld + (j + 1 + i);
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int l = 0;
@@ -171,7 +222,7 @@ __device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, d
         if (j + 3 < k) householder(j + 1, vn);
       } else {
         // rows 1..m-1 of the trailing block by the other warps: thread per column l, rows strided
-        const int t2 = tid - 32, nt2 = ENT - 32;
+        const int t2 = tid - 32, nt2 = NTH - 32;
         const int rg = udiv_small(nt2, m);  // row groups
         const int grp = udiv_small(t2, m), l = t2 - grp * m;
         if (grp < rg) {

@@ -156,26 +156,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
     const double lm = lam[c];
     double* Dp = a.V + (size_t)c * a.ldv;
     double* Dm = a.Tm + (size_t)c * a.ldt;
-    const double pivmin = 1e-290;
-    if (side == 0) {
-      double x = d[0] - lm;
-      if (fabs(x) < pivmin) x = -pivmin;
-      Dp[0] = x;
-      for (int i = 1; i < k; ++i) {
-        x = (d[i] - lm) - e2[i - 1] / x;
-        if (fabs(x) < pivmin) x = -pivmin;
-        Dp[i] = x;
-      }
-    } else {
-      double x = d[k - 1] - lm;
-      if (fabs(x) < pivmin) x = -pivmin;
-      Dm[k - 1] = x;
-      for (int i = k - 2; i >= 0; --i) {
-        x = (d[i] - lm) - e2[i] / x;
-        if (fabs(x) < pivmin) x = -pivmin;
-        Dm[i] = x;
-      }
-    }
+    twisted_pivots(d, e2, k, lm, side == 0, side == 0 ? Dp : Dm);
     __syncwarp(msk);
     __threadfence_block();
     // twist index: argmin |gamma_i|, the two lanes scan halves

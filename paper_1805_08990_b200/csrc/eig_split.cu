@@ -15,6 +15,7 @@
 #include "small_common.cuh"
 
 #include <cmath>
+#include <cstdlib>
 
 namespace dme {
 
@@ -38,8 +39,10 @@ struct EsLayout {
   __host__ __device__ double* dm() const { return dp() + (size_t)KM * KM; }
 };
 
-template <int FK>
-__global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
+// NTH threads (512; DME_TRI_THREADS = 256 or 128 for k <= 96: A/B of the per-step latency)
+template <int FK, int NTH>
+__global__ void __launch_bounds__(NTH, 1) eig_tri_kernel(SmallArgs a) {
+  constexpr int NWT = NTH / 32;
   extern __shared__ double A[];
   __shared__ double d[FK], e[FK], e2[FK], tau[FK], vec[FK], pv[FK], pv2[FK];
   __shared__ int cnt_s[256];
@@ -52,21 +55,21 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
     // column j of G into row j of A (coalesced, 8 loads in flight per thread), then the exact
     // symmetrisation A = (G + G^T) / 2 in shared memory
     constexpr int B = 8;
-    for (int e0 = tid; e0 < k * k; e0 += B * ENT) {
+    for (int e0 = tid; e0 < k * k; e0 += B * NTH) {
       double v[B];
 #pragma unroll
       for (int u = 0; u < B; ++u) {
-        const int e_ = e0 + u * ENT;
+        const int e_ = e0 + u * NTH;
         v[u] = e_ < k * k ? a.G[(e_ % k) + (size_t)(e_ / k) * a.ldg] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < B; ++u) {
-        const int e_ = e0 + u * ENT;
+        const int e_ = e0 + u * NTH;
         if (e_ < k * k) A[(e_ / k) * ld + (e_ % k)] = v[u];
       }
     }
     __syncthreads();
-    for (int e_ = tid; e_ < k * k; e_ += ENT) {
+    for (int e_ = tid; e_ < k * k; e_ += NTH) {
       const int i = e_ % k, j = e_ / k;
       if (i < j) {
         const double v = 0.5 * (A[i * ld + j] + A[j * ld + i]);
@@ -77,12 +80,12 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
   }
   __syncthreads();
   const long long t0 = clock64();
-  tridiagonalise<FK>(A, k, ld, d, e, tau, vec, pv, pv2);
+  tridiagonalise<FK, NTH>(A, k, ld, d, e, tau, vec, pv, pv2);
   const long long t1 = clock64();
   {
     // normalise T by a Gershgorin bound of ||T|| (same arithmetic as normalise_tridiagonal, in
     // parallel: one row per thread, block max/min reductions)
-    __shared__ double rmax[NW], rlo[NW], rhi[NW];
+    __shared__ double rmax[NWT], rlo[NWT], rhi[NWT];
     const int lane = tid & 31, warp = tid >> 5;
     double rr = 0.0, di = 0.0;
     if (tid < k) {
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
     if (lane == 0) rmax[warp] = m;
     __syncthreads();
     double nrm = 0.0;
-    for (int w = 0; w < NW; ++w) nrm = fmax(nrm, rmax[w]);
+    for (int w = 0; w < NWT; ++w) nrm = fmax(nrm, rmax[w]);
     if (!(nrm > 0.0)) nrm = 1.0;
     const double inv = 1.0 / nrm;
     __syncthreads();  // every thread has read the old d, e
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
     __syncthreads();
     if (tid == 0) {
       double l2 = 1e300, h2 = -1e300;
-      for (int w = 0; w < NW; ++w) { l2 = fmin(l2, rlo[w]); h2 = fmax(h2, rhi[w]); }
+      for (int w = 0; w < NWT; ++w) { l2 = fmin(l2, rlo[w]); h2 = fmax(h2, rhi[w]); }
       s_scale = nrm;
       s_lo = l2 - 1e-14;
       s_hi = h2 + 1e-14;
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
   }
   __syncthreads();
   // theta_max to 16 bits (enough for the threshold; it is refined with the others in VEC)
-  constexpr int PB = 256;
+  constexpr int PB = NTH < 256 ? NTH : 256;
   for (int it = 0; it < 2; ++it) {
     const double a0 = s_lo_t, b0 = s_hi_t;
     if (tid < PB) cnt_s[tid] = sturm_count(d, e2, k, a0 + (b0 - a0) * (tid + 1) / (PB + 1.0));
@@ -166,14 +169,14 @@ __global__ void __launch_bounds__(ENT, 1) eig_tri_kernel(SmallArgs a) {
       a.stats[9] = (double)(clock64() - t1);
     }
   }
-  for (int i = tid; i < k; i += ENT) {
+  for (int i = tid; i < k; i += NTH) {
     es.d()[i] = d[i];
     es.e()[i] = e[i];
     es.e2()[i] = e2[i];
     es.tau()[i] = tau[i];
   }
   double* R = es.refl();
-  for (int e_ = tid; e_ < k * ld; e_ += ENT) R[e_] = A[e_];
+  for (int e_ = tid; e_ < k * ld; e_ += NTH) R[e_] = A[e_];
   if (a.stats) {  // whole-kernel cycles (entry to last store issued)
     __syncthreads();
     if (tid == 0) a.stats[7] = (double)(clock64() - t_in);
@@ -279,26 +282,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
     // FK <= 96: the twisted-factorisation arrays live in shared memory behind the reflectors
     double* Dp = FK <= 96 ? R + k * ld + (tid >> 1) * FK : es.dp() + (size_t)c * SMALL_K_MAX;
     double* Dm = FK <= 96 ? R + k * ld + (MAXE + (tid >> 1)) * FK : es.dm() + (size_t)c * SMALL_K_MAX;
-    const double pivmin = 1e-290;
-    if (side == 0) {
-      double x = d[0] - lm;
-      if (fabs(x) < pivmin) x = -pivmin;
-      Dp[0] = x;
-      for (int i = 1; i < k; ++i) {
-        x = (d[i] - lm) - e2[i - 1] * frcp(x);
-        if (fabs(x) < pivmin) x = -pivmin;
-        Dp[i] = x;
-      }
-    } else {
-      double x = d[k - 1] - lm;
-      if (fabs(x) < pivmin) x = -pivmin;
-      Dm[k - 1] = x;
-      for (int i = k - 2; i >= 0; --i) {
-        x = (d[i] - lm) - e2[i] * frcp(x);
-        if (fabs(x) < pivmin) x = -pivmin;
-        Dm[i] = x;
-      }
-    }
+    twisted_pivots(d, e2, k, lm, side == 0, side == 0 ? Dp : Dm);
     __syncwarp(msk);
     __threadfence_block();
     const int h0 = side ? k / 2 : 0, h1 = side ? k : k / 2;
@@ -623,17 +607,32 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
       mx += vec_x > fin_x ? vec_x : fin_x;
     }
     mx += 2 * (int)sizeof(double);  // VEC's rounded-up reflector copy
-    DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    if (FK <= 96) {
+      DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      DME_CUDA(cudaFuncSetAttribute(eig_tri_kernel<FK, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    }
     DME_CUDA(cudaFuncSetAttribute(eig_vec_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_fin_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   });
-  eig_tri_kernel<FK><<<1, ENT, smem, st>>>(a);
+  static const int tri_nth = [] {
+    const char* e = std::getenv("DME_TRI_THREADS");
+    return e ? std::atoi(e) : 512;
+  }();
+  if (FK <= 96 && tri_nth == 128) eig_tri_kernel<FK, 128><<<1, 128, smem, st>>>(a);
+  else if (FK <= 96 && tri_nth == 256) eig_tri_kernel<FK, 256><<<1, 256, smem, st>>>(a);
+  else eig_tri_kernel<FK, 512><<<1, 512, smem, st>>>(a);
   DME_KCHECK();
   constexpr int MAXE = (FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1;
   // (+ 2 doubles: the bulk copy of the reflectors is rounded up to 16 bytes)
   const size_t vsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * MAXE * FK + 2)
                                 : smem + 2 * sizeof(double);
-  eig_vec_kernel<FK><<<EIG_SPLIT_CTAS, ENT, vsmem > smem ? vsmem : smem, st>>>(a);
+  static const int vec_ctas = [] {
+    const char* e = std::getenv("DME_VEC_CTAS");
+    const int v = e ? std::atoi(e) : EIG_SPLIT_CTAS;
+    return v < EIG_SPLIT_CTAS ? EIG_SPLIT_CTAS : v;  // MAXE is sized for >= EIG_SPLIT_CTAS CTAs
+  }();
+  eig_vec_kernel<FK><<<vec_ctas, ENT, vsmem > smem ? vsmem : smem, st>>>(a);
   DME_KCHECK();
   const size_t fsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * (size_t)a.k * SMALL_M_MAX +
                                                   (size_t)a.k * SMALL_M_MAX)

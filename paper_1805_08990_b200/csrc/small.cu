@@ -378,105 +378,91 @@ __global__ void __launch_bounds__(NT) complement_basis_kernel(const double* __re
   }
 }
 
-// Complement basis for k <= 96 by Householder reconstruction from an LU factorisation (Ballard,
-// Demmel, Grigori, Jacquelin, Nguyen, Solomonik 2014: "Reconstructing Householder vectors from
-// tall-skinny QR"). W (k x kb) has orthonormal columns, so its Householder QR is W = Q [S; 0] with
-// S = diag(+-1) and Q = I - Y T Y^T; then W - [S; 0] = Y (-T Y1^T S) is an LU factorisation
-// (Y unit lower trapezoidal, Y1 its leading kb x kb block) that needs no pivoting when s_j is taken
-// as -sign of the current diagonal entry (|u_jj| >= 1). The trailing columns of Q are
-//   U = Q [0; I_s] = [0; I_s] - Y T Y2^T = [0; I_s] + Y (U_lu S Z^T),   Z = Y2 Y1^{-1}  (s x kb).
-// Same U as the column-by-column kernel below in exact arithmetic; its kb sequential steps are plain
-// rank-1 updates (one division, no norms or reductions, one barrier), and the rest is small
-// products that all 1024 threads share.
-__device__ __forceinline__ int cdiv_small(int x, int d) {  // x / d, 0 <= x < 2^20, 0 < d < 2^12
-  int q = __float2int_rz(__fmul_rz((float)x, __frcp_rn((float)d)));
-  if ((q + 1) * d <= x) ++q;
-  if (q * d > x) --q;
-  return q;
-}
-
+// Complement basis for k <= 96 by Householder reconstruction (Ballard, Demmel, Grigori, Jacquelin,
+// Nguyen, Solomonik 2014, "Reconstructing Householder vectors from tall-skinny QR"). W (k x kb) has
+// orthonormal columns, so its Householder QR is W = Q [S; 0], S = diag(+-1), Q = I - Y T Y^T, and
+// X = W - [S; 0] = Y (-T Y1^T S) is an LU factorisation (Y unit lower trapezoidal, Y1 = Y[:kb])
+// that needs no pivoting when s_j = -sign of the current diagonal entry (|u_jj| >= 1). The trailing
+// columns of Q are then
+//   U = Q [0; I_s] = [0; I_s] - Y T Y2^T = [0; I_s] + X S Z^T,   Z = Y2 Y1^{-1} = W2 X1^{-1},
+// (Y U_lu = X), so neither Y nor T is formed: Gauss-Jordan elimination of [X1^T | W2^T] = W^T with the
+// diagonal shifted by -s_j at its pivot (the LU's pivots, so s_j is decided on the fly) leaves Z^T
+// in the right block. Same U as the column-by-column Householder kernel below in exact arithmetic;
+// its kb sequential steps are plain rank-1 updates (one thread per column, one barrier, no norms or
+// reductions), and U = [0; I] + X S Z^T is a small product all 1024 threads share.
 constexpr int CLU_KMAX = 96;
 
-__global__ void __launch_bounds__(NT) complement_lu_kernel(const double* __restrict__ W, int64_t ldw, int k,
+__global__ void __launch_bounds__(NT) complement_gj_kernel(const double* __restrict__ W, int64_t ldw, int k,
                                                            int kb, double* __restrict__ U, int64_t ldu) {
   extern __shared__ double sm[];
-  __shared__ double sg[CLU_KMAX], ud[CLU_KMAX];
-  const int tid = threadIdx.x, s = k - kb;
-  double* Ms = sm;                         // k x kb (ld k): W, reduced in place; rows < kb end as U_lu
-  double* Ls = Ms + (size_t)k * kb;        // k x kb (ld k): Y below the diagonal
-  double* Zs = Ls + (size_t)k * kb;        // s x kb (ld s): Z = Y2 Y1^{-1}
-  double* M2 = Zs + (size_t)s * kb;        // kb x s (ld kb): U_lu S Z^T
-  {
-    constexpr int B = 4;
-    for (int e0 = tid; e0 < k * kb; e0 += B * NT) {
-      double v[B];
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int e = e0 + u * NT;
-        if (e < k * kb) {
-          const int c = cdiv_small(e, k);
-          v[u] = W[(e - c * k) + (size_t)c * ldw];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < B; ++u)
-        if (e0 + u * NT < k * kb) Ms[e0 + u * NT] = v[u];
+  __shared__ double sg[CLU_KMAX];
+  const int tid = threadIdx.x, s = k - kb, lda = kb | 1;
+  double* Ws = sm;                       // k x kb (ld k): W
+  double* A = Ws + (size_t)k * kb;       // kb x k (ld lda, column c = row c of W): W^T, eliminated
+  for (int c = tid >> 5; c < kb; c += NT / 32)
+    for (int i = tid & 31; i < k; i += 32) {
+      const double w = W[i + (size_t)c * ldw];
+      Ws[i + c * k] = w;
+      A[c + i * lda] = w;
     }
-  }
   __syncthreads();
-  // LU of W - [S; 0], right-looking, one barrier per step (column j of L goes to Ls, so the
-  // step's reads of column j and row j of Ms never race with its writes)
   for (int j = 0; j < kb; ++j) {
-    const double mjj = Ms[j + j * k];
-    const double sj = mjj >= 0.0 ? -1.0 : 1.0;
-    const double ujj = mjj - sj;  // |u_jj| >= 1
-    const double rj = 1.0 / ujj;
-    const int rows = k - j - 1, cols = kb - j;
-    for (int e = tid; e < rows * cols; e += NT) {
-      const int cc = cdiv_small(e, rows);
-      const int i = j + 1 + (e - cc * rows), c = j + cc;
-      const double lij = Ms[i + j * k] * rj;
-      if (c == j) Ls[i + j * k] = lij;
-      else Ms[i + c * k] -= lij * Ms[j + c * k];
+    const double dj = A[j + j * lda];
+    const double sj = dj >= 0.0 ? -1.0 : 1.0;
+    const double inv = 1.0 / (dj - sj);  // |pivot| >= 1
+    const int c = j + 1 + tid;
+    if (c < k) {
+      double* col = A + c * lda;
+      const double* cj = A + j * lda;
+      const double ajc = col[j] * inv;
+      int i = 0;
+      for (; i + 3 < kb; i += 4) {
+        double x[4], y[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { x[u] = col[i + u]; y[u] = cj[i + u]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) col[i + u] = fma(-y[u], ajc, x[u]);
+      }
+      for (; i < kb; ++i) col[i] = fma(-cj[i], ajc, col[i]);
+      col[j] = ajc;  // (row j: scaled, not eliminated)
     }
-    if (tid == 0) {
-      sg[j] = sj;
-      ud[j] = ujj;
-    }
+    if (tid == 0) sg[j] = sj;
     __syncthreads();
   }
-  // Z = Y2 Y1^{-1}: row r solves z Y1 = y2 (Y1 unit lower triangular), one thread per row
-  if (tid < s) {
-    const int r = tid;
-    for (int i = 0; i < kb; ++i) Zs[r + i * s] = Ls[kb + r + i * k];
-    for (int l = kb - 1; l > 0; --l) {
-      const double zl = Zs[r + l * s];
-      for (int i = 0; i < l; ++i) Zs[r + i * s] = fma(-zl, Ls[l + i * k], Zs[r + i * s]);
+  // U = [0; I_s] + X (S Z^T), X = W - [S; 0], Z^T = A[:, kb:]; 4 x 2 register tiles
+  const int nti = (k + 3) / 4, ntr = (s + 1) / 2;
+  for (int t = tid; t < nti * ntr; t += NT) {
+    const int tr = t / nti, ti = t - tr * nti;
+    const int i0 = 4 * ti, r0 = 2 * tr;
+    double acc[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) acc[u][v] = (i0 + u == kb + r0 + v) ? 1.0 : 0.0;
+    for (int l = 0; l < kb; ++l) {
+      double z[2], x[4];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) z[v] = r0 + v < s ? sg[l] * A[l + (kb + r0 + v) * lda] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        x[u] = i < k ? Ws[i + l * k] - (i == l ? sg[l] : 0.0) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) acc[u][v] = fma(x[u], z[v], acc[u][v]);
     }
-  }
-  __syncthreads();
-  // M2 = U_lu S Z^T  (kb x s): M2[i][r] = sum_{l >= i} U[i][l] s_l Z[r][l]
-  for (int e = tid; e < kb * s; e += NT) {
-    const int r = cdiv_small(e, kb), i = e - r * kb;
-    double acc = ud[i] * sg[i] * Zs[r + i * s];
-    for (int l = i + 1; l < kb; ++l) acc = fma(Ms[i + l * k] * sg[l], Zs[r + l * s], acc);
-    M2[i + r * kb] = acc;
-  }
-  __syncthreads();
-  // U = [0; I_s] + Y M2  (k x s): Y[row][i] = 1 (row == i), Ls[row + i k] (row > i), 0 (row < i)
-  for (int e = tid; e < k * s; e += NT) {
-    const int r = cdiv_small(e, k), row = e - r * k;
-    double acc = (row == kb + r) ? 1.0 : 0.0;
-    const int imax = row < kb ? row : kb;  // i < imax: Y[row][i] = Ls
-    for (int i = 0; i < imax; ++i) acc = fma(Ls[row + i * k], M2[i + r * kb], acc);
-    if (row < kb) acc += M2[row + r * kb];
-    U[row + (size_t)r * ldu] = acc;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        if (i0 + u < k && r0 + v < s) U[(i0 + u) + (size_t)(r0 + v) * ldu] = acc[u][v];
   }
 }
 
-size_t complement_lu_smem(int k, int kb) {
-  const int s = k - kb;
-  return sizeof(double) * (2 * (size_t)k * kb + 2 * (size_t)s * kb + 2);
+size_t complement_gj_smem(int k, int kb) {
+  return sizeof(double) * ((size_t)k * kb + (size_t)(kb | 1) * k);
 }
 
 __global__ void tail_product_kernel(double* Tm, int64_t ldt, const double* __restrict__ U, int64_t ldu,
@@ -548,13 +534,13 @@ void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, in
   per_device_once(attr_mu, attr_mask, [&] {
     DME_CUDA(cudaFuncSetAttribute(complement_basis_kernel<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(complement_basis_kernel<5, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    DME_CUDA(cudaFuncSetAttribute(complement_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)complement_lu_smem(CLU_KMAX, CLU_KMAX)));
+    DME_CUDA(cudaFuncSetAttribute(complement_gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)complement_gj_smem(CLU_KMAX, CLU_KMAX)));
   });
   const size_t smem = sizeof(double) * (size_t)(kb > 0 ? kb : 1) * (k | 1);
   static const bool old_cb = std::getenv("DME_CB_HOUSEHOLDER") != nullptr;  // A/B knob
   if (k <= CLU_KMAX && !old_cb)
-    complement_lu_kernel<<<1, NT, complement_lu_smem(k, kb), st>>>(W, ldw, k, kb, U, ldu);
+    complement_gj_kernel<<<1, NT, complement_gj_smem(k, kb), st>>>(W, ldw, k, kb, U, ldu);
   else if (k <= 96) complement_basis_kernel<3, 3><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   else complement_basis_kernel<5, 5><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   DME_KCHECK();

@@ -8,7 +8,9 @@ constexpr int SMALL_K_MAX = 224;          // packed k(k+1)/2 doubles fit in 201 
 constexpr int SMALL_M_MAX = 8;
 constexpr int FAST_K_MAX = 160;           // fast tridiagonal eigen-compression: k x (k|1) in smem
 constexpr int EIG_SPLIT_MIN = 48;         // k from which the eigen-compression runs as TRI/VEC/FIN
-constexpr int EIG_SPLIT_CTAS = 32;        // CTAs of the VEC kernel (the look-ahead E pass leaves them)            // columns of B handled by the fused Riccati flow
+constexpr int EIG_SPLIT_CTAS = 32;        // CTAs of the VEC kernel (the look-ahead E pass leaves them;
+                                          // 8 CTAs measured slower: 68 vs 56 us in-step, the per-CTA
+                                          // chains lengthen); DME_VEC_CTAS >= 32 for A/B            // columns of B handled by the fused Riccati flow
 constexpr int SMALL_SMEM_MAX = SMALL_K_MAX * (SMALL_K_MAX + 1) / 2 * 8;
 
 // Host-mapped (pinned, zero-copy) record through which the small kernels publish the new rank:

@@ -1,6 +1,7 @@
 #!/bin/bash
-# gpurun: compare in-tree library builds (args: .so names under paper_1805_08990_b200/; "cur" =
-# libdme.so): quick bench + ncu launch-list medians of the pipelined step kernels
+# gpurun: compare library builds / measurement knobs. Args: "cur" (libdme.so), a .so name under
+# paper_1805_08990_b200/ (loaded through DME_LIB), or "env:NAME=VALUE" (libdme.so with that knob).
+# Quick bench x2 (alternating) + one ncu launch list (kernel medians) per variant.
 O=gpurun_out; mkdir -p $O
 P=paper_1805_08990_b200
 qb() {
@@ -10,13 +11,23 @@ import json
 d=json.load(open('gpurun_out/bench_q.json'))
 print('steps/s %.1f ms/step %.4f rank %s' % (d['value'], d['ms_per_step'], d['config'].get('rank_after_timed_steps')))"
 }
-for rep in 1 2; do
+setv() {
+  unset DME_LIB; for e in $ENVS; do unset ${e%%=*}; done
+  case $1 in
+    cur) ;;
+    env:*) export ${1#env:}; ENVS="$ENVS ${1#env:}" ;;
+    *) export DME_LIB=$PWD/$P/$1 ;;
+  esac
+}
+ENVS=""
+for rep in 1 2 3; do
 for v in "$@"; do
-  if [ $v = cur ]; then unset DME_LIB; else export DME_LIB=$PWD/$P/$v; fi
+  setv $v
   echo "== $v"; qb
-  if [ $rep = 1 ]; then
-    timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ll_$v.csv python tools/pipe_probe.py > /dev/null 2>&1
-    python tools/ll_summary.py $O/ll_$v.csv 200 2>/dev/null | head -12
+  if [ $rep = 1 ] && [ -z "$NO_NCU" ]; then
+    tag=$(echo $v | tr ':=/' '___')
+    timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ll_$tag.csv python tools/pipe_probe.py > /dev/null 2>&1
+    python tools/ll_summary.py $O/ll_$tag.csv 200 2>/dev/null | head -14
   fi
 done
 done
