@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(512) gram_congruence_kernel(const double* __re
                                                               const double* __restrict__ Tm,
                                                               int64_t ldt, int r, double* G,
                                                               int64_t ldg) {
+  pdl_wait();
   extern __shared__ double sm[];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int rows = q + m + kp, la = q + m, k = q + r;
@@ -574,7 +575,7 @@ void gram_congruence(const double* Gh, int64_t ldh, int q, int m, int kp, const 
                                   220 * 1024));
   });
   if (smem > 220 * 1024) throw std::runtime_error("gram_congruence: too large");
-  gram_congruence_kernel<<<ctas, 512, smem, st>>>(Gh, ldh, q, m, kp, Tm, ldt, r, G, ldg);
+  launch_pdl(gram_congruence_kernel, dim3(ctas), dim3(512), smem, st, Gh, ldh, q, m, kp, Tm, ldt, r, G, ldg);
   DME_KCHECK();
 }
 

@@ -8,6 +8,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace dme {
 
@@ -40,6 +41,30 @@ inline void per_device_once(std::mutex& m, uint64_t& mask, F&& f) {
   if ((mask >> (dev & 63)) & 1) return;
   f();
   mask |= 1ull << (dev & 63);
+}
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// The latency-bound kernels of the step's critical stream are launched with programmatic stream
+// serialisation: the next kernel is scheduled while its predecessor drains (after every CTA of the
+// predecessor executed pdl_trigger() or exited) and waits in pdl_wait() -- its first statement --
+// until the predecessor has completed and its memory is visible. Without the attribute both are
+// no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  DME_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 // ------------------------------------------------------------------ PTX wrappers

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
   const int nr = r < k ? r + 1 : r;  // + the first dropped one, for the stats
   {
     int P = nr > 0 ? ENT / nr : 1;
-    P = P < 1 ? 1 : (P > 64 ? 64 : P);
+    P = P < 1 ? 1 : P;  // (up to all ENT threads on one eigenvalue: 9 bits per round)
     const int grp = tid / P, t = tid % P;
     const bool act = grp < nr;
     const int jj = k - 1 - grp;

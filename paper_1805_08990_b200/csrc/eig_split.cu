@@ -4,7 +4,7 @@
 //   TRI (1 CTA)       Householder tridiagonalisation, normalisation, theta_max and the rank r
 //                     (Sturm counts); T and the reflectors go to the global scratch Es.
 //   VEC (EIG_SPLIT_CTAS CTAs)  each CTA owns a contiguous slice of the kept eigenvalues (+ the first
-//                     dropped one, for the stats): multisection with up to 64 probes per eigenvalue,
+//                     dropped one, for the stats): multisection with up to 512 probes per eigenvalue,
 //                     twisted-factorisation vectors (lane pairs), back-transformation by the
 //                     reflectors (one warp per column, column in registers), Tm columns written.
 //   FIN (1 CTA)       weighted orthogonality check (fallback flag), stats, fused Riccati flow T3.
@@ -42,6 +42,7 @@ struct EsLayout {
 // NTH threads (512; DME_TRI_THREADS = 256 or 128 for k <= 96: A/B of the per-step latency)
 template <int FK, int NTH>
 __global__ void __launch_bounds__(NTH, 1) eig_tri_kernel(SmallArgs a) {
+  pdl_wait();
   constexpr int NWT = NTH / 32;
   extern __shared__ double A[];
   __shared__ double d[FK], e[FK], e2[FK], tau[FK], vec[FK], pv[FK], pv2[FK];
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(NTH, 1) eig_tri_kernel(SmallArgs a) {
   const long long t0 = clock64();
   tridiagonalise<FK, NTH>(A, k, ld, d, e, tau, vec, pv, pv2);
   const long long t1 = clock64();
+  pdl_trigger();  // VEC may be scheduled now (it waits for this grid in pdl_wait)
   {
     // normalise T by a Gershgorin bound of ||T|| (same arithmetic as normalise_tridiagonal, in
     // parallel: one row per thread, block max/min reductions)
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(NTH, 1) eig_tri_kernel(SmallArgs a) {
 
 template <int FK>
 __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
+  pdl_wait();
   constexpr int RCH = (FK + 31) / 32;
   constexpr int MAXE = (FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1;
   extern __shared__ double R[];  // reflectors, k x ld
@@ -230,9 +233,9 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   t_ph[1] = clock64();
   {
     // one Sturm count per thread and round: with few eigenvalues per CTA (the tail pass of the
-    // refined compression) up to 64 probes per eigenvalue cut the rounds from ~11 to ~7
+    // refined compression) up to 512 probes per eigenvalue cut the rounds from ~11 to ~6
     int P = ENT / nb;
-    P = P < 1 ? 1 : (P > 64 ? 64 : P);
+    P = P < 1 ? 1 : P;  // (up to all ENT threads on one eigenvalue: 9 bits per round)
     const int grp = tid / P, t = tid % P;
     const bool act = grp < nb;
     const int jj = k - 1 - (c0 + grp);  // ascending index
@@ -324,6 +327,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   }
   __syncthreads();
 
+  pdl_trigger();
   // ------------------------------------------------------------ W = Q Z, one warp per column
   // Reflectors are applied four at a time (H_j0 H_j1 H_j2 H_j3 with j0 = j3 + 3 applied first):
   // the four dots v_jm^T z share one warp reduction and the coupling v_p^T v_q of the block
@@ -409,6 +413,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
 
 template <int FK>
 __global__ void __launch_bounds__(ENT, 1) eig_fin_kernel(SmallArgs a) {
+  pdl_wait();
   extern __shared__ double A[];  // W^T, r x ld
   __shared__ double lam[FK + 1], slam[FK + 1];
   __shared__ double red[NW];
@@ -510,6 +515,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_fin_kernel(SmallArgs a) {
     if (tid == 0) publish_rank(a, -1);  // caller falls back to the Jacobi kernel
     return;
   }
+  pdl_trigger();
   const long long f2 = clock64();
   if (a.t3 && r > 0) {
     if constexpr (FK <= 96) {
@@ -619,9 +625,9 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
     const char* e = std::getenv("DME_TRI_THREADS");
     return e ? std::atoi(e) : 512;
   }();
-  if (FK <= 96 && tri_nth == 128) eig_tri_kernel<FK, 128><<<1, 128, smem, st>>>(a);
-  else if (FK <= 96 && tri_nth == 256) eig_tri_kernel<FK, 256><<<1, 256, smem, st>>>(a);
-  else eig_tri_kernel<FK, 512><<<1, 512, smem, st>>>(a);
+  if (FK <= 96 && tri_nth == 128) launch_pdl(eig_tri_kernel<FK, 128>, dim3(1), dim3(128), smem, st, a);
+  else if (FK <= 96 && tri_nth == 256) launch_pdl(eig_tri_kernel<FK, 256>, dim3(1), dim3(256), smem, st, a);
+  else launch_pdl(eig_tri_kernel<FK, 512>, dim3(1), dim3(512), smem, st, a);
   DME_KCHECK();
   constexpr int MAXE = (FK + 1 + EIG_SPLIT_CTAS - 1) / EIG_SPLIT_CTAS + 1;
   // (+ 2 doubles: the bulk copy of the reflectors is rounded up to 16 bytes)
@@ -632,12 +638,12 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
     const int v = e ? std::atoi(e) : EIG_SPLIT_CTAS;
     return v < EIG_SPLIT_CTAS ? EIG_SPLIT_CTAS : v;  // MAXE is sized for >= EIG_SPLIT_CTAS CTAs
   }();
-  eig_vec_kernel<FK><<<vec_ctas, ENT, vsmem > smem ? vsmem : smem, st>>>(a);
+  launch_pdl(eig_vec_kernel<FK>, dim3(vec_ctas), dim3(ENT), vsmem > smem ? vsmem : smem, st, a);
   DME_KCHECK();
   const size_t fsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * (size_t)a.k * SMALL_M_MAX +
                                                   (size_t)a.k * SMALL_M_MAX)
                                  : smem;
-  eig_fin_kernel<FK><<<1, ENT, fsmem > smem ? fsmem : smem, st>>>(a);
+  launch_pdl(eig_fin_kernel<FK>, dim3(1), dim3(ENT), fsmem > smem ? fsmem : smem, st, a);
   DME_KCHECK();
 }
 

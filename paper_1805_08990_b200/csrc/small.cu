@@ -394,6 +394,7 @@ constexpr int CLU_KMAX = 96;
 
 __global__ void __launch_bounds__(NT) complement_gj_kernel(const double* __restrict__ W, int64_t ldw, int k,
                                                            int kb, double* __restrict__ U, int64_t ldu) {
+  pdl_wait();
   extern __shared__ double sm[];
   __shared__ double sg[CLU_KMAX];
   const int tid = threadIdx.x, s = k - kb, lda = kb | 1;
@@ -429,6 +430,7 @@ __global__ void __launch_bounds__(NT) complement_gj_kernel(const double* __restr
     if (tid == 0) sg[j] = sj;
     __syncthreads();
   }
+  pdl_trigger();
   // U = [0; I_s] + X (S Z^T), X = W - [S; 0], Z^T = A[:, kb:]; 4 x 2 register tiles
   const int nti = (k + 3) / 4, ntr = (s + 1) / 2;
   for (int t = tid; t < nti * ntr; t += NT) {
@@ -480,6 +482,7 @@ __global__ void tail_product_kernel(double* Tm, int64_t ldt, const double* __res
 __global__ void __launch_bounds__(NT) tail_assemble_kernel(SmallArgs a, const double* __restrict__ U,
                                                            int64_t ldu, int s, const double* __restrict__ V,
                                                            int64_t ldv, int kb, int ks, const int* ks_dev) {
+  pdl_wait();
   extern __shared__ double S[];
   if (ks_dev) {  // the tail rank published by the preceding eigen pass (< 0: it fell back to Jacobi)
     ks = *ks_dev;
@@ -540,7 +543,7 @@ void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, in
   const size_t smem = sizeof(double) * (size_t)(kb > 0 ? kb : 1) * (k | 1);
   static const bool old_cb = std::getenv("DME_CB_HOUSEHOLDER") != nullptr;  // A/B knob
   if (k <= CLU_KMAX && !old_cb)
-    complement_gj_kernel<<<1, NT, complement_gj_smem(k, kb), st>>>(W, ldw, k, kb, U, ldu);
+    launch_pdl(complement_gj_kernel, dim3(1), dim3(NT), complement_gj_smem(k, kb), st, W, ldw, k, kb, U, ldu);
   else if (k <= 96) complement_basis_kernel<3, 3><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   else complement_basis_kernel<5, 5><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   DME_KCHECK();
@@ -577,7 +580,7 @@ void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, c
     DME_CUDA(cudaFuncSetAttribute(tail_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SMALL_SMEM_MAX));
   });
-  tail_assemble_kernel<<<1, NT, need, st>>>(a, U, ldu, s, V, ldv, kb, ks, ks_dev);
+  launch_pdl(tail_assemble_kernel, dim3(1), dim3(NT), need, st, a, U, ldu, s, V, ldv, kb, ks, ks_dev);
   DME_KCHECK();
 }
 
