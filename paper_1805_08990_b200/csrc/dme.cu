@@ -915,7 +915,17 @@ int64_t eig_finish(dme_ctx* c, const SmallArgs& a, bool fast) {
 // Finish a compression: first pass, then (refined) the tail pass and T3. zc_ready: an event after
 // which Zc is complete (the pipeline writes part of it on the second stream), or null.
 int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = nullptr) {
+  // refined: the complement basis of the first pass's kept vectors is queued before the host has
+  // seen kb (the kernel reads the published rank on the device; a Jacobi fallback publishes -1,
+  // turning it into a no-op, and it is queued again below with the host's kb)
+  bool cb_queued = false;
+  if (cp.refine && cp.fast) {
+    ProfScope ps(c, PROF_SMALL);
+    cb_queued = complement_basis_dev(cp.a.Tm, KMAX, (int)cp.k, c->r_dev, c->Us, KMAX, c->st);
+  }
+  const int64_t fb0 = c->stats.eig_fallbacks;
   const int64_t kb = eig_finish(c, cp.a, cp.fast);
+  if (c->stats.eig_fallbacks != fb0) cb_queued = false;
   if (!cp.refine) {
     if (cp.do_compress) c->stats.last_drop = c->last_st[2];
     return kb;
@@ -930,7 +940,7 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
   if (kb < k && tmax > 0.0 && kb < cap) {
     // U (k x s): orthonormal basis of the complement of span(W_b); Zs = Zc U (n x s), Gs = Zs^T Zs
     s = k - kb;
-    {
+    if (!cb_queued) {
       ProfScope ps(c, PROF_SMALL);
       complement_basis(cp.a.Tm, KMAX, (int)k, (int)kb, c->Us, KMAX, c->st);
     }

@@ -393,8 +393,13 @@ __global__ void __launch_bounds__(NT) complement_basis_kernel(const double* __re
 constexpr int CLU_KMAX = 96;
 
 __global__ void __launch_bounds__(NT) complement_gj_kernel(const double* __restrict__ W, int64_t ldw, int k,
-                                                           int kb, double* __restrict__ U, int64_t ldu) {
+                                                           int kb, double* __restrict__ U, int64_t ldu,
+                                                           const int* __restrict__ kb_dev) {
   pdl_wait();
+  if (kb_dev) {  // (speculative launch: the rank the first eigen pass published; < 0 = fallback)
+    kb = *kb_dev;
+    if (kb < 0 || kb >= k) return;
+  }
   extern __shared__ double sm[];
   __shared__ double sg[CLU_KMAX];
   const int tid = threadIdx.x, s = k - kb, lda = kb | 1;
@@ -529,7 +534,7 @@ __global__ void __launch_bounds__(NT) tail_assemble_kernel(SmallArgs a, const do
 }  // namespace
 
 void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, int64_t ldu,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool attrs_only) {
   if (k > FAST_K_MAX || kb > k || kb < 0) throw std::runtime_error("complement_basis: bad size");
   const int mx = (int)(sizeof(double) * FAST_K_MAX * (FAST_K_MAX | 1));
   static std::mutex attr_mu;
@@ -540,13 +545,26 @@ void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, in
     DME_CUDA(cudaFuncSetAttribute(complement_gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)complement_gj_smem(CLU_KMAX, CLU_KMAX)));
   });
+  if (attrs_only) return;
   const size_t smem = sizeof(double) * (size_t)(kb > 0 ? kb : 1) * (k | 1);
   static const bool old_cb = std::getenv("DME_CB_HOUSEHOLDER") != nullptr;  // A/B knob
   if (k <= CLU_KMAX && !old_cb)
-    launch_pdl(complement_gj_kernel, dim3(1), dim3(NT), complement_gj_smem(k, kb), st, W, ldw, k, kb, U, ldu);
+    launch_pdl(complement_gj_kernel, dim3(1), dim3(NT), complement_gj_smem(k, kb), st, W, ldw, k, kb, U, ldu,
+               (const int*)nullptr);
   else if (k <= 96) complement_basis_kernel<3, 3><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   else complement_basis_kernel<5, 5><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   DME_KCHECK();
+}
+
+bool complement_basis_dev(const double* W, int64_t ldw, int k, const int* kb_dev, double* U, int64_t ldu,
+                          cudaStream_t st) {
+  static const bool old_cb = std::getenv("DME_CB_HOUSEHOLDER") != nullptr;
+  if (k > CLU_KMAX || old_cb) return false;
+  complement_basis(W, ldw, k, 0, U, 0, nullptr, true);  // (attributes only)
+  launch_pdl(complement_gj_kernel, dim3(1), dim3(NT), complement_gj_smem(k, k), st, W, ldw, k, 0, U, ldu,
+             kb_dev);
+  DME_KCHECK();
+  return true;
 }
 
 void t3_only(const SmallArgs& a, int r, cudaStream_t st);

@@ -58,7 +58,11 @@ size_t eig_split_scratch_doubles();
 void t3_only(const SmallArgs& a, int r, cudaStream_t st);  // T3 on Tm (k x r) alone
 // U (k x (k - kb), ldu): orthonormal basis of the complement of span(W), W = k x kb orthonormal
 void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, int64_t ldu,
-                      cudaStream_t st);
+                      cudaStream_t st, bool attrs_only = false);
+// The same with kb read on the device (*kb_dev: the rank the first eigen pass published; < 0 makes
+// it a no-op), so it can be queued before the host has seen kb; false: not available (k > 96)
+bool complement_basis_dev(const double* W, int64_t ldw, int k, const int* kb_dev, double* U, int64_t ldu,
+                          cudaStream_t st);
 // a.Tm[:, kb:kb+ks] = U V (U: k x s, V: s x ks), then T3 on a.Tm (k x (kb + ks)) if a.t3.
 // ks_dev != nullptr: ks is read on the device (the rank the preceding eigen pass published; a
 // negative value -- Jacobi fallback pending -- makes the kernel a no-op); ks is then an upper bound
