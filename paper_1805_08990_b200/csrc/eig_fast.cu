@@ -114,10 +114,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
       hi_s[grp] = s_hi;
     }
     __syncthreads();
-    const double bits = log2((double)P + 1.0);
+    const float bits = __log2f((float)P + 1.0f);  // (fast float math: only sizes the loop)
     // absolute accuracy 1e-13 ||T||: enough for the twisted vectors (their error ~ |dlambda| / gap
     // only matters weighted by theta)
-    const int nit = (int)ceil(log2((s_hi - s_lo) / 1e-13 + 1.0) / bits) + 1;
+    const int nit = (int)ceilf(1.00001f * __log2f((float)((s_hi - s_lo) / 1e-13) + 1.0f) / bits) + 1;
     for (int it = 0; it < nit; ++it) {
       if (act) {
         const double a0 = lo_s[grp], b0 = hi_s[grp];

@@ -244,8 +244,8 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
       hi_s[grp] = ghi;
     }
     __syncthreads();
-    const double bits = log2((double)P + 1.0);
-    const int nit = (int)ceil(log2((ghi - glo) / 1e-13 + 1.0) / bits) + 1;
+    const float bits = __log2f((float)P + 1.0f);  // (fast float math: only sizes the loop)
+    const int nit = (int)ceilf(1.00001f * __log2f((float)((ghi - glo) / 1e-13) + 1.0f) / bits) + 1;
     for (int it = 0; it < nit; ++it) {
       if (act) {
         const double a0 = lo_s[grp], b0 = hi_s[grp];
