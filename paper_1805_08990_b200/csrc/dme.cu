@@ -1,6 +1,7 @@
 // C-ABI implementation: context, init (upload, Padé-13 expm, quadrature ladder), composition driver.
 // See include/dme.h for the contract and DESIGN.md for the design and the paper readings.
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <chrono>
@@ -22,6 +23,16 @@
 #include "small.h"
 
 using namespace dme;
+
+// NVTX ranges per flow / phase (SURVEY §5 tracing; the paper profiles per sub-function):
+// "dme::T1", "dme::T12", "dme::compress", "dme::init", ... visible in nsys / ncu --nvtx.
+// Header-only NVTX3: without an attached tool a range costs a few ns.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 void axpy_cols(double* Y, int64_t ldy, const double* X, int64_t ldx, int64_t rows, int64_t cols,
                double alpha, cudaStream_t st);
@@ -1012,6 +1023,7 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
 // Compress the factor Zc (n x k, col-major ldn) into out (n x r); optionally fuse T3(tau3).
 int64_t compress(dme_ctx* c, double* Zc, int64_t k, double* out, bool t3, double tau3,
                  bool do_compress = true) {
+  NvtxRange nvtx_("dme::compress");
   if (k <= 0) return 0;
   Compression cp;
   compress_launch(c, Zc, k, t3, tau3, do_compress, cp);
@@ -1028,6 +1040,7 @@ int64_t compress(dme_ctx* c, double* Zc, int64_t k, double* out, bool t3, double
 void swapZ(dme_ctx* c) { std::swap(c->Z, c->Ztmp); }
 
 void flow_T1(dme_ctx* c, double tau) {
+  NvtxRange nvtx_("dme::T1");
   eact(c, tau == c->h, c->Z, c->r, c->Ztmp, c->ldn);
   swapZ(c);
 }
@@ -1039,12 +1052,14 @@ void finish_compress(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3) {
 }
 
 void flow_T2(dme_ctx* c, double tau, bool t3, double tau3) {
+  NvtxRange nvtx_("dme::T2");
   copy_cols(c->Zc2, c->ldn, c->Z, c->ldn, c->n, c->r, 1.0, c->st);
   copy_cols(c->Zc2 + c->r * c->ldn, c->ldn, c->LQ, c->ldn, c->n, c->p, std::sqrt(tau), c->st);
   finish_compress(c, c->Zc2, c->r + c->p, t3, tau3);
 }
 
 void flow_T12(dme_ctx* c, double tau, bool t3, double tau3) {
+  NvtxRange nvtx_("dme::T12");
   const bool full = (tau == c->h);
   double* Zc = full ? c->Zc12f : c->Zc12h;
   const int64_t q = full ? c->qf : c->qh;
@@ -1053,6 +1068,7 @@ void flow_T12(dme_ctx* c, double tau, bool t3, double tau3) {
 }
 
 void flow_T3(dme_ctx* c, double tau) {
+  NvtxRange nvtx_("dme::T3");
   if (c->r == 0) return;
   const int64_t r = compress(c, c->Z, c->r, c->Ztmp, true, tau, /*do_compress=*/false);
   (void)r;
@@ -1072,6 +1088,7 @@ void s_pass(dme_ctx* c, const double* X, int64_t k, double* out, int64_t ldo, do
 }
 
 void flow_T4(dme_ctx* c, double tau, int order, bool t3, double tau3) {
+  NvtxRange nvtx_("dme::T4");
   if (c->r == 0) return;
   const int64_t r = c->r, ld = c->ldn;
   copy_cols(c->Zc2, ld, c->Z, ld, c->n, r, 1.0, c->st);
@@ -1159,6 +1176,7 @@ void run_sequence(dme_ctx* c, const std::vector<Op>& seq) {
 // E_h Y_{t+1} and Ghat_{t+1} (n-row work) underneath. Exact reassociation of the same products
 // (rounding differs only); only the last step materialises the state Z.
 void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
+  NvtxRange nvtx_("dme::F12F3.pipelined");
   if (nb <= 0) return;
   const int64_t ld = c->ldn, q = c->qf, n = c->n, m = c->m;
   double* Zc = c->Zc12f;
@@ -1184,6 +1202,7 @@ void run_f12f3_body(dme_ctx* c, int64_t nb, double h) {
   int64_t rn = compress_finish(c, cp);
   DME_CUDA(cudaEventRecord(c->ev_tm, c->st));  // Tm_0 final (after the tail pass and T3)
   for (int64_t it = 0; it < nb; ++it) {
+    NvtxRange nvtx_step("dme::step");
     double* Tm_cur = Tmb[it & 1];
     const int64_t kp = q + r_prev;  // columns of Zc_t = columns of LA_t
     const bool last = it + 1 == nb;
@@ -1281,6 +1300,7 @@ void matmul_sq(dme_ctx* c, const double* X, const double* Y, double* out) {
 // L_I(2w) = compress([L_I(w), E_w L_I(w)])  (exact doubling of the composite rule, reading G6);
 // E_w is the dense Ew, or (sparse A) the Chebyshev action with tau = w
 void ladder_double(dme_ctx* c, double* LI, int64_t& q, const double* Ew, double w) {
+  NvtxRange nvtx_("dme::init.quadrature_rung");
   if (q == 0) return;
   DME_REQUIRE(2 * q <= KMAX, DME_ERR_DIM, "quadrature factor rank exceeds 112");
   if (c->sparse || c->cheb_e) sparse_pass(c, w, LI, q, LI + q * c->ldn, c->ldn, c->st);
@@ -1291,6 +1311,7 @@ void ladder_double(dme_ctx* c, double* LI, int64_t& q, const double* Ew, double 
 }
 
 void init_all(dme_ctx* c, const dme_problem* pr) {
+  NvtxRange nvtx_("dme::init");
   const int64_t n = c->n, ld = c->ldn;
   cudaStream_t st = c->st;
   DME_CUDA(cudaMemsetAsync(c->gs.counters, 0, sizeof(int) * c->gs.max_tiles, st));

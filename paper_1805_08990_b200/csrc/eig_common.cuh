@@ -136,7 +136,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 // memory), in place: d, e (unnormalised) and tau; reflector j kept in row j (v_0 = 1 implicit).
 template <int FK, int NTH = ENT>
 __device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, double* tau,
-                               double* vec, double* pv, double* pv2) {
+                               double* vec, double* pv, double* pv2, long long* ph = nullptr) {
+#ifdef DME_TRI_PHASES  // measurement build only (tools/tri_phases.sh): per-phase cycle sums
+  long long acc_a = 0, acc_w = 0, acc_bar = 0;
+#endif
   constexpr int RCH = (FK + 31) / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // Step j: reflector H_j = I - tau_j v v^T built from ROW j (= column j, symmetric storage) and
@@ -180,6 +183,9 @@ __device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, d
   if (k > 2 && warp == 0) householder(0, vec);
   __syncthreads();
   for (int j = 0; j + 2 < k; ++j) {
+#ifdef DME_TRI_PHASES
+    const long long t_a = clock64();
+#endif
     const int m = k - j - 1;
     const double* vj = (j & 1) ? pv2 : vec;  // double-buffered reflector
     double* vn = (j & 1) ? vec : pv2;
@@ -201,6 +207,9 @@ __device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, d
       }
     }
     __syncthreads();
+#ifdef DME_TRI_PHASES
+    const long long t_b = clock64();
+#endif
     if (tj != 0.0) {
       // K = tau/2 p^T v (every warp, redundantly), w = p - K v
       double dot = 0.0;
@@ -254,8 +263,21 @@ __device__ void tridiagonalise(double* A, int k, int ld, double* d, double* e, d
     } else if (warp == 0 && j + 3 < k) {
       householder(j + 1, vn);
     }
+#ifdef DME_TRI_PHASES
+    const long long t_c = clock64();
+#endif
     __syncthreads();
+#ifdef DME_TRI_PHASES
+    acc_a += t_b - t_a;
+    acc_w += t_c - t_b;
+    acc_bar += clock64() - t_c;
+#endif
   }
+#ifdef DME_TRI_PHASES
+  if (ph && tid == 0) { ph[0] = acc_a; ph[1] = acc_w; ph[2] = acc_bar; }
+  if (ph && tid == 32) { ph[3] = acc_w; ph[4] = acc_bar; }
+  if (ph && tid == 0 + 64) ph[5] = acc_w;
+#endif
   if (tid == 0) {
     if (k >= 2) {
       d[k - 2] = A[(k - 2) * ld + (k - 2)];

@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(NTH, 1) eig_tri_kernel(SmallArgs a) {
   }
   __syncthreads();
   const long long t0 = clock64();
-  tridiagonalise<FK, NTH>(A, k, ld, d, e, tau, vec, pv, pv2);
+  __shared__ long long tph[8];
+  tridiagonalise<FK, NTH>(A, k, ld, d, e, tau, vec, pv, pv2, tph);
   const long long t1 = clock64();
   pdl_trigger();  // VEC may be scheduled now (it waits for this grid in pdl_wait)
   {
@@ -169,6 +170,10 @@ __global__ void __launch_bounds__(NTH, 1) eig_tri_kernel(SmallArgs a) {
       a.stats[6] = (double)(t0 - t_in);
       a.stats[8] = (double)(t1 - t0);
       a.stats[9] = (double)(clock64() - t1);
+#ifdef DME_TRI_PHASES  // (measurement build) phase sums over the reflector steps
+      for (int q = 0; q < 6; ++q) a.stats[10 + q] = (double)tph[q];
+      a.stats[7] = (double)k;
+#endif
     }
   }
   for (int i = tid; i < k; i += NTH) {
@@ -407,8 +412,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   }
   __syncthreads();
   t_ph[4] = clock64();
+#ifndef DME_TRI_PHASES
   if (blockIdx.x == 0 && tid == 0 && a.stats)  // phase cycles (tools/eig_split_probe.py)
     for (int q = 0; q < 4; ++q) a.stats[10 + q] = (double)(t_ph[q + 1] - t_ph[q]);
+#endif
 }
 
 template <int FK>
@@ -590,8 +597,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_fin_kernel(SmallArgs a) {
   if (tid == 0) {
     publish_rank(a, r);
     if (a.stats) {  // phase cycles (tools/eig_split_probe.py)
+#ifndef DME_TRI_PHASES
       a.stats[14] = (double)(f1 - f0);
       a.stats[15] = (double)(f2 - f1);
+#endif
       a.stats[5] = (double)(clock64() - f2);
     }
   }
