@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(256) tall_small_kernel(const double* A, int64_
                                                          const double* __restrict__ B, int64_t ldb,
                                                          double* C, int64_t ldc, int64_t M,
                                                          int64_t N, int64_t K) {
+  pdl_wait();
   __shared__ double sA[TS_BK][TS_BM + 4];
   __shared__ double sB[TS_BN][TS_BK + 4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -754,7 +755,7 @@ void tall_small(const double* A, int64_t lda, const double* B, int64_t ldb, doub
   if (K <= 0) throw std::runtime_error("tall_small: K must be positive");
   if (C == A && N > TS_BN) throw std::runtime_error("tall_small: in place needs N <= 64");
   dim3 grid((unsigned)ceil_div(M, TS_BM), (unsigned)ceil_div(N, TS_BN));
-  tall_small_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K);
+  launch_pdl(tall_small_kernel, grid, dim3(256), 0, st, A, lda, B, ldb, C, ldc, M, N, K);
   DME_KCHECK();
 }
 

@@ -32,6 +32,7 @@ using namespace eigk;
 
 template <int FK>
 __global__ void __launch_bounds__(ENT, 1) eig_fast_kernel(SmallArgs a) {
+  pdl_wait();
   constexpr int RCH = (FK + 31) / 32;      // column chunks per lane
   constexpr int RPW = (FK + NW - 1) / NW;  // rows per warp
   extern __shared__ double A[];            // k x ld, full symmetric, ld odd
@@ -386,7 +387,7 @@ void launch_fast(const SmallArgs& a, cudaStream_t st) {
     DME_CUDA(cudaFuncSetAttribute(eig_fast_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(need > floor_b ? need : floor_b)));
   });
-  eig_fast_kernel<FK><<<1, ENT, smem, st>>>(a);
+  launch_pdl(eig_fast_kernel<FK>, dim3(1), dim3(ENT), smem, st, a);
   DME_KCHECK();
 }
 
