@@ -1,7 +1,7 @@
 #!/bin/bash
 # gpurun: quick bench A/B for configs 1, 2, 5 (args as tools/gpu_abc.sh: cur / lib.so / env:K=V)
 P=paper_1805_08990_b200
-for c in 1 2 5; do
+for c in ${CFGS:-1 2 5}; do
 for rep in 1 2; do
 for v in "$@"; do
   unset DME_LIB
