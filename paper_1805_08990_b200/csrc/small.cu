@@ -321,60 +321,90 @@ __global__ void __launch_bounds__(NT) complement_basis_kernel(const double* __re
     }
   }
   __syncthreads();
-  // U = H_0 ... H_{kb-1} [0; I_s]: column t of U starts as e_{kb + t}. Eight lanes per column
-  // (rows sub + 8u), so a reflector costs each column a 3-level shuffle reduction (instead of a
-  // 5-level one per column and per warp slot): the phase is bound by the SM's shuffle throughput.
-  // (k > 96: a whole warp per column, as in phase 1, to stay within 64 registers)
-  constexpr int LPC = RPL * CPW <= 9 ? 8 : 32;      // lanes per column
-  constexpr int NG = NT / LPC;                      // column groups
-  constexpr int R8 = (32 * RPL + LPC - 1) / LPC;    // rows per lane
-  constexpr int CPG = (32 * CPW + NG - 1) / NG;     // columns per group
-  const int sub = lane & (LPC - 1), grp = tid / LPC;
-  double y[CPG][R8];
+  if constexpr (RPL * CPW > 9) {
+    // k > 96: a whole warp per column (the 8-lane layout would not fit in 64 registers), slots
+    // applied one after another, only those holding a column of U
 #pragma unroll
-  for (int q = 0; q < CPG; ++q)
+    for (int q = 0; q < CPW; ++q) {
+      const int t = warp + 32 * q;
 #pragma unroll
-    for (int u = 0; u < R8; ++u) y[q][u] = (sub + LPC * u == kb + grp + NG * q) ? 1.0 : 0.0;
-  for (int j = kb - 1; j >= 0; --j) {
-    const double t = tau_s[j];
-    if (t == 0.0) continue;
-    double vv[R8];
-#pragma unroll
-    for (int u = 0; u < R8; ++u) {
-      const int i = sub + LPC * u;
-      vv[u] = i < k ? Vh[j * ld + i] : 0.0;
+      for (int u = 0; u < RPL; ++u) x[q][u] = (lane + 32 * u == kb + t) ? 1.0 : 0.0;
     }
-    double d[CPG];
+    for (int j = kb - 1; j >= 0; --j)
 #pragma unroll
-    for (int q = 0; q < CPG; ++q) {
-      double d0 = 0.0, d1 = 0.0;
+      for (int q = 0; q < CPW; ++q)
+        if (warp + 32 * q < s) apply(j, q);
 #pragma unroll
-      for (int u = 0; u < R8; u += 2) {
-        d0 = fma(vv[u], y[q][u], d0);
-        if (u + 1 < R8) d1 = fma(vv[u + 1], y[q][u + 1], d1);
-      }
-      d[q] = d0 + d1;
+    for (int q = 0; q < CPW; ++q) {
+      const int t = warp + 32 * q;
+      if (t < s)
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int i = lane + 32 * u;
+          if (i < k) U[i + (size_t)t * ldu] = x[q][u];
+        }
     }
-#pragma unroll
-    for (int o = 1; o < LPC; o <<= 1)
-#pragma unroll
-      for (int q = 0; q < CPG; ++q) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
-#pragma unroll
-    for (int q = 0; q < CPG; ++q) {
-      const double dq = t * d[q];
-#pragma unroll
-      for (int u = 0; u < R8; ++u) y[q][u] = fma(-dq, vv[u], y[q][u]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < CPG; ++q) {
-    const int t = grp + NG * q;
-    if (t < s)
-#pragma unroll
+  } else {
+    // U = H_0 ... H_{kb-1} [0; I_s]: column t of U starts as e_{kb + t}. Eight lanes per column
+    // (rows sub + 8u), so a reflector costs each column a 3-level shuffle reduction (instead of a
+    // 5-level one per column and per warp slot): the phase is bound by the SM's shuffle throughput.
+    // (k > 96: a whole warp per column, as in phase 1, to stay within 64 registers)
+    constexpr int LPC = RPL * CPW <= 9 ? 8 : 32;      // lanes per column
+    constexpr int NG = NT / LPC;                      // column groups
+    constexpr int R8 = (32 * RPL + LPC - 1) / LPC;    // rows per lane
+    constexpr int CPG = (32 * CPW + NG - 1) / NG;     // columns per group
+    const int sub = lane & (LPC - 1), grp = tid / LPC, g0 = (tid & ~31) / LPC;
+    double y[CPG][R8];
+  #pragma unroll
+    for (int q = 0; q < CPG; ++q)
+  #pragma unroll
+      for (int u = 0; u < R8; ++u) y[q][u] = (sub + LPC * u == kb + grp + NG * q) ? 1.0 : 0.0;
+    for (int j = kb - 1; j >= 0; --j) {
+      const double t = tau_s[j];
+      if (t == 0.0) continue;
+      double vv[R8];
+  #pragma unroll
       for (int u = 0; u < R8; ++u) {
         const int i = sub + LPC * u;
-        if (i < k) U[i + (size_t)t * ldu] = y[q][u];
+        vv[u] = i < k ? Vh[j * ld + i] : 0.0;
       }
+      double d[CPG];
+  #pragma unroll
+      for (int q = 0; q < CPG; ++q) {
+        d[q] = 0.0;
+        if (g0 + NG * q < s) {  // (warp-uniform: slots holding no column of U are skipped)
+          double d0 = 0.0, d1 = 0.0;
+  #pragma unroll
+          for (int u = 0; u < R8; u += 2) {
+            d0 = fma(vv[u], y[q][u], d0);
+            if (u + 1 < R8) d1 = fma(vv[u + 1], y[q][u + 1], d1);
+          }
+          d[q] = d0 + d1;
+        }
+      }
+  #pragma unroll
+      for (int o = 1; o < LPC; o <<= 1)
+  #pragma unroll
+        for (int q = 0; q < CPG; ++q)
+          if (g0 + NG * q < s) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+  #pragma unroll
+      for (int q = 0; q < CPG; ++q) {
+        if (g0 + NG * q >= s) continue;
+        const double dq = t * d[q];
+  #pragma unroll
+        for (int u = 0; u < R8; ++u) y[q][u] = fma(-dq, vv[u], y[q][u]);
+      }
+    }
+  #pragma unroll
+    for (int q = 0; q < CPG; ++q) {
+      const int t = grp + NG * q;
+      if (t < s)
+  #pragma unroll
+        for (int u = 0; u < R8; ++u) {
+          const int i = sub + LPC * u;
+          if (i < k) U[i + (size_t)t * ldu] = y[q][u];
+        }
+    }
   }
 }
 
