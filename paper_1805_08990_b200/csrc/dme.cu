@@ -866,6 +866,12 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
   a.Tm = Tm_out ? Tm_out : c->Tm; a.ldt = KMAX;
   a.V = c->Vg; a.ldv = KMAX;
   a.Es = c->Es;
+  static const int msec_p = [] {
+    const char* e = std::getenv("DME_MSEC_P");
+    const int v = e ? std::atoi(e) : 128;
+    return v < 1 ? 1 : (v > 512 ? 512 : v);
+  }();
+  a.msec_p = msec_p;
   a.r_out = c->r_dev;
   a.stats = c->sstats;
   if (c->hmap_dev) {

@@ -17,9 +17,11 @@ constexpr int NW = ENT / 32;
 __device__ __forceinline__ void rescale_pair(double& p1, double& p2) {
   const double m1 = fmax(fabs(p1), fabs(p2));
   if (m1 > 0x1p64 || (m1 < 0x1p-64 && m1 > 0.0)) {
-    int ex;
-    frexp(m1, &ex);
-    const double sc = ldexp(1.0, -ex);
+    // exponent field of m1 (a subnormal m1 reads as 2^-1022: the product is then scaled up by 2^1022,
+    // short of ~1 but normal); 2^-e built directly, e in [-1022, 1023]
+    const int e = ((__double2hiint(m1) >> 20) & 0x7ff) - 1023;
+    const int ec = e < -1022 ? -1022 : e;
+    const double sc = __hiloint2double((1023 - ec) << 20, 0);
     p1 *= sc;
     p2 *= sc;
   }
@@ -30,8 +32,10 @@ __device__ __forceinline__ void rescale_pair(double& p1, double& p2) {
 // a measure-zero event that only moves a bisection probe by one count)
 __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
                                            const double* __restrict__ e2, int k, double x) {
+  // signs from the high word (INT pipe; the FP64 pipe is what many concurrent probes saturate);
+  // an exact zero counts by its sign bit, a measure-zero event that moves a probe by one count
   double p2 = 1.0, p1 = d[0] - x;
-  bool neg_prev = p1 <= 0.0;
+  bool neg_prev = __double2hiint(p1) < 0;
   int cnt = neg_prev;
   int i = 1;
   // blocks of 8: the loads are independent of the recurrence and issue ahead of it; the exact
@@ -48,7 +52,7 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const double p = fma(dd[u], p1, -ff[u] * p2);
-      const bool ng = p <= 0.0;
+      const bool ng = __double2hiint(p) < 0;
       cnt += ng != neg_prev;
       neg_prev = ng;
       p2 = p1;
@@ -58,7 +62,7 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
   }
   for (; i < k; ++i) {
     const double p = fma(d[i] - x, p1, -e2[i - 1] * p2);
-    const bool ng = p <= 0.0;
+    const bool ng = __double2hiint(p) < 0;
     cnt += ng != neg_prev;
     neg_prev = ng;
     p2 = p1;

@@ -239,8 +239,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_vec_kernel(SmallArgs a) {
   {
     // one Sturm count per thread and round: with few eigenvalues per CTA (the tail pass of the
     // refined compression) up to 512 probes per eigenvalue cut the rounds from ~11 to ~6
+    // probes per eigenvalue: more probes mean fewer rounds but, past ~4 warps, a round is bound by
+    // the FP64 pipe of the SM rather than by one count's dependency chain (DME_MSEC_P: A/B knob)
     int P = ENT / nb;
-    P = P < 1 ? 1 : P;  // (up to all ENT threads on one eigenvalue: 9 bits per round)
+    P = P < 1 ? 1 : (P > a.msec_p ? a.msec_p : P);
     const int grp = tid / P, t = tid % P;
     const bool act = grp < nb;
     const int jj = k - 1 - (c0 + grp);  // ascending index

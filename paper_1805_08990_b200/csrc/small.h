@@ -49,6 +49,7 @@ struct SmallArgs {
   double orth_tol = 1e-12;   // fast path: max weighted |W^T W - I| before falling back to Jacobi
   HostMap* map = nullptr;    // device alias of the host-mapped record (nullptr: r_out only)
   int map_seq = 0;           // sequence number this launch publishes
+  int msec_p = 128;          // split path: multisection probes per eigenvalue (cap)
 };
 
 void compress_t3(const SmallArgs& a, cudaStream_t st);  // Jacobi (any k <= SMALL_K_MAX)
