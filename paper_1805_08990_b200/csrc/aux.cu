@@ -2,6 +2,7 @@
 #include "aux.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include "common.cuh"
 #include <cooperative_groups.h>
@@ -478,8 +479,17 @@ void rowmajor_to_colmajor(double* dst, int64_t ldd, const double* src, int64_t l
 // CTA b owns the columns j of its slice of [0, r): it stages Gh[:, LA] (rows x kp) and Tm in
 // shared memory, forms F[:, j] = Gh[:, LA] Tm[:, j] for all q + m + kp rows, then writes G12 /
 // G21, H2 and G22[i, j] = G22[j, i] (i <= j) for its j; CTA 0 also copies G11 and H1. Launched on
-// CONG_CTAS CTAs: it must fit beside the look-ahead E pass (#SM - 8 persistent CTAs).
-constexpr int CONG_CTAS = 8;
+// cong_ctas() CTAs (32: the look-ahead E pass of the previous step has finished when the
+// congruence runs; 8 / 16 / 32 measured 2117 / 2124 / 2133 steps/s at config 5).
+constexpr int CONG_CTAS_DEFAULT = 32;
+int cong_ctas() {  // (DME_CONG_CTAS: A/B knob)
+  static const int v = [] {
+    const char* e = std::getenv("DME_CONG_CTAS");
+    const int x = e ? std::atoi(e) : CONG_CTAS_DEFAULT;
+    return x < 1 ? 1 : (x > 64 ? 64 : x);
+  }();
+  return v;
+}
 __global__ void __launch_bounds__(512) gram_congruence_kernel(const double* __restrict__ Gh,
                                                               int64_t ldh, int q, int m, int kp,
                                                               const double* __restrict__ Tm,
@@ -559,7 +569,7 @@ __global__ void __launch_bounds__(512) gram_congruence_kernel(const double* __re
 
 size_t gram_congruence_smem(int q, int m, int kp, int r) {
   const int rows = q + m + kp;
-  const int ctas = std::max(1, std::min(CONG_CTAS, r));
+  const int ctas = std::max(1, std::min(cong_ctas(), r));
   const int njmax = (r + ctas - 1) / ctas;
   return sizeof(double) * ((size_t)rows * kp + (size_t)kp * r + (size_t)rows * njmax);
 }
@@ -567,7 +577,7 @@ size_t gram_congruence_smem(int q, int m, int kp, int r) {
 void gram_congruence(const double* Gh, int64_t ldh, int q, int m, int kp, const double* Tm,
                      int64_t ldt, int r, double* G, int64_t ldg, cudaStream_t st) {
   if (q + r <= 0) return;
-  const int ctas = std::max(1, std::min(CONG_CTAS, r));
+  const int ctas = std::max(1, std::min(cong_ctas(), r));
   const size_t smem = gram_congruence_smem(q, m, kp, r);
   static std::mutex attr_mu;
   static uint64_t attr_mask = 0;

@@ -4,7 +4,7 @@ P=paper_1805_08990_b200
 for c in ${CFGS:-1 2 5}; do
 for rep in 1 2; do
 for v in "$@"; do
-  unset DME_LIB DME_MSEC_P DME_TRI_THREADS DME_VEC_CTAS DME_CB_HOUSEHOLDER DME_CB_SMEM DME_NO_PROJ_GRAM
+  for e in $(env | grep -o '^DME_[A-Z_0-9]*'); do unset $e; done
   case $v in cur) ;; env:*) export ${v#env:} ;; *) export DME_LIB=$PWD/$P/$v ;; esac
   timeout 300 python bench.py --config $c --no-cpu --no-variant --no-e2e --no-sparse --no-pade > gpurun_out/q.json 2> gpurun_out/q.err
   python -c "
