@@ -202,6 +202,29 @@ def test_compress_eigen_paths(dme, case):
         assert s.stats()["eig_fallbacks"] == f0
 
 
+def test_compress_fallback_with_tail(dme):
+    """Refined compression (G7') whose first eigen pass falls back to Jacobi (an exactly
+    degenerate leading cluster) while a tail below 1e-11 theta_max remains: the complement basis
+    queued on the device rank must turn into a no-op and be redone with the host's kb; P against
+    the oracle's SVD + diagonalisation at tol 1e-16."""
+    prob = make_config(2, nx=14)
+    n = prob.n
+    rng = np.random.default_rng(11)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, 60)))
+    head = Q[:, :40] * np.repeat([1.0, 0.5, 0.25, 0.125], 10)[None, :]
+    tail = Q[:, 40:] * np.logspace(-6.5, -9.5, 20)[None, :]   # theta 1e-13 .. 1e-19
+    L = np.hstack([head, tail]) @ np.linalg.qr(rng.standard_normal((60, 60)))[0]  # mixed columns
+    s = _solver(dme, prob, 5e-3)
+    f0 = s.stats()["eig_fallbacks"]
+    s.debug_set_factor(L)
+    s.debug_apply("compress", 0.0)
+    Lg, Dg = s.get_factor()
+    Lo, Do = lowrank.column_compression(L, np.eye(L.shape[1]), 1e-16)
+    assert s.stats()["eig_fallbacks"] >= f0 + 1
+    assert lowrank.rel_diff(Lg, Dg, Lo, Do) <= 1e-13
+    assert abs(Lg.shape[1] - Lo.shape[1]) <= 2, (Lg.shape[1], Lo.shape[1])
+
+
 @pytest.mark.parametrize("comp", ["F12F3", "F1F2F3"])
 def test_fsal_matches_unmerged(dme, comp):
     """First-same-as-last merging inside one split_step call equals the sub-step-by-sub-step run."""
