@@ -143,6 +143,7 @@ struct dme_ctx {
   double *Zs = nullptr, *Gs = nullptr, *Us = nullptr, *Ts = nullptr;  // refined compression: Zc U, its Gram, U, tail eigenvectors
   bool refine = true;      // options.compression == DME_COMPRESS_REFINED
   bool no_proj_gram = false;  // DME_NO_PROJ_GRAM: unfused Zs = Zc U + Gram (A/B measurement knob)
+  bool no_fused_fin = false;  // DME_NO_FUSED_FIN: the tail pass's FIN kernel instead of the fused check
   double tol_scale = 1.0;  // intermediate quadrature-ladder compressions run at trunc_tol * LADDER_TOL
   double last_st[5] = {0, 0, 0, 0, 0};  // stats of the last small-kernel pass read by the host
   cudaEvent_t ev_zc = nullptr, ev_tm = nullptr;
@@ -445,6 +446,7 @@ void fill_dims(dme_ctx* c, const dme_problem* pr, const dme_options* o) {
   c->fsal = o->no_fsal == 0;
   c->refine = o->compression == DME_COMPRESS_REFINED;
   c->no_proj_gram = std::getenv("DME_NO_PROJ_GRAM") != nullptr;
+  c->no_fused_fin = std::getenv("DME_NO_FUSED_FIN") != nullptr;
   c->sparse = pr->A == nullptr && pr->A_rowptr != nullptr;
   if (c->sparse) {
     std::string err;
@@ -992,6 +994,12 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
     b.Tm = c->Ts;
     if (b.map) b.map_seq = ++c->map_seq;
     bool fast2 = false;
+    // split tail pass: no FIN kernel; the tail assembly checks, publishes and assembles in one launch
+    const int ks_bound0 = std::min<int>(b.cap, (int)s);
+    const bool fin_fused = !c->no_fused_fin && s >= EIG_SPLIT_MIN && s <= FAST_K_MAX && !c->force_jacobi &&
+                           tail_assemble_smem((int)k, (int)c->m, (int)s, (int)kb, ks_bound0) <=
+                               (size_t)SMALL_SMEM_MAX;
+    b.skip_fin = fin_fused ? 1 : 0;
     launch_eig(c, b, fast2);
     // the tail assembly (+ T3) is queued right behind the eigen pass and reads ks on the device,
     // so the critical stream does not idle through this host round trip; a Jacobi fallback of the
@@ -1004,7 +1012,8 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
       t.k = (int)k;
       t.t3 = cp.t3 ? 1 : 0;
       ProfScope ps(c, PROF_SMALL);
-      tail_assemble_t3(t, c->Us, KMAX, (int)s, c->Ts, KMAX, (int)kb, ks_bound, c->st, c->r_dev);
+      tail_assemble_t3(t, c->Us, KMAX, (int)s, c->Ts, KMAX, (int)kb, ks_bound, c->st, c->r_dev,
+                       fin_fused ? &b : nullptr);
     }
     const int64_t pubs = c->stats.eig_fallbacks;
     ks = eig_finish(c, b, fast2);

@@ -23,21 +23,6 @@ namespace {
 
 using namespace eigk;
 
-// global scratch layout (doubles)
-struct EsLayout {
-  static constexpr int HDR = 16;
-  double* base;
-  int KM;  // capacity (SMALL_K_MAX)
-  __host__ __device__ double* hdr() const { return base; }
-  __host__ __device__ double* d() const { return base + HDR; }
-  __host__ __device__ double* e() const { return base + HDR + KM; }
-  __host__ __device__ double* e2() const { return base + HDR + 2 * KM; }
-  __host__ __device__ double* tau() const { return base + HDR + 3 * KM; }
-  __host__ __device__ double* lam() const { return base + HDR + 4 * KM; }  // KM + 1
-  __host__ __device__ double* refl() const { return base + HDR + 5 * KM + 8; }  // k x ld
-  __host__ __device__ double* dp() const { return refl() + (size_t)KM * (KM | 1); }  // KM x KM
-  __host__ __device__ double* dm() const { return dp() + (size_t)KM * KM; }
-};
 
 // NTH threads (512; DME_TRI_THREADS = 256 or 128 for k <= 96: A/B of the per-step latency)
 template <int FK, int NTH>
@@ -654,6 +639,7 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
   const size_t fsmem = FK <= 96 ? sizeof(double) * ((size_t)a.k * (a.k | 1) + 2 * (size_t)a.k * SMALL_M_MAX +
                                                   (size_t)a.k * SMALL_M_MAX)
                                  : smem;
+  if (a.skip_fin) return;  // (the tail assembly does FIN's work: small.cu, tail_assemble_t3)
   launch_pdl(eig_fin_kernel<FK>, dim3(1), dim3(ENT), fsmem > smem ? fsmem : smem, st, a);
   DME_KCHECK();
 }

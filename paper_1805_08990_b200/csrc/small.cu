@@ -516,10 +516,25 @@ __global__ void tail_product_kernel(double* Tm, int64_t ldt, const double* __res
 // the Riccati flow T3 on the whole Tm (k x (kb + ks)) when a.t3 is set.
 __global__ void __launch_bounds__(NT) tail_assemble_kernel(SmallArgs a, const double* __restrict__ U,
                                                            int64_t ldu, int s, const double* __restrict__ V,
-                                                           int64_t ldv, int kb, int ks, const int* ks_dev) {
+                                                           int64_t ldv, int kb, int ks, const int* ks_dev,
+                                                           SmallArgs fin, int has_fin) {
   pdl_wait();
   extern __shared__ double S[];
-  if (ks_dev) {  // the tail rank published by the preceding eigen pass (< 0: it fell back to Jacobi)
+  __shared__ double flam[FAST_K_MAX + 1], fslam[FAST_K_MAX + 1], fred[NT / 32];
+  __shared__ int f_bad;
+  double fscale = 0.0, ftmax = 0.0;
+  if (has_fin) {  // the split eigen pass of the tail ran without FIN: its rank from the scratch header
+    const EsLayout es{fin.Es, SMALL_K_MAX};
+    const double* h = es.hdr();
+    fscale = h[0];
+    ftmax = h[3];
+    ks = (int)h[4];
+    const int nr = ks < fin.k ? ks + 1 : ks;
+    for (int i = threadIdx.x; i < nr; i += NT) {
+      flam[i] = es.lam()[i];
+      fslam[i] = sqrt(fabs(flam[i]));
+    }
+  } else if (ks_dev) {  // the tail rank published by the preceding eigen pass (< 0: it fell back to Jacobi)
     ks = *ks_dev;
     if (ks < 0) return;
   }
@@ -543,6 +558,46 @@ __global__ void __launch_bounds__(NT) tail_assemble_kernel(SmallArgs a, const do
   for (int c = warp; c < ks; c += NWP)
     for (int i = lane; i < s; i += 32) Vs[i + c * s] = V[i + (size_t)c * ldv];
   __syncthreads();
+  if (has_fin) {
+    // FIN's work for the tail pass (eig_split.cu, eig_fin_kernel): weighted orthogonality of the ks
+    // unit vectors V (|V^T V - I|, off-diagonal entries weighted by sqrt(lam_i lam_j) / lam_0),
+    // stats, then the rank (or -1: the caller falls back to Jacobi and assembles again)
+    double mx = 0.0;
+    const int np = ks * (ks + 1) / 2;
+    for (int e = threadIdx.x; e < np; e += NT) {
+      int c2 = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((c2 + 1) * (c2 + 2) / 2 <= e) ++c2;
+      while (c2 * (c2 + 1) / 2 > e) --c2;
+      const int c1 = e - c2 * (c2 + 1) / 2;
+      const double* v1 = Vs + (size_t)c1 * s;
+      const double* v2 = Vs + (size_t)c2 * s;
+      double d0 = 0.0, d1 = 0.0;
+      int i = 0;
+      for (; i + 1 < s; i += 2) { d0 = fma(v1[i], v2[i], d0); d1 = fma(v1[i + 1], v2[i + 1], d1); }
+      if (i < s) d0 = fma(v1[i], v2[i], d0);
+      const double w = (c1 == c2) ? 1.0 : fslam[c1] * fslam[c2] / fmax(fabs(flam[0]), 1e-300);
+      mx = fmax(mx, fabs((d0 + d1) - (c1 == c2 ? 1.0 : 0.0)) * w);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) fred[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m2 = 0.0;
+      for (int w = 0; w < NT / 32; ++w) m2 = fmax(m2, fred[w]);
+      f_bad = !(m2 <= fin.orth_tol);  // NaN-safe
+      if (fin.stats) {
+        fin.stats[0] = (double)ks;
+        fin.stats[1] = ftmax * fscale;
+        fin.stats[2] = (ks < fin.k && ftmax > 0.0) ? fabs(flam[ks]) / ftmax : 0.0;
+        fin.stats[3] = f_bad ? 1.0 : 0.0;
+        fin.stats[4] = m2;
+      }
+      publish_rank(fin, f_bad ? -1 : ks);
+    }
+    __syncthreads();
+    if (f_bad) return;
+  }
   for (int c = warp; c < ks; c += NWP)
     for (int i = lane; i < k; i += 32) {
       double acc = 0.0;
@@ -607,14 +662,14 @@ size_t tail_assemble_smem(int k, int m, int s, int kb, int ks) {
 }
 
 void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, const double* V,
-                      int64_t ldv, int kb, int ks, cudaStream_t st, const int* ks_dev) {
+                      int64_t ldv, int kb, int ks, cudaStream_t st, const int* ks_dev, const SmallArgs* fin) {
   if (a.m > SMALL_M_MAX) throw std::runtime_error("tail_assemble_t3: m exceeds SMALL_M_MAX");
   const int k = a.k, r = kb + ks;
   size_t need = sizeof(double) * ((size_t)k * r + (size_t)k * a.m + (size_t)k * s + (size_t)s * ks);
   const size_t t3s = sizeof(double) * ((size_t)k * r + (size_t)k * a.m + 2 * SMALL_K_MAX * SMALL_M_MAX);
   if (need < t3s) need = t3s;
   if (need > (size_t)SMALL_SMEM_MAX) {  // wide systems: the product in global memory, then T3 alone
-    if (ks_dev) throw std::runtime_error("tail_assemble_t3: device rank needs the shared-memory path");
+    if (ks_dev || fin) throw std::runtime_error("tail_assemble_t3: device rank needs the shared-memory path");
     if (ks > 0) {
       tail_product_kernel<<<(k * ks + 255) / 256, 256, 0, st>>>(a.Tm, a.ldt, U, ldu, s, V, ldv, k, kb, ks);
       DME_KCHECK();
@@ -628,7 +683,9 @@ void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, c
     DME_CUDA(cudaFuncSetAttribute(tail_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SMALL_SMEM_MAX));
   });
-  launch_pdl(tail_assemble_kernel, dim3(1), dim3(NT), need, st, a, U, ldu, s, V, ldv, kb, ks, ks_dev);
+  const SmallArgs none{};
+  launch_pdl(tail_assemble_kernel, dim3(1), dim3(NT), need, st, a, U, ldu, s, V, ldv, kb, ks, ks_dev,
+             fin ? *fin : none, fin ? 1 : 0);
   DME_KCHECK();
 }
 

@@ -50,6 +50,7 @@ struct SmallArgs {
   HostMap* map = nullptr;    // device alias of the host-mapped record (nullptr: r_out only)
   int map_seq = 0;           // sequence number this launch publishes
   int msec_p = 128;          // split path: multisection probes per eigenvalue (cap)
+  int skip_fin = 0;          // split path: no FIN kernel (the caller's tail assembly checks and publishes)
 };
 
 void compress_t3(const SmallArgs& a, cudaStream_t st);  // Jacobi (any k <= SMALL_K_MAX)
@@ -68,8 +69,28 @@ bool complement_basis_dev(const double* W, int64_t ldw, int k, const int* kb_dev
 // ks_dev != nullptr: ks is read on the device (the rank the preceding eigen pass published; a
 // negative value -- Jacobi fallback pending -- makes the kernel a no-op); ks is then an upper bound
 size_t tail_assemble_smem(int k, int m, int s, int kb, int ks);
+// fin != nullptr (the split eigen pass of the tail launched with skip_fin): the kernel first does
+// that pass's FIN work -- weighted orthogonality check of V, stats, publish of ks or -1 -- with ks
+// read from the pass's scratch header; ks is then an upper bound
 void tail_assemble_t3(const SmallArgs& a, const double* U, int64_t ldu, int s, const double* V,
-                      int64_t ldv, int kb, int ks, cudaStream_t st, const int* ks_dev = nullptr);
+                      int64_t ldv, int kb, int ks, cudaStream_t st, const int* ks_dev = nullptr,
+                      const SmallArgs* fin = nullptr);
+
+// global scratch of the split eigen path (doubles): header, tridiagonal, eigenvalues, reflectors
+struct EsLayout {
+  static constexpr int HDR = 16;
+  double* base;
+  int KM;  // capacity (SMALL_K_MAX)
+  __host__ __device__ double* hdr() const { return base; }
+  __host__ __device__ double* d() const { return base + HDR; }
+  __host__ __device__ double* e() const { return base + HDR + KM; }
+  __host__ __device__ double* e2() const { return base + HDR + 2 * KM; }
+  __host__ __device__ double* tau() const { return base + HDR + 3 * KM; }
+  __host__ __device__ double* lam() const { return base + HDR + 4 * KM; }  // KM + 1
+  __host__ __device__ double* refl() const { return base + HDR + 5 * KM + 8; }  // k x ld
+  __host__ __device__ double* dp() const { return refl() + (size_t)KM * (KM | 1); }  // KM x KM
+  __host__ __device__ double* dm() const { return dp() + (size_t)KM * KM; }
+};
 // Pp = I - W W^T (k x k), W: k x kb (the kept leading eigenvectors of the first pass)
 void complement_projector(const double* W, int64_t ldw, int k, int kb, double* Pp, int64_t ldp,
                           cudaStream_t st);
