@@ -800,6 +800,7 @@ void eact(dme_ctx* c, bool full, const double* X, int64_t k, double* out, int64_
 struct Compression {
   SmallArgs a;
   bool fast = false, do_compress = true, t3 = false, refine = false;
+  bool fin_in_cb = false;  // refined, split first pass: FIN's work done by the queued complement
   double tau3 = 0.0;
   double* Zc = nullptr;
   int64_t k = 0;
@@ -880,6 +881,11 @@ void compress_launch(dme_ctx* c, double* Zc, int64_t k, bool t3, double tau3, bo
     a.map = c->hmap_dev;
     a.map_seq = ++c->map_seq;
   }
+  // refined + split first pass (t3 = 0): no FIN kernel, the complement basis queued right behind
+  // the pass checks, publishes kb and builds U in one launch (compress_finish)
+  cp.fin_in_cb = cp.refine && !c->no_fused_fin && k >= EIG_SPLIT_MIN && k <= FAST_K_MAX &&
+                 !c->force_jacobi && complement_dev_available((int)k);
+  a.skip_fin = cp.fin_in_cb ? 1 : 0;
   launch_eig(c, a, cp.fast);
 }
 
@@ -940,7 +946,9 @@ int64_t compress_finish(dme_ctx* c, Compression& cp, cudaEvent_t zc_ready = null
   bool cb_queued = false;
   if (cp.refine && cp.fast) {
     ProfScope ps(c, PROF_SMALL);
-    cb_queued = complement_basis_dev(cp.a.Tm, KMAX, (int)cp.k, c->r_dev, c->Us, KMAX, c->st);
+    cb_queued = complement_basis_dev(cp.a.Tm, KMAX, (int)cp.k, c->r_dev, c->Us, KMAX, c->st,
+                                     cp.fin_in_cb ? &cp.a : nullptr);
+    DME_REQUIRE(cb_queued || !cp.fin_in_cb, DME_ERR_CUDA, "first pass without FIN needs the complement");
   }
   const int64_t fb0 = c->stats.eig_fallbacks;
   const int64_t kb = eig_finish(c, cp.a, cp.fast);

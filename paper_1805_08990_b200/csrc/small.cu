@@ -424,9 +424,24 @@ constexpr int CLU_KMAX = 96;
 
 __global__ void __launch_bounds__(NT) complement_gj_kernel(const double* __restrict__ W, int64_t ldw, int k,
                                                            int kb, double* __restrict__ U, int64_t ldu,
-                                                           const int* __restrict__ kb_dev) {
+                                                           const int* __restrict__ kb_dev, SmallArgs fin,
+                                                           int has_fin) {
   pdl_wait();
-  if (kb_dev) {  // (speculative launch: the rank the first eigen pass published; < 0 = fallback)
+  __shared__ double flam[CLU_KMAX + 1], fslam[CLU_KMAX + 1], fred[NT / 32];
+  __shared__ int f_bad;
+  double fscale = 0.0, ftmax = 0.0;
+  if (has_fin) {  // the first eigen pass ran without FIN: its rank from the scratch header
+    const EsLayout es{fin.Es, SMALL_K_MAX};
+    const double* h = es.hdr();
+    fscale = h[0];
+    ftmax = h[3];
+    kb = (int)h[4];
+    const int nr = kb < k ? kb + 1 : kb;
+    for (int i = threadIdx.x; i < nr; i += NT) {
+      flam[i] = es.lam()[i];
+      fslam[i] = sqrt(fabs(flam[i]));
+    }
+  } else if (kb_dev) {  // (speculative launch: the rank the first eigen pass published; < 0 = fallback)
     kb = *kb_dev;
     if (kb < 0 || kb >= k) return;
   }
@@ -442,6 +457,46 @@ __global__ void __launch_bounds__(NT) complement_gj_kernel(const double* __restr
       A[c + i * lda] = w;
     }
   __syncthreads();
+  if (has_fin) {
+    // FIN's work for the first pass (eig_split.cu, eig_fin_kernel, t3 = 0): weighted orthogonality
+    // of the kb unit vectors W, stats, then the rank (or -1: the caller falls back to Jacobi and
+    // queues the complement again)
+    double mx = 0.0;
+    const int np = kb * (kb + 1) / 2;
+    for (int e = tid; e < np; e += NT) {
+      int c2 = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((c2 + 1) * (c2 + 2) / 2 <= e) ++c2;
+      while (c2 * (c2 + 1) / 2 > e) --c2;
+      const int c1 = e - c2 * (c2 + 1) / 2;
+      const double* v1 = Ws + (size_t)c1 * k;
+      const double* v2 = Ws + (size_t)c2 * k;
+      double d0 = 0.0, d1 = 0.0;
+      int i = 0;
+      for (; i + 1 < k; i += 2) { d0 = fma(v1[i], v2[i], d0); d1 = fma(v1[i + 1], v2[i + 1], d1); }
+      if (i < k) d0 = fma(v1[i], v2[i], d0);
+      const double w = (c1 == c2) ? 1.0 : fslam[c1] * fslam[c2] / fmax(fabs(flam[0]), 1e-300);
+      mx = fmax(mx, fabs((d0 + d1) - (c1 == c2 ? 1.0 : 0.0)) * w);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) fred[tid >> 5] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double m2 = 0.0;
+      for (int w = 0; w < NT / 32; ++w) m2 = fmax(m2, fred[w]);
+      f_bad = !(m2 <= fin.orth_tol);  // NaN-safe
+      if (fin.stats) {
+        fin.stats[0] = (double)kb;
+        fin.stats[1] = ftmax * fscale;
+        fin.stats[2] = (kb < k && ftmax > 0.0) ? fabs(flam[kb]) / ftmax : 0.0;
+        fin.stats[3] = f_bad ? 1.0 : 0.0;
+        fin.stats[4] = m2;
+      }
+      publish_rank(fin, f_bad ? -1 : kb);
+    }
+    __syncthreads();
+    if (f_bad || kb >= k) return;
+  }
   for (int j = 0; j < kb; ++j) {
     const double dj = A[j + j * lda];
     const double sj = dj >= 0.0 ? -1.0 : 1.0;
@@ -635,19 +690,23 @@ void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, in
   static const bool old_cb = std::getenv("DME_CB_HOUSEHOLDER") != nullptr;  // A/B knob
   if (k <= CLU_KMAX && !old_cb)
     launch_pdl(complement_gj_kernel, dim3(1), dim3(NT), complement_gj_smem(k, kb), st, W, ldw, k, kb, U, ldu,
-               (const int*)nullptr);
+               (const int*)nullptr, SmallArgs{}, 0);
   else if (k <= 96) complement_basis_kernel<3, 3><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   else complement_basis_kernel<5, 5><<<1, NT, smem, st>>>(W, ldw, k, kb, U, ldu);
   DME_KCHECK();
 }
 
-bool complement_basis_dev(const double* W, int64_t ldw, int k, const int* kb_dev, double* U, int64_t ldu,
-                          cudaStream_t st) {
+bool complement_dev_available(int k) {
   static const bool old_cb = std::getenv("DME_CB_HOUSEHOLDER") != nullptr;
-  if (k > CLU_KMAX || old_cb) return false;
+  return k <= CLU_KMAX && !old_cb;
+}
+
+bool complement_basis_dev(const double* W, int64_t ldw, int k, const int* kb_dev, double* U, int64_t ldu,
+                          cudaStream_t st, const SmallArgs* fin) {
+  if (!complement_dev_available(k)) return false;
   complement_basis(W, ldw, k, 0, U, 0, nullptr, true);  // (attributes only)
   launch_pdl(complement_gj_kernel, dim3(1), dim3(NT), complement_gj_smem(k, k), st, W, ldw, k, 0, U, ldu,
-             kb_dev);
+             kb_dev, fin ? *fin : SmallArgs{}, fin ? 1 : 0);
   DME_KCHECK();
   return true;
 }

@@ -64,7 +64,10 @@ void complement_basis(const double* W, int64_t ldw, int k, int kb, double* U, in
 // The same with kb read on the device (*kb_dev: the rank the first eigen pass published; < 0 makes
 // it a no-op), so it can be queued before the host has seen kb; false: not available (k > 96)
 bool complement_basis_dev(const double* W, int64_t ldw, int k, const int* kb_dev, double* U, int64_t ldu,
-                          cudaStream_t st);
+                          cudaStream_t st, const struct SmallArgs* fin = nullptr);
+bool complement_dev_available(int k);  // complement_basis_dev's kernel applies (k <= 96)
+// fin != nullptr: the split first pass was launched with skip_fin; the kernel does its FIN work
+// (check, stats, publish of kb or -1) and reads kb from the pass's scratch header
 // a.Tm[:, kb:kb+ks] = U V (U: k x s, V: s x ks), then T3 on a.Tm (k x (kb + ks)) if a.t3.
 // ks_dev != nullptr: ks is read on the device (the rank the preceding eigen pass published; a
 // negative value -- Jacobi fallback pending -- makes the kernel a no-op); ks is then an upper bound
