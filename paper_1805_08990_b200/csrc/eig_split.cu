@@ -617,10 +617,13 @@ void launch_split(const SmallArgs& a, cudaStream_t st) {
     DME_CUDA(cudaFuncSetAttribute(eig_vec_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     DME_CUDA(cudaFuncSetAttribute(eig_fin_kernel<FK>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   });
-  static const int tri_nth = [] {
+  static const int tri_env = [] {
     const char* e = std::getenv("DME_TRI_THREADS");
-    return e ? std::atoi(e) : 512;
+    return e ? std::atoi(e) : 0;
   }();
+  // 512 threads for the first pass (k ~ 92: 184 us against 188 at 256), 256 for k <= 64 (the tail
+  // pass, s ~ 57: 79 us against 82 at 512)
+  const int tri_nth = tri_env ? tri_env : (a.k <= 64 ? 256 : 512);
   if (FK <= 96 && tri_nth == 128) launch_pdl(eig_tri_kernel<FK, 128>, dim3(1), dim3(128), smem, st, a);
   else if (FK <= 96 && tri_nth == 256) launch_pdl(eig_tri_kernel<FK, 256>, dim3(1), dim3(256), smem, st, a);
   else launch_pdl(eig_tri_kernel<FK, 512>, dim3(1), dim3(512), smem, st, a);
